@@ -1,0 +1,195 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+ctypes wrapper of the plain serial C oracle (oracle/*.c), written from the paper
+(PAPER.md:653-681 SR4 count-sort rounds; Algorithm 1 GSD).
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
+reference leg may import this package.  The product path
+(paper_1808_10292_b200/) never does, and shares no code with it.
+
+Parity status: SR-b, histograms and the GSD concatenated
+output are pinned (library sort, brute force, masked stable sort, bincount);
+GSD's per-rank partition is pinned only by the SPEC.md:290 hand trace and the
+balance bound — beyond those it is "parity unpinned" by the paper, which prints
+no partition.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRCS = [os.path.join(_HERE, f) for f in ("sr.c", "gsd.c", "verify.c")]
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """gcc -O2 (generic x86-64, so the .so also runs on the GPU box's host)."""
+    newest = max(os.path.getmtime(p) for p in _SRCS + [os.path.join(_HERE, "oracle.h")])
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < newest:
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-fopenmp",
+                               "-o", tmp] + _SRCS)
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB_PATH)
+        vp, sz, i32, u64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint64
+        for name in ("or_sr_u32", "or_sr_u64"):
+            getattr(L, name).argtypes = [vp, sz, i32, i32]
+            getattr(L, name).restype = i32
+        L.or_sr_pairs_u64_u32.argtypes = [vp, vp, sz, i32, i32]
+        L.or_sr_pairs_u64_u32.restype = i32
+        for name in ("or_hist_u32", "or_hist_u64"):
+            getattr(L, name).argtypes = [vp, sz, i32, vp]
+            getattr(L, name).restype = i32
+        L.or_gsd_u64.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, sz, vp, vp, vp]
+        L.or_gsd_u64.restype = i32
+        L.or_gsd_u32.argtypes = [i32, i32, i32, vp, vp, vp, sz, vp, vp, vp]
+        L.or_gsd_u32.restype = i32
+        for name in ("or_is_nondecreasing_u32", "or_is_nondecreasing_u64"):
+            getattr(L, name).argtypes = [vp, sz]
+            getattr(L, name).restype = i32
+        for name in ("or_multiset_hash_u32", "or_multiset_hash_u64"):
+            getattr(L, name).argtypes = [vp, sz, vp]
+            getattr(L, name).restype = None
+        L.or_multiset_hash_pairs_u64_u32.argtypes = [vp, vp, sz, vp]
+        L.or_multiset_hash_pairs_u64_u32.restype = None
+        L.or_pairs_stable_u64_u32.argtypes = [vp, vp, sz]
+        L.or_pairs_stable_u64_u32.restype = i32
+        L.or_check_order_stats_u32.argtypes = [vp, sz, vp, vp, sz]
+        L.or_check_order_stats_u32.restype = sz
+        _lib = L
+    return _lib
+
+
+def _c(a, dtype):
+    a = np.ascontiguousarray(a, dtype=dtype)
+    return a
+
+
+# ---- SR-b ------------------------------------------------
+
+def sr(keys: np.ndarray, b: int = 8, rounds: int = -1, vals: np.ndarray | None = None):
+    """Serial LSD radix sort by count-sort rounds; returns a sorted copy (and vals).
+
+    `rounds` >= 0 stops after that many rounds (the intermediate array after
+    round t is what a GPU pass t must produce)."""
+    k = np.array(keys, copy=True)
+    L = lib()
+    if vals is not None:
+        assert k.dtype == np.uint64
+        v = np.array(vals, dtype=np.uint32, copy=True)
+        rc = L.or_sr_pairs_u64_u32(k.ctypes.data, v.ctypes.data, k.size, b, rounds)
+        if rc:
+            raise ValueError("or_sr_pairs_u64_u32 failed")
+        return k, v
+    if k.dtype == np.uint32:
+        rc = L.or_sr_u32(k.ctypes.data, k.size, b, rounds)
+    elif k.dtype == np.uint64:
+        rc = L.or_sr_u64(k.ctypes.data, k.size, b, rounds)
+    else:
+        raise TypeError(k.dtype)
+    if rc:
+        raise ValueError(f"or_sr failed (b={b})")
+    return k
+
+
+def hist(keys: np.ndarray, b: int = 8) -> np.ndarray:
+    """All rounds' digit counts: shape (keybits/b, 2^b)."""
+    k = np.ascontiguousarray(keys)
+    P = k.dtype.itemsize * 8 // b
+    out = np.zeros((P, 1 << b), dtype=np.uint64)
+    fn = lib().or_hist_u32 if k.dtype == np.uint32 else lib().or_hist_u64
+    if fn(k.ctypes.data, k.size, b, out.ctypes.data):
+        raise ValueError("or_hist failed")
+    return out
+
+
+# ---- GSD ---------------------------------------------------
+
+def gsd(shards, r: int, b: int = 8, vals=None, cap: int | None = None):
+    """Simulate GSD over p = len(shards) blocks.
+
+    Returns dict(Y=[...], Yv=[...] or None, splitters=(p-1,3) array, counts=(p,p))."""
+    p = len(shards)
+    is32 = shards[0].dtype == np.uint32
+    dt = np.uint32 if is32 else np.uint64
+    ks = [np.ascontiguousarray(s, dtype=dt) for s in shards]
+    N = np.array([s.size for s in ks], dtype=np.uint64)
+    if cap is None:
+        cap = int(N.sum())
+    Y = [np.empty(max(cap, 1), dtype=dt) for _ in range(p)]
+    kp = (ctypes.c_void_p * p)(*[s.ctypes.data for s in ks])
+    yp = (ctypes.c_void_p * p)(*[y.ctypes.data for y in Y])
+    ylen = np.zeros(p, dtype=np.uint64)
+    spl = np.zeros((max(p - 1, 1), 3), dtype=np.uint64)
+    counts = np.zeros((p, p), dtype=np.uint64)
+    L = lib()
+    Yv = None
+    if is32:
+        assert vals is None
+        rc = L.or_gsd_u32(p, r, b, kp, N.ctypes.data, yp, cap, ylen.ctypes.data,
+                          spl.ctypes.data, counts.ctypes.data)
+    else:
+        vp_ = None
+        if vals is not None:
+            vs = [np.ascontiguousarray(v, dtype=np.uint32) for v in vals]
+            Yv = [np.empty(max(cap, 1), dtype=np.uint32) for _ in range(p)]
+            vp_ = (ctypes.c_void_p * p)(*[v.ctypes.data for v in vs])
+            yvp = (ctypes.c_void_p * p)(*[y.ctypes.data for y in Yv])
+        rc = L.or_gsd_u64(p, r, b, kp, vp_, N.ctypes.data, yp,
+                          yvp if vals is not None else None, cap, ylen.ctypes.data,
+                          spl.ctypes.data, counts.ctypes.data)
+    if rc == -2:
+        raise OverflowError("GSD output exceeds capacity")
+    if rc:
+        raise ValueError("or_gsd failed")
+    out = dict(Y=[Y[j][: int(ylen[j])] for j in range(p)], splitters=spl[: p - 1], counts=counts,
+               Ylen=ylen)
+    out["Yv"] = None if Yv is None else [Yv[j][: int(ylen[j])] for j in range(p)]
+    return out
+
+
+# ---- invariants -------------------------------------------------------------
+
+def is_nondecreasing(a: np.ndarray) -> bool:
+    a = np.ascontiguousarray(a)
+    fn = lib().or_is_nondecreasing_u32 if a.dtype == np.uint32 else lib().or_is_nondecreasing_u64
+    return bool(fn(a.ctypes.data, a.size))
+
+
+def multiset_hash(a: np.ndarray, vals: np.ndarray | None = None) -> tuple:
+    a = np.ascontiguousarray(a)
+    out = np.zeros(3, dtype=np.uint64)
+    if vals is not None:
+        v = np.ascontiguousarray(vals, dtype=np.uint32)
+        lib().or_multiset_hash_pairs_u64_u32(a.ctypes.data, v.ctypes.data, a.size, out.ctypes.data)
+    elif a.dtype == np.uint32:
+        lib().or_multiset_hash_u32(a.ctypes.data, a.size, out.ctypes.data)
+    else:
+        lib().or_multiset_hash_u64(a.ctypes.data, a.size, out.ctypes.data)
+    return tuple(int(x) for x in out)
+
+
+def pairs_stable(k: np.ndarray, v: np.ndarray) -> bool:
+    k = np.ascontiguousarray(k, dtype=np.uint64)
+    v = np.ascontiguousarray(v, dtype=np.uint32)
+    return bool(lib().or_pairs_stable_u64_u32(k.ctypes.data, v.ctypes.data, k.size))
+
+
+def check_order_stats_u32(a: np.ndarray, pos: np.ndarray, val: np.ndarray) -> int:
+    """Number of sampled (pos, val) that are NOT the pos-th smallest of a[]."""
+    a = np.ascontiguousarray(a, dtype=np.uint32)
+    pos = np.ascontiguousarray(pos, dtype=np.uint64)
+    val = np.ascontiguousarray(val, dtype=np.uint32)
+    return int(lib().or_check_order_stats_u32(a.ctypes.data, a.size, pos.ctypes.data,
+                                               val.ctypes.data, pos.size))
