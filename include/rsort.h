@@ -1,0 +1,189 @@
+/*
+ * rsort.h — C ABI of the B200-native radix sort / GSD sample sort library
+ * (paper_1808_10292_b200/librsort.so).
+ *
+ * What it computes (PAPER.md = /root/reference/PAPER.md, Gerbessiotis,
+ * "A study of integer sorting on multicores", arXiv 1808.10292):
+ *
+ *   single GPU (comm == NULL): LSD radix sort of unsigned keys as a sequence of
+ *     stable count-sort passes — digit histogram, exclusive prefix of bucket
+ *     offsets, stable scatter (SR4; PAPER.md:685-714 PR4/PR2).
+ *     digit_bits = 8 is the paper's radix-256 (PR4: 4 passes on u32, 8 on u64);
+ *     digit_bits = 16 is radix-65536 (PR2: 2 passes on u32, 4 on u64).
+ *   multi GPU (comm != NULL): GSD, deterministic regular oversampling sample sort
+ *     (Algorithm 1): local radix sort, regular sample of
+ *     s = r·p composite keys per rank, splitters S_i = T[i·s−1], binary-search
+ *     split, NCCL all-to-all over NVLink, final p-way merge on each rank.
+ *
+ * Result order: ascending unsigned.  Sorts are STABLE: equal keys keep input
+ * order (pairs: the payload travels with its key).  Across ranks a rank's keys
+ * precede equal keys of higher ranks (readings R14-R16).
+ *
+ * Conventions for every entry point:
+ *   - extern "C", plain pointers and sizes; no torch / CUDA types (a `stream`
+ *     is a cudaStream_t passed as void*, NULL = legacy default stream).
+ *   - Pointers named keys/vals/out/ws are DEVICE pointers (cudaMalloc or torch
+ *     CUDA tensors) on the current CUDA device, 16-byte aligned.
+ *   - The caller owns all buffers.  The library never allocates device memory
+ *     on a sort call: scratch comes from `ws` (size from rs_workspace_bytes).
+ *   - Calls are asynchronous on `stream` unless stated; they never abort or
+ *     throw.  Arguments are validated before anything is enqueued, so on
+ *     RS_EINVAL / RS_ECAPACITY the inputs are untouched.  On RS_ECUDA /
+ *     RS_ENCCL buffer contents are undefined (and a comm must be destroyed).
+ *   - rs_last_error() returns a thread-local message for the last failure.
+ *   - n = 0 is a no-op returning RS_OK (a rank with n = 0 still participates
+ *     in a collective call).  n must be < 2^32 per GPU.
+ */
+#ifndef RSORT_H
+#define RSORT_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default) /* only the declarations below are exported */
+#endif
+
+typedef enum {
+    RS_OK = 0,
+    RS_EINVAL = 1,      /* bad argument: digit_bits ∉ {8,16}, NULL with n>0, misaligned,
+                           n >= 2^32, ws too small, collective header mismatch */
+    RS_ECUDA = 2,       /* a CUDA launch / runtime call failed */
+    RS_ENCCL = 3,       /* an NCCL call failed */
+    RS_ENOMEM = 4,      /* host allocation failed (comm creation only) */
+    RS_ECAPACITY = 5    /* multi-GPU: out_cap smaller than |Y_j| */
+} rs_status_t;
+
+const char* rs_status_string(rs_status_t s);
+const char* rs_last_error(void);
+/* library version string, e.g. "rsort-b200 0.1 sm_100a" */
+const char* rs_version(void);
+
+/* ---------------------------------------------------------------- sizing -- */
+
+/* Bytes of device scratch needed by rs_sort_* for this (key, value) width,
+ * local n, digit width and communicator (NULL = single GPU).
+ * key_bytes ∈ {4, 8}; val_bytes ∈ {0, 4}.  Returns 0 on an invalid combination. */
+size_t rs_workspace_bytes(int key_bytes, int val_bytes, size_t n, int digit_bits, void* comm);
+
+/* Multi-GPU: capacity each rank's `out` must have when every rank holds at most
+ * n_local_max keys: ⌊(1 + 1/r)·n_local_max⌋ + p (R18, the Lemma
+ * `balance` bound PAPER.md:891-955 for this reading).  comm NULL → n_local_max. */
+size_t rs_output_capacity(size_t n_local_max, void* comm);
+
+/* ------------------------------------------------------------ single GPU -- */
+/* (comm == NULL in rs_sort_*) — keys/out may alias (in-place).  *n_out = n.     */
+
+/* rs_sort_u32: sort n u32 keys.  keys: input (read; clobbered only if out==keys).
+ * out: n u32 result.  digit_bits ∈ {8, 16}. */
+rs_status_t rs_sort_u32(uint32_t* keys, size_t n, int digit_bits, void* comm,
+                        uint32_t* out, size_t out_cap, size_t* n_out,
+                        void* ws, size_t ws_bytes, void* stream);
+
+/* rs_sort_u64: sort n u64 keys (8 passes at digit_bits 8, 4 at 16). */
+rs_status_t rs_sort_u64(uint64_t* keys, size_t n, int digit_bits, void* comm,
+                        uint64_t* out, size_t out_cap, size_t* n_out,
+                        void* ws, size_t ws_bytes, void* stream);
+
+/* rs_sort_pairs_u64_u32: stable sort of (u64 key, u32 value) pairs stored as
+ * two arrays (SoA).  Values are permuted with their keys; equal keys keep input
+ * order.  out_keys/out_vals may alias keys/vals. */
+rs_status_t rs_sort_pairs_u64_u32(uint64_t* keys, uint32_t* vals, size_t n, int digit_bits,
+                                  void* comm, uint64_t* out_keys, uint32_t* out_vals,
+                                  size_t out_cap, size_t* n_out,
+                                  void* ws, size_t ws_bytes, void* stream);
+
+/* rs_sort_bits: single-GPU core with an explicit bit range: stable sort by
+ * the low `end_bit` bits of the key (digits t = 0 .. ⌈end_bit/b⌉−1, LSD first;
+ * end_bit = keybits is the full sort).  After t+1 passes of radix 2^b the array
+ * is exactly the paper's array after round t — the hook the
+ * per-pass parity tests use.  key_bytes ∈ {4, 8}; vals/out_vals NULL or u32. */
+rs_status_t rs_sort_bits(int key_bytes, void* keys, uint32_t* vals, size_t n, int digit_bits,
+                         int end_bit, void* out_keys, uint32_t* out_vals,
+                         void* ws, size_t ws_bytes, void* stream);
+
+/* rs_digit_histogram: counting step of every pass in ONE read of the keys
+ * ("initial counting process", all rounds at once):
+ * hist[t*2^b + d] = #{i : (key_i >> t·b) & (2^b − 1) = d}, t < keybits/b.
+ * hist: device u32 array of (keybits/b)·2^b entries, overwritten.  Needs
+ * ws of rs_workspace_bytes(key_bytes, 0, n, b, NULL). */
+rs_status_t rs_digit_histogram(int key_bytes, const void* keys, size_t n, int digit_bits,
+                               uint32_t* hist, void* ws, size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------- multi GPU -- */
+
+/* NCCL bootstrap: rank 0 calls rs_get_unique_id, the caller broadcasts the
+ * 128 bytes (e.g. torch.distributed.broadcast_object_list), then every rank
+ * calls rs_comm_create on its own device.  The comm owns an NCCL communicator
+ * and a small pinned host buffer.  Blocking, collective. */
+rs_status_t rs_get_unique_id(void* uid128);
+rs_status_t rs_comm_create(const void* uid128, int nranks, int rank, int cuda_device, void** comm);
+rs_status_t rs_comm_destroy(void* comm);
+/* GSD oversampling factor r (s = r·p samples per rank; default 8, BASELINE
+ * config 4 "oversampling factor 8·p").  Must match on every rank. */
+rs_status_t rs_comm_set_oversampling(void* comm, int r);
+int rs_comm_rank(void* comm);
+int rs_comm_size(void* comm);
+
+/* With comm != NULL, rs_sort_* is the GSD collective: every rank calls it with
+ * the same key/value types, digit_bits and r (checked: RS_EINVAL on all ranks
+ * on a mismatch).  n may differ per rank.  Rank j receives Y_j, the j-th
+ * contiguous slice of the global sorted order, in out[0 .. *n_out).  `keys`
+ * (and vals) are used as scratch (they hold X_j, the locally sorted block, on
+ * return).  The call blocks the host once, on the p×p count exchange; *n_out is
+ * valid on return.  out_cap < |Y_j| → RS_ECAPACITY (on that rank). */
+
+/* ---------------------------------------------------------- GSD emulation -- */
+/* rs_gsd_emulate: GSD over p ranks whose blocks all live on THIS GPU, run rank
+ * by rank in one stream (no NCCL, nothing waits on another rank): the same
+ * kernels and host plan as the multi-GPU path, with device copies standing in
+ * for the all-gathers and the all-to-all.  Used to test the multi-GPU path's
+ * kernels on one GPU.
+ *   keys[k], vals[k] (vals NULL for keys-only), n[k]: the p blocks (scratch).
+ *   out_keys[j], out_vals[j], out_cap: per-rank outputs; n_out[j] = |Y_j|.
+ *   splitters: NULL or host u64[3*(p-1)] receiving (key, rank, pos) of S_i.
+ *   counts:    NULL or host u64[p*p] receiving |X_{k,j}| at [k*p + j].
+ *   ws: rs_gsd_emulate_ws_bytes(key_bytes, val_bytes, p, r, digit_bits,
+ *       max_k n[k], out_cap) bytes.
+ * Blocks the host once (the count exchange), like the multi-GPU call. */
+size_t rs_gsd_emulate_ws_bytes(int key_bytes, int val_bytes, int p, int r, int digit_bits, size_t n_max,
+                               size_t out_cap);
+rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits,
+                           void* const* keys, uint32_t* const* vals, const size_t* n,
+                           void* const* out_keys, uint32_t* const* out_vals, size_t out_cap,
+                           size_t* n_out, uint64_t* splitters, uint64_t* counts,
+                           void* ws, size_t ws_bytes, void* stream);
+
+/* --------------------------------------------------------------- options -- */
+/* Process-wide tuning / test knobs (not needed for normal use):
+ *   "wide_status"    1 = use 64-bit look-back status words at any n (they are
+ *                    used automatically when n >= 2^30, where 30-bit counts
+ *                    could overflow); lets the tests run that path on small n.
+ *   "rank_variant"   in-tile ranking: 0 = ballot peer masks (default), 2 = peer
+ *                    masks by shared-memory atomic OR,
+ *                    1 = match.any.
+ * Returns RS_EINVAL for an unknown name or a negative value. */
+rs_status_t rs_set_option(const char* name, long long value);
+
+/* ---------------------------------------------------------------- timing -- */
+/* Per-kernel device timing for measurement (bench.py): when enabled, every
+ * kernel the library launches is bracketed by CUDA events on its own stream.
+ * rs_timing_query sums the elapsed ms and launch count of kernels whose name
+ * starts with `prefix` (e.g. "onesweep", "hist", "" = all) since the last
+ * rs_timing_reset; it synchronises the recorded events. */
+void rs_timing_enable(int on);
+void rs_timing_reset(void);
+rs_status_t rs_timing_query(const char* prefix, double* total_ms, int* launches);
+/* kernel launches issued by the library since the last rs_timing_reset
+ * (counted whether or not timing is enabled) */
+long long rs_launch_count(void);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* RSORT_H */

@@ -1,0 +1,229 @@
+"""B200-native LSD radix sort (the paper's PR4/PR2 count-sort passes) and GSD
+regular-oversampling sample sort across GPUs — Gerbessiotis, "A study of
+integer sorting on multicores" (arXiv 1808.10292).
+
+The work happens in librsort.so (hand-written sm_100a CUDA + NCCL) behind the C
+ABI of include/rsort.h.  This module only marshals torch tensors (device memory,
+the current stream, process groups) into those calls; it never computes on the
+CPU and has no fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _abi
+from ._abi import RSortError, check, lib
+
+__all__ = ["sort", "sort_pairs", "sort_bits", "digit_histogram", "workspace_bytes", "Comm", "gsd_emulate",
+           "RSortError", "lib", "rs_sort_u32", "rs_sort_u64", "rs_sort_pairs_u64_u32"]
+
+_KEY_BYTES = {torch.uint32: 4, torch.int32: 4, torch.uint64: 8, torch.int64: 8}
+
+
+def _stream(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _ptr(t: torch.Tensor | None) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def _check_tensor(t: torch.Tensor, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU path)")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+def workspace_bytes(key_bytes: int, val_bytes: int, n: int, digit_bits: int = 8, comm: "Comm | None" = None) -> int:
+    return lib().rs_workspace_bytes(key_bytes, val_bytes, n, digit_bits, comm.handle if comm else None)
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor:
+    return torch.empty(max(nbytes, 16), dtype=torch.uint8, device=device)
+
+
+# ---- C-ABI names, re-exported -------------------------------------------------
+def rs_sort_u32(*a):
+    return lib().rs_sort_u32(*a)
+
+
+def rs_sort_u64(*a):
+    return lib().rs_sort_u64(*a)
+
+
+def rs_sort_pairs_u64_u32(*a):
+    return lib().rs_sort_pairs_u64_u32(*a)
+
+
+# ---- tensor API -----------------------------------------------------------------
+def sort(keys: torch.Tensor, digit_bits: int = 8, comm: "Comm | None" = None, out: torch.Tensor | None = None,
+         ws: torch.Tensor | None = None, out_cap: int | None = None, stream=None) -> torch.Tensor:
+    """Sort a 1-D CUDA tensor of uint32/uint64 keys (unsigned order).
+
+    Single GPU: returns `out` (default: in place in `keys`).  With `comm`, runs
+    GSD across ranks and returns this rank's slice Y_j (keys is scratch)."""
+    _check_tensor(keys, "keys")
+    kb = _KEY_BYTES[keys.dtype]
+    n = keys.numel()
+    h = comm.handle if comm else None
+    if comm is not None:
+        cap = out_cap if out_cap is not None else comm.capacity(n)
+        if out is None:
+            out = torch.empty(max(cap, 1), dtype=keys.dtype, device=keys.device)
+        cap = min(cap, out.numel())
+    else:
+        if out is None:
+            out = keys
+        cap = out.numel()
+    if ws is None:
+        ws = _workspace(lib().rs_workspace_bytes(kb, 0, comm.ws_n(n) if comm else n, digit_bits, h), keys.device)
+    n_out = ctypes.c_size_t(0)
+    fn = lib().rs_sort_u32 if kb == 4 else lib().rs_sort_u64
+    check(fn(keys.data_ptr(), n, digit_bits, h, out.data_ptr(), cap, ctypes.byref(n_out), ws.data_ptr(), ws.numel(),
+             _stream(stream)), "rs_sort")
+    return out[: n_out.value] if comm is not None else out
+
+
+def sort_pairs(keys: torch.Tensor, vals: torch.Tensor, digit_bits: int = 8, comm: "Comm | None" = None,
+               out_keys: torch.Tensor | None = None, out_vals: torch.Tensor | None = None,
+               ws: torch.Tensor | None = None, out_cap: int | None = None, stream=None):
+    """Stable sort of (uint64 key, uint32 value) pairs; returns (keys, vals)."""
+    _check_tensor(keys, "keys")
+    _check_tensor(vals, "vals")
+    if _KEY_BYTES[keys.dtype] != 8 or vals.element_size() != 4 or vals.numel() != keys.numel():
+        raise ValueError("sort_pairs expects uint64 keys and 32-bit values of equal length")
+    n = keys.numel()
+    h = comm.handle if comm else None
+    if comm is not None:
+        cap = out_cap if out_cap is not None else comm.capacity(n)
+        out_keys = out_keys if out_keys is not None else torch.empty(max(cap, 1), dtype=keys.dtype, device=keys.device)
+        out_vals = out_vals if out_vals is not None else torch.empty(max(cap, 1), dtype=vals.dtype, device=vals.device)
+        cap = min(cap, out_keys.numel(), out_vals.numel())
+    else:
+        out_keys = keys if out_keys is None else out_keys
+        out_vals = vals if out_vals is None else out_vals
+        cap = out_keys.numel()
+    if ws is None:
+        ws = _workspace(lib().rs_workspace_bytes(8, 4, comm.ws_n(n) if comm else n, digit_bits, h), keys.device)
+    n_out = ctypes.c_size_t(0)
+    check(lib().rs_sort_pairs_u64_u32(keys.data_ptr(), vals.data_ptr(), n, digit_bits, h, out_keys.data_ptr(),
+                                      out_vals.data_ptr(), cap, ctypes.byref(n_out), ws.data_ptr(), ws.numel(),
+                                      _stream(stream)), "rs_sort_pairs_u64_u32")
+    if comm is not None:
+        return out_keys[: n_out.value], out_vals[: n_out.value]
+    return out_keys, out_vals
+
+
+def sort_bits(keys: torch.Tensor, end_bit: int, digit_bits: int = 8, vals: torch.Tensor | None = None,
+              out_keys: torch.Tensor | None = None, out_vals: torch.Tensor | None = None,
+              ws: torch.Tensor | None = None, stream=None):
+    """Stable sort by the low `end_bit` bits (passes 0..ceil(end_bit/b)-1)."""
+    _check_tensor(keys, "keys")
+    kb = _KEY_BYTES[keys.dtype]
+    n = keys.numel()
+    out_keys = torch.empty_like(keys) if out_keys is None else out_keys
+    if vals is not None and out_vals is None:
+        out_vals = torch.empty_like(vals)
+    if ws is None:
+        ws = _workspace(lib().rs_workspace_bytes(kb, 4 if vals is not None else 0, n, digit_bits, None), keys.device)
+    check(lib().rs_sort_bits(kb, keys.data_ptr(), _ptr(vals), n, digit_bits, end_bit, out_keys.data_ptr(),
+                             _ptr(out_vals), ws.data_ptr(), ws.numel(), _stream(stream)), "rs_sort_bits")
+    return (out_keys, out_vals) if vals is not None else out_keys
+
+
+def digit_histogram(keys: torch.Tensor, digit_bits: int = 8, stream=None) -> torch.Tensor:
+    """All passes' digit counts from one read: int64-viewable (P, 2^b) uint32 tensor."""
+    _check_tensor(keys, "keys")
+    kb = _KEY_BYTES[keys.dtype]
+    P = kb * 8 // digit_bits
+    hist = torch.empty(P * (1 << digit_bits), dtype=torch.int32, device=keys.device)
+    ws = _workspace(16, keys.device)
+    check(lib().rs_digit_histogram(kb, keys.data_ptr(), keys.numel(), digit_bits, hist.data_ptr(), ws.data_ptr(),
+                                   ws.numel(), _stream(stream)), "rs_digit_histogram")
+    return hist.view(P, 1 << digit_bits)
+
+
+class Comm:
+    """GSD communicator: an NCCL comm owned by librsort, bootstrapped over a
+    torch.distributed process group (only the 128-byte unique id travels)."""
+
+    def __init__(self, group=None, device: int | None = None, oversampling: int = 8):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+        self.device = torch.cuda.current_device() if device is None else device
+        uid = (ctypes.c_char * 128)()
+        if self.rank == 0:
+            check(lib().rs_get_unique_id(uid), "rs_get_unique_id")
+        obj = [bytes(uid)]
+        src = dist.get_global_rank(group, 0) if group is not None else 0
+        dist.broadcast_object_list(obj, src=src, group=group)
+        uid = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+        h = ctypes.c_void_p()
+        check(lib().rs_comm_create(uid, self.size, self.rank, self.device, ctypes.byref(h)), "rs_comm_create")
+        self.handle = h
+        self.set_oversampling(oversampling)
+        # largest local n over ranks, for workspace / capacity sizing
+        self._group = group
+
+    def set_oversampling(self, r: int):
+        check(lib().rs_comm_set_oversampling(self.handle, r), "rs_comm_set_oversampling")
+        self.r = r
+
+    def capacity(self, n_local: int) -> int:
+        return lib().rs_output_capacity(self.ws_n(n_local), self.handle)
+
+    def ws_n(self, n_local: int) -> int:
+        import torch.distributed as dist
+        t = torch.tensor([n_local], dtype=torch.int64)
+        if dist.get_backend(self._group) == "nccl":
+            t = t.cuda()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self._group)
+        return int(t.item())
+
+    def close(self):
+        if self.handle:
+            lib().rs_comm_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def gsd_emulate(blocks: list[torch.Tensor], r: int = 8, digit_bits: int = 8, vals: list[torch.Tensor] | None = None,
+                out_cap: int | None = None, stream=None):
+    """GSD over p = len(blocks) ranks held on this GPU (see include/rsort.h):
+    returns dict(Y, Yv, n_out, splitters (p-1,3) uint64, counts (p,p) uint64)."""
+    import numpy as np
+    p = len(blocks)
+    kb = _KEY_BYTES[blocks[0].dtype]
+    n = [b.numel() for b in blocks]
+    nmax = max(n) if n else 0
+    cap = out_cap if out_cap is not None else nmax + nmax // r + p
+    dev = blocks[0].device
+    outs = [torch.empty(max(cap, 1), dtype=blocks[0].dtype, device=dev) for _ in range(p)]
+    vouts = [torch.empty(max(cap, 1), dtype=torch.int32, device=dev) for _ in range(p)] if vals is not None else None
+    wsb = lib().rs_gsd_emulate_ws_bytes(kb, 4 if vals is not None else 0, p, r, digit_bits, nmax, cap)
+    ws = _workspace(wsb, dev)
+    arr = ctypes.c_void_p * p
+    n_arr = (ctypes.c_size_t * p)(*n)
+    n_out = (ctypes.c_size_t * p)()
+    spl = np.zeros((max(p - 1, 1), 3), dtype=np.uint64)
+    counts = np.zeros((p, p), dtype=np.uint64)
+    check(lib().rs_gsd_emulate(kb, p, r, digit_bits, arr(*[b.data_ptr() for b in blocks]),
+                               arr(*[v.data_ptr() for v in vals]) if vals is not None else None, n_arr,
+                               arr(*[o.data_ptr() for o in outs]),
+                               arr(*[o.data_ptr() for o in vouts]) if vals is not None else None, cap, n_out,
+                               spl.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+                               counts.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ws.data_ptr(), ws.numel(),
+                               _stream(stream)), "rs_gsd_emulate")
+    return dict(Y=[outs[j][: n_out[j]] for j in range(p)],
+                Yv=[vouts[j][: n_out[j]] for j in range(p)] if vals is not None else None,
+                n_out=list(n_out), splitters=spl[: p - 1], counts=counts)

@@ -1,0 +1,457 @@
+// GSD (Algorithm 1) on B200s: one process per GPU, NCCL
+// over NVLink/NVSwitch for the three exchanges, the radix sort for step 1.
+//
+//   step 1 LocalSorting    local radix sort of the rank's block in place  (radix.cu)
+//   step 2 SampleSelection K5 k_gsd_sample: s = r·p composites of X_k at ⌈N·i/s⌉−1,
+//                          i = 1..s−1, plus N−1 (reading R10); C1 ncclAllGather
+//   step 3 SplitterSelect  K6 k_gsd_splitters: bitonic sort of the r·p² sample in one
+//                          CTA, S_i = T[i·s−1] (R11, R12) — identical on every rank,
+//                          so the paper's "Broadcast splitters" is implicit
+//   step 4 Split           K7 k_gsd_split: binary search of the composite splitters
+//                          (R14) -> |X_{k,j}|; C2 ncclAllGather of the p counts, one
+//                          D2H copy + host sync (NCCL send/recv take host counts);
+//                          C3 grouped ncclSend/ncclRecv of the X_{k,j} slices (the
+//                          sorted block is already grouped by destination: zero-copy)
+//   step 5 Merging         Y_j from the p received runs, ties to the lower source rank
+//                          (R16): a stable radix re-sort of the concatenation, which is
+//                          identical to the p-way merge (R17).
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "gsd.h"
+
+namespace rs {
+
+// ------------------------------------------------------------------ K5 ----
+template <typename K>
+__global__ void k_gsd_sample(const K* __restrict__ X, size_t N, uint32_t rank, int s, Comp* __restrict__ out) {
+    for (int i = 1 + threadIdx.x + blockIdx.x * blockDim.x; i <= s; i += blockDim.x * gridDim.x) {
+        Comp c;
+        c.rank = rank;
+        if (N == 0) {
+            c.key = ~0ull;
+            c.pos = kPosInf;
+        } else {
+            const size_t pos = i < s ? (N * (size_t)i + (size_t)s - 1) / (size_t)s - 1 : N - 1;
+            c.key = static_cast<uint64_t>(X[pos]);
+            c.pos = (uint32_t)pos;
+        }
+        out[i - 1] = c;
+    }
+}
+
+__device__ __forceinline__ bool comp_less(const Comp& a, const Comp& b) {
+    if (a.key != b.key) return a.key < b.key;
+    if (a.rank != b.rank) return a.rank < b.rank;
+    return a.pos < b.pos;
+}
+
+// ------------------------------------------------------------------ K6 ----
+__global__ void __launch_bounds__(1024) k_gsd_splitters(const Comp* __restrict__ T_all, int M, int s, int p,
+                                                        Comp* __restrict__ S) {
+    extern __shared__ Comp sT[];
+    int L = 1;
+    while (L < M) L <<= 1;
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        if (i < M) sT[i] = T_all[i];
+        else sT[i] = Comp{~0ull, 0xFFFFFFFFu, 0xFFFFFFFFu};
+    }
+    __syncthreads();
+    for (int k = 2; k <= L; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < L; i += blockDim.x) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = (i & k) == 0;
+                    Comp a = sT[i], b = sT[ixj];
+                    if (comp_less(b, a) == up) {
+                        sT[i] = b;
+                        sT[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    for (int i = 1 + threadIdx.x; i < p; i += blockDim.x) S[i - 1] = sT[(size_t)i * s - 1];
+}
+
+// ------------------------------------------------------------------ K7 ----
+template <typename K>
+__device__ size_t bound(const K* X, size_t N, uint64_t v, bool upper) {
+    size_t lo = 0, hi = N;
+    while (lo < hi) {
+        const size_t mid = (lo + hi) >> 1;
+        const uint64_t x = static_cast<uint64_t>(X[mid]);
+        if (upper ? (x <= v) : (x < v)) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// cut(j) = #{e in X_k : e <=_c S_j}; for S_j = (v, r, q): k < r -> upper_bound(v),
+// k > r -> lower_bound(v), k == r -> min(q + 1, N)   (reading R14)
+template <typename K>
+__global__ void k_gsd_split(const K* __restrict__ X, size_t N, uint32_t rank, int p, const Comp* __restrict__ S,
+                            uint64_t* __restrict__ counts) {
+    const int j = threadIdx.x;
+    if (j >= p) return;
+    auto cut = [&](int jj) -> size_t {
+        if (jj <= 0) return 0;
+        if (jj >= p) return N;
+        const Comp sp = S[jj - 1];
+        if (rank < sp.rank) return bound<K>(X, N, sp.key, true);
+        if (rank > sp.rank) return bound<K>(X, N, sp.key, false);
+        const uint64_t q1 = (uint64_t)sp.pos + 1;
+        return (size_t)(q1 < (uint64_t)N ? q1 : (uint64_t)N);
+    };
+    counts[j] = (uint64_t)(cut(j + 1) - cut(j));
+}
+
+// ------------------------------------------------------------------ host --
+struct GsdLayout {
+    void* local_ws;
+    size_t local_ws_bytes;
+    void* recv_keys;
+    uint32_t* recv_vals;
+    uint64_t* hdr_local;  // 8 words
+    uint64_t* hdr_all;    // p*8
+    Comp* samp_local;     // s
+    Comp* samp_all;       // p*s
+    Comp* splitters;      // p-1
+    uint64_t* counts_local;  // p
+    uint64_t* counts_all;    // p*p (or p slots of p for the emulation)
+    size_t bytes;
+};
+
+static GsdLayout gsd_layout(void* ws, int key_bytes, bool has_val, size_t n, size_t cap, int b, int p, int r,
+                            size_t recv_slots) {
+    GsdLayout L{};
+    Carver c(ws);
+    const size_t s = (size_t)r * p;
+    L.local_ws_bytes = local_ws_bytes(key_bytes, has_val, std::max(n, cap), b);
+    L.local_ws = c.take(L.local_ws_bytes);
+    L.recv_keys = c.take(recv_slots * cap * key_bytes);
+    L.recv_vals = static_cast<uint32_t*>(has_val ? c.take(recv_slots * cap * 4) : nullptr);
+    L.hdr_local = static_cast<uint64_t*>(c.take(8 * 8));
+    L.hdr_all = static_cast<uint64_t*>(c.take((size_t)p * 8 * 8));
+    L.samp_local = static_cast<Comp*>(c.take(s * sizeof(Comp)));
+    L.samp_all = static_cast<Comp*>(c.take((size_t)p * s * sizeof(Comp)));
+    L.splitters = static_cast<Comp*>(c.take((size_t)p * sizeof(Comp)));
+    L.counts_local = static_cast<uint64_t*>(c.take((size_t)p * 8));
+    L.counts_all = static_cast<uint64_t*>(c.take((size_t)p * p * 8));
+    L.bytes = c.used();
+    return L;
+}
+
+static size_t capacity_for(size_t n_local_max, int r, int p) {
+    // ⌊(1 + 1/r)·N_max⌋ + p   (reading R18)
+    return n_local_max + n_local_max / (size_t)r + (size_t)p;
+}
+
+size_t gsd_capacity(Comm* c, size_t n_local_max) { return capacity_for(n_local_max, c->r, c->nranks); }
+
+size_t gsd_ws_bytes(Comm* c, int key_bytes, bool has_val, size_t n_local_max, int b) {
+    const size_t cap = gsd_capacity(c, n_local_max);
+    return gsd_layout(nullptr, key_bytes, has_val, n_local_max, cap, b, c->nranks, c->r, 1).bytes;
+}
+
+static rs_status_t launch_sample(int key_bytes, const void* X, size_t N, int rank, int s, Comp* out,
+                                 cudaStream_t st) {
+    LaunchScope ls("gsd_sample", st);
+    const int threads = std::min(256, std::max(32, s));
+    const int grid = (s + threads - 1) / threads;
+    if (key_bytes == 4)
+        k_gsd_sample<uint32_t><<<grid, threads, 0, st>>>(static_cast<const uint32_t*>(X), N, rank, s, out);
+    else
+        k_gsd_sample<uint64_t><<<grid, threads, 0, st>>>(static_cast<const uint64_t*>(X), N, rank, s, out);
+    return RS_OK;
+}
+
+static rs_status_t launch_splitters(const Comp* T_all, int M, int s, int p, Comp* S, cudaStream_t st) {
+    int L = 1;
+    while (L < M) L <<= 1;
+    const size_t smem = (size_t)L * sizeof(Comp);
+    static bool attr = false;
+    if (!attr) {
+        RS_CUDA_TRY(cudaFuncSetAttribute(k_gsd_splitters, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(kMaxSample * sizeof(Comp))));
+        attr = true;
+    }
+    LaunchScope ls("gsd_splitters", st);
+    k_gsd_splitters<<<1, 1024, smem, st>>>(T_all, M, s, p, S);
+    return RS_OK;
+}
+
+static rs_status_t launch_split(int key_bytes, const void* X, size_t N, int rank, int p, const Comp* S,
+                                uint64_t* counts, cudaStream_t st) {
+    LaunchScope ls("gsd_split", st);
+    const int threads = ((p + 31) / 32) * 32;
+    if (key_bytes == 4)
+        k_gsd_split<uint32_t><<<1, threads, 0, st>>>(static_cast<const uint32_t*>(X), N, rank, p, S, counts);
+    else
+        k_gsd_split<uint64_t><<<1, threads, 0, st>>>(static_cast<const uint64_t*>(X), N, rank, p, S, counts);
+    return RS_OK;
+}
+
+// step 5: Y_j from the concatenated runs (source-rank order) by a stable sort
+static rs_status_t merge_runs(int key_bytes, void* runs, uint32_t* vruns, size_t total, int b, void* out,
+                              uint32_t* vout, const GsdLayout& L, cudaStream_t st) {
+    if (total == 0) return RS_OK;
+    return local_sort(key_bytes, runs, vruns, total, b, key_bytes * 8, out, vout, L.local_ws, L.local_ws_bytes, st);
+}
+
+#define RS_NCCL_TRY(expr)                                                                     \
+    do {                                                                                      \
+        ncclResult_t r_ = (expr);                                                             \
+        if (r_ != ncclSuccess)                                                                \
+            return fail(RS_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(r_));        \
+    } while (0)
+
+rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t n, int b, void* out, uint32_t* vout,
+                     size_t out_cap, size_t* n_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+    const int p = c->nranks, rank = c->rank, r = c->r;
+    const size_t s = (size_t)r * p;
+    const bool hv = vals != nullptr;
+    if ((size_t)p * s > (size_t)kMaxSample)
+        return fail(RS_EINVAL, "r*p^2 exceeds the one-CTA sample sort limit of 8192");
+    const GsdLayout L = gsd_layout(ws, key_bytes, hv, n, out_cap, b, p, r, 1);
+    if (!ws || ws_bytes < L.bytes || !aligned16(ws))
+        return fail(RS_EINVAL, "GSD workspace too small / misaligned: need " + std::to_string(L.bytes));
+    if (out_cap && (!out || (hv && !vout))) return fail(RS_EINVAL, "NULL output with out_cap > 0");
+
+    // header all-gather: a mismatch is an error on every rank, not a hang
+    uint64_t* h = c->h_pinned;
+    uint64_t hdr[8] = {0x52534F5254ull, (uint64_t)key_bytes, (uint64_t)hv, (uint64_t)b, (uint64_t)r, (uint64_t)p,
+                       (uint64_t)out_cap, (uint64_t)n};
+    std::memcpy(h, hdr, sizeof(hdr));
+    RS_CUDA_TRY(cudaMemcpyAsync(L.hdr_local, h, sizeof(hdr), cudaMemcpyHostToDevice, st));
+    RS_NCCL_TRY(ncclAllGather(L.hdr_local, L.hdr_all, 8, ncclUint64, c->nccl, st));
+    RS_CUDA_TRY(cudaMemcpyAsync(h, L.hdr_all, (size_t)p * 64, cudaMemcpyDeviceToHost, st));
+    RS_CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<uint64_t> caps(p);
+    for (int k = 0; k < p; ++k) {
+        for (int f = 0; f < 6; ++f)
+            if (h[k * 8 + f] != hdr[f])
+                return fail(RS_EINVAL, "GSD header mismatch with rank " + std::to_string(k) + " (field " +
+                                           std::to_string(f) + ")");
+        caps[k] = h[k * 8 + 6];
+        if (h[k * 8 + 7] >= (1ull << 32)) return fail(RS_EINVAL, "n >= 2^32 on rank " + std::to_string(k));
+    }
+
+    // step 1: local sort in place -> X_k
+    rs_status_t sst = n ? local_sort(key_bytes, keys, vals, n, b, key_bytes * 8, keys, vals, L.local_ws,
+                                     L.local_ws_bytes, st)
+                        : RS_OK;
+    if (sst != RS_OK) return sst;
+    // step 2: regular sample + all-gather
+    if ((sst = launch_sample(key_bytes, keys, n, rank, (int)s, L.samp_local, st)) != RS_OK) return sst;
+    RS_NCCL_TRY(ncclAllGather(L.samp_local, L.samp_all, s * sizeof(Comp), ncclUint8, c->nccl, st));
+    // step 3: splitters, identical on every rank
+    if ((sst = launch_splitters(L.samp_all, (int)(p * s), (int)s, p, L.splitters, st)) != RS_OK) return sst;
+    // step 4: split + count exchange
+    if ((sst = launch_split(key_bytes, keys, n, rank, p, L.splitters, L.counts_local, st)) != RS_OK) return sst;
+    RS_NCCL_TRY(ncclAllGather(L.counts_local, L.counts_all, p, ncclUint64, c->nccl, st));
+    RS_CUDA_TRY(cudaMemcpyAsync(h, L.counts_all, (size_t)p * p * 8, cudaMemcpyDeviceToHost, st));
+    RS_CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<uint64_t> cnt(h, h + (size_t)p * p);
+    for (int j = 0; j < p; ++j) {
+        uint64_t tot = 0;
+        for (int k = 0; k < p; ++k) tot += cnt[(size_t)k * p + j];
+        if (tot > caps[j])
+            return fail(RS_ECAPACITY, "rank " + std::to_string(j) + " receives " + std::to_string(tot) +
+                                          " keys > out_cap " + std::to_string(caps[j]));
+    }
+    std::vector<uint64_t> soff(p + 1, 0), roff(p + 1, 0);
+    for (int j = 0; j < p; ++j) soff[j + 1] = soff[j] + cnt[(size_t)rank * p + j];
+    for (int k = 0; k < p; ++k) roff[k + 1] = roff[k] + cnt[(size_t)k * p + rank];
+    const size_t total = roff[p];
+    // exchange X_{k,j}: grouped send/recv; the self slice is a device copy
+    char* kx = static_cast<char*>(keys);
+    char* rk = static_cast<char*>(L.recv_keys);
+    {
+        LaunchScope ls("gsd_exchange", st, false);
+        RS_NCCL_TRY(ncclGroupStart());
+        for (int j = 0; j < p; ++j) {
+            if (j == rank) continue;
+            const uint64_t sc = cnt[(size_t)rank * p + j], rc = cnt[(size_t)j * p + rank];
+            if (sc) {
+                RS_NCCL_TRY(ncclSend(kx + soff[j] * key_bytes, sc * key_bytes, ncclUint8, j, c->nccl, st));
+                if (hv) RS_NCCL_TRY(ncclSend(vals + soff[j], sc, ncclUint32, j, c->nccl, st));
+            }
+            if (rc) {
+                RS_NCCL_TRY(ncclRecv(rk + roff[j] * key_bytes, rc * key_bytes, ncclUint8, j, c->nccl, st));
+                if (hv) RS_NCCL_TRY(ncclRecv(L.recv_vals + roff[j], rc, ncclUint32, j, c->nccl, st));
+            }
+        }
+        RS_NCCL_TRY(ncclGroupEnd());
+        const uint64_t self = cnt[(size_t)rank * p + rank];
+        if (self) {
+            RS_CUDA_TRY(cudaMemcpyAsync(rk + roff[rank] * key_bytes, kx + soff[rank] * key_bytes, self * key_bytes,
+                                        cudaMemcpyDeviceToDevice, st));
+            if (hv)
+                RS_CUDA_TRY(cudaMemcpyAsync(L.recv_vals + roff[rank], vals + soff[rank], self * 4,
+                                            cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    // step 5: merge
+    if ((sst = merge_runs(key_bytes, L.recv_keys, L.recv_vals, total, b, out, vout, L, st)) != RS_OK) return sst;
+    if (n_out) *n_out = total;
+    RS_CUDA_TRY(cudaGetLastError());
+    return RS_OK;
+}
+
+}  // namespace rs
+
+using namespace rs;
+
+extern "C" {
+
+rs_status_t rs_get_unique_id(void* uid128) {
+    if (!uid128) return fail(RS_EINVAL, "NULL uid");
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId id;
+    RS_NCCL_TRY(ncclGetUniqueId(&id));
+    std::memcpy(uid128, &id, sizeof(id));
+    return RS_OK;
+}
+
+rs_status_t rs_comm_create(const void* uid128, int nranks, int rank, int cuda_device, void** out) {
+    if (!uid128 || !out || nranks < 1 || rank < 0 || rank >= nranks) return fail(RS_EINVAL, "bad comm arguments");
+    Comm* c = new (std::nothrow) Comm();
+    if (!c) return fail(RS_ENOMEM, "comm allocation");
+    c->rank = rank;
+    c->nranks = nranks;
+    c->device = cuda_device;
+    cudaError_t e = cudaSetDevice(cuda_device);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaSetDevice");
+    }
+    c->h_pinned_words = std::max<size_t>((size_t)nranks * nranks, (size_t)nranks * 8) + 64;
+    e = cudaMallocHost(&c->h_pinned, c->h_pinned_words * 8);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_fail(e, "cudaMallocHost");
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, uid128, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, id, rank);
+    if (r != ncclSuccess) {
+        cudaFreeHost(c->h_pinned);
+        delete c;
+        return fail(RS_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    }
+    *out = c;
+    return RS_OK;
+}
+
+rs_status_t rs_comm_destroy(void* comm) {
+    if (!comm) return RS_OK;
+    Comm* c = static_cast<Comm*>(comm);
+    if (c->nccl) ncclCommDestroy(c->nccl);
+    if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    delete c;
+    return RS_OK;
+}
+
+rs_status_t rs_comm_set_oversampling(void* comm, int r) {
+    if (!comm || r < 1) return fail(RS_EINVAL, "bad comm / r");
+    static_cast<Comm*>(comm)->r = r;
+    return RS_OK;
+}
+
+int rs_comm_rank(void* comm) { return comm ? static_cast<Comm*>(comm)->rank : 0; }
+int rs_comm_size(void* comm) { return comm ? static_cast<Comm*>(comm)->nranks : 1; }
+
+// ---------------------------------------------------------- emulation ----
+size_t rs_gsd_emulate_ws_bytes(int key_bytes, int val_bytes, int p, int r, int digit_bits, size_t n_max,
+                               size_t out_cap) {
+    if (p < 1 || r < 1) return 0;
+    return gsd_layout(nullptr, key_bytes, val_bytes != 0, n_max, out_cap, digit_bits, p, r, 1).bytes;
+}
+
+rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits, void* const* keys, uint32_t* const* vals,
+                           const size_t* n, void* const* out_keys, uint32_t* const* out_vals, size_t out_cap,
+                           size_t* n_out, uint64_t* splitters, uint64_t* counts, void* ws, size_t ws_bytes,
+                           void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (p < 1 || r < 1 || !keys || !n || !out_keys || !n_out) return fail(RS_EINVAL, "bad emulate arguments");
+    if (digit_bits != 8 && digit_bits != 16) return fail(RS_EINVAL, "digit_bits must be 8 or 16");
+    if (key_bytes != 4 && key_bytes != 8) return fail(RS_EINVAL, "key_bytes must be 4 or 8");
+    const bool hv = vals != nullptr;
+    const size_t s = (size_t)r * p;
+    if ((size_t)p * s > (size_t)kMaxSample) return fail(RS_EINVAL, "r*p^2 exceeds 8192");
+    size_t n_max = 0;
+    for (int k = 0; k < p; ++k) {
+        if (n[k] >= (1ull << 32)) return fail(RS_EINVAL, "n >= 2^32");
+        if (n[k] && (!keys[k] || !aligned16(keys[k]) || (hv && (!vals[k] || !aligned16(vals[k])))))
+            return fail(RS_EINVAL, "NULL / misaligned block");
+        n_max = std::max(n_max, n[k]);
+    }
+    const GsdLayout L = gsd_layout(ws, key_bytes, hv, n_max, out_cap, digit_bits, p, r, 1);
+    if (!ws || ws_bytes < L.bytes) return fail(RS_EINVAL, "emulate workspace too small: need " + std::to_string(L.bytes));
+    rs_status_t sst;
+    for (int k = 0; k < p; ++k)  // step 1
+        if (n[k] && (sst = local_sort(key_bytes, keys[k], hv ? vals[k] : nullptr, n[k], digit_bits, key_bytes * 8,
+                                      keys[k], hv ? vals[k] : nullptr, L.local_ws, L.local_ws_bytes, st)) != RS_OK)
+            return sst;
+    for (int k = 0; k < p; ++k)  // step 2 (the all-gather is the slot layout)
+        if ((sst = launch_sample(key_bytes, keys[k], n[k], k, (int)s, L.samp_all + (size_t)k * s, st)) != RS_OK)
+            return sst;
+    if ((sst = launch_splitters(L.samp_all, (int)(p * s), (int)s, p, L.splitters, st)) != RS_OK) return sst;
+    for (int k = 0; k < p; ++k)  // step 4
+        if ((sst = launch_split(key_bytes, keys[k], n[k], k, p, L.splitters, L.counts_all + (size_t)k * p, st)) !=
+            RS_OK)
+            return sst;
+    std::vector<uint64_t> cnt((size_t)p * p);
+    std::vector<Comp> spl(std::max(1, p - 1));
+    RS_CUDA_TRY(cudaMemcpyAsync(cnt.data(), L.counts_all, cnt.size() * 8, cudaMemcpyDeviceToHost, st));
+    if (p > 1)
+        RS_CUDA_TRY(cudaMemcpyAsync(spl.data(), L.splitters, (p - 1) * sizeof(Comp), cudaMemcpyDeviceToHost, st));
+    RS_CUDA_TRY(cudaStreamSynchronize(st));
+    if (counts) std::memcpy(counts, cnt.data(), cnt.size() * 8);
+    if (splitters)
+        for (int i = 0; i + 1 < p; ++i) {
+            splitters[3 * i] = spl[i].key;
+            splitters[3 * i + 1] = spl[i].rank;
+            splitters[3 * i + 2] = spl[i].pos == kPosInf ? ~0ull : spl[i].pos;
+        }
+    std::vector<uint64_t> cut((size_t)p * (p + 1));
+    for (int k = 0; k < p; ++k) {
+        cut[(size_t)k * (p + 1)] = 0;
+        for (int j = 0; j < p; ++j) cut[(size_t)k * (p + 1) + j + 1] = cut[(size_t)k * (p + 1) + j] + cnt[(size_t)k * p + j];
+    }
+    for (int j = 0; j < p; ++j) {
+        uint64_t tot = 0;
+        for (int k = 0; k < p; ++k) tot += cnt[(size_t)k * p + j];
+        n_out[j] = tot;
+        if (tot > out_cap) return fail(RS_ECAPACITY, "rank " + std::to_string(j) + " exceeds out_cap");
+    }
+    for (int j = 0; j < p; ++j) {  // step 4 exchange + step 5 merge, rank by rank
+        char* rk = static_cast<char*>(L.recv_keys);
+        uint64_t off = 0;
+        {
+            LaunchScope ls("gsd_exchange", st, false);
+            for (int k = 0; k < p; ++k) {
+                const uint64_t c = cnt[(size_t)k * p + j];
+                if (!c) continue;
+                const uint64_t so = cut[(size_t)k * (p + 1) + j];
+                RS_CUDA_TRY(cudaMemcpyAsync(rk + off * key_bytes, static_cast<char*>(keys[k]) + so * key_bytes,
+                                            c * key_bytes, cudaMemcpyDeviceToDevice, st));
+                if (hv)
+                    RS_CUDA_TRY(cudaMemcpyAsync(L.recv_vals + off, vals[k] + so, c * 4, cudaMemcpyDeviceToDevice, st));
+                off += c;
+            }
+        }
+        if ((sst = merge_runs(key_bytes, L.recv_keys, L.recv_vals, off, digit_bits, out_keys[j],
+                              hv ? out_vals[j] : nullptr, L, st)) != RS_OK)
+            return sst;
+    }
+    RS_CUDA_TRY(cudaGetLastError());
+    return RS_OK;
+}
+
+}  // extern "C"

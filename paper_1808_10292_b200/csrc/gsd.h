@@ -1,0 +1,36 @@
+// GSD — deterministic regular oversampling sample sort across GPUs
+// (Algorithm 1), host side.
+#pragma once
+#include <nccl.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "runtime.h"
+
+namespace rs {
+
+struct Comm {
+    ncclComm_t nccl = nullptr;
+    int rank = 0, nranks = 1, device = 0;
+    int r = 8;                     // oversampling factor, s = r·p
+    uint64_t* h_pinned = nullptr;  // p*p counts + headers (pinned host)
+    size_t h_pinned_words = 0;
+};
+
+// composite key (key, rank, pos): the unique total order used for sampling
+// and splitting (readings R10, R14-R16)
+struct Comp {
+    uint64_t key;
+    uint32_t rank;
+    uint32_t pos;
+};
+constexpr uint32_t kPosInf = 0xFFFFFFFFu;
+constexpr int kMaxSample = 8192;  // r·p² composites sorted in one CTA
+
+size_t gsd_capacity(Comm* c, size_t n_local_max);
+size_t gsd_ws_bytes(Comm* c, int key_bytes, bool has_val, size_t n_local_max, int b);
+rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t n, int b, void* out,
+                     uint32_t* vout, size_t out_cap, size_t* n_out, void* ws, size_t ws_bytes, cudaStream_t st);
+
+}  // namespace rs

@@ -1,0 +1,211 @@
+// Single-GPU LSD radix sort driver: workspace layout and the launch sequence
+//   memset(ctrl, hist) -> K1 hist -> K2 plan -> K3 pass × P -> K4 final copy
+// for radix 256 (SR4/PR4), and the radix-65536 path
+// (PR2) in radix16.cuh.  Everything is enqueued on the
+// caller's stream; no host synchronisation, no allocation.
+#include <algorithm>
+#include <cstring>
+
+#include "onesweep.cuh"
+#include "radix16.cuh"
+#include "runtime.h"
+
+namespace rs {
+
+// ------------------------------------------------------- tile configurations
+// (THREADS, keys per thread, min CTAs per SM); overridable with -D for tuning runs
+#ifndef RS_U32_T
+#define RS_U32_T 512
+#define RS_U32_KPT 12
+#define RS_U32_MINB 2
+#endif
+#define RS_TUNE_U32 RS_U32_T, RS_U32_KPT, RS_U32_MINB
+#define RS_TUNE_U64 512, 8, 2
+#define RS_TUNE_PAIRS 512, 8, 2
+#define RS_TUNE_U32V 512, 8, 2
+template <int T_, int KPT_, int MINB_>
+struct TuneT {
+    static constexpr int THREADS = T_, KPT = KPT_, MINB = MINB_;
+};
+template <typename K, bool V>
+struct Tune;
+template <>
+struct Tune<uint32_t, false> : TuneT<RS_TUNE_U32> {};
+template <>
+struct Tune<uint64_t, false> : TuneT<RS_TUNE_U64> {};
+template <>
+struct Tune<uint64_t, true> : TuneT<RS_TUNE_PAIRS> {};
+template <>
+struct Tune<uint32_t, true> : TuneT<RS_TUNE_U32V> {};
+
+constexpr int kHistThreads = 512;
+
+template <typename K, bool V>
+static constexpr int tile_keys() {
+    return Tune<K, V>::THREADS * Tune<K, V>::KPT;
+}
+
+static int tile_for(int key_bytes, bool has_val) {
+    if (key_bytes == 4) return has_val ? tile_keys<uint32_t, true>() : tile_keys<uint32_t, false>();
+    return has_val ? tile_keys<uint64_t, true>() : tile_keys<uint64_t, false>();
+}
+
+struct Layout8 {
+    Ctrl* ctrl;
+    uint32_t* hist;
+    uint32_t* bases;
+    void* status;  // [2][T][256] u32 or u64 words
+    void* alt_keys;
+    uint32_t* alt_vals;
+    size_t T, status_bytes, bytes;
+    bool wide;
+};
+
+static Layout8 layout8(void* ws, int key_bytes, bool has_val, size_t n) {
+    Layout8 L{};
+    const size_t tile = (size_t)tile_for(key_bytes, has_val);
+    const int P = key_bytes * 8 / 8;
+    L.T = std::max<size_t>(1, (n + tile - 1) / tile);
+    L.wide = n > kNarrowStatusMaxN || options().wide_status;  // counts need > 30 bits
+    L.status_bytes = L.T * 256 * (L.wide ? 8 : 4);            // one region
+    Carver c(ws);
+    L.ctrl = static_cast<Ctrl*>(c.take(sizeof(Ctrl)));
+    L.hist = static_cast<uint32_t*>(c.take(P * 256 * 4));
+    L.bases = static_cast<uint32_t*>(c.take(P * 256 * 4));
+    L.status = c.take(2 * L.status_bytes);
+    L.alt_keys = c.take(n * key_bytes);
+    L.alt_vals = static_cast<uint32_t*>(has_val ? c.take(n * 4) : nullptr);
+    L.bytes = c.used();
+    return L;
+}
+
+size_t local_ws_bytes(int key_bytes, bool has_val, size_t n, int b) {
+    if (b == 8) return layout8(nullptr, key_bytes, has_val, n).bytes;
+    return radix16_ws_bytes(key_bytes, has_val, n);
+}
+
+template <typename K, bool V, int VARIANT, typename S>
+static rs_status_t launch_pass_v(const PassArgs& a, size_t T, cudaStream_t st) {
+    using TN = Tune<K, V>;
+    using C = OnesweepCfg<K, V, TN::THREADS, TN::KPT, VARIANT == 2 ? 2 : 1>;
+    auto kern = k_onesweep<K, V, TN::THREADS, TN::KPT, TN::MINB, VARIANT, S>;
+    static int grid_cap = 0;
+    if (!grid_cap) {
+        RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
+        int per_sm = 0;
+        RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TN::THREADS, C::smem_bytes));
+        grid_cap = std::max(1, per_sm) * sm_count();
+    }
+    const unsigned grid = (unsigned)std::min<size_t>(T, (size_t)grid_cap);  // persistent CTAs
+    LaunchScope ls("onesweep", st);
+    kern<<<grid, TN::THREADS, C::smem_bytes, st>>>(a);
+    return RS_OK;
+}
+
+template <typename K, bool V>
+static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStream_t st) {
+    const int rv = options().rank_variant;
+    if (wide) {
+        if (rv == 1) return launch_pass_v<K, V, 1, uint64_t>(a, T, st);
+        if (rv == 2) return launch_pass_v<K, V, 2, uint64_t>(a, T, st);
+        return launch_pass_v<K, V, 0, uint64_t>(a, T, st);
+    }
+    if (rv == 1) return launch_pass_v<K, V, 1, uint32_t>(a, T, st);
+    if (rv == 2) return launch_pass_v<K, V, 2, uint32_t>(a, T, st);
+    return launch_pass_v<K, V, 0, uint32_t>(a, T, st);
+}
+
+template <typename K>
+static rs_status_t launch_hist(const K* keys, size_t n, int P, uint32_t* hist,
+                               uint32_t* zero_ptr, size_t zero_words, cudaStream_t st) {
+    constexpr int COPIES = kHistThreads / 128;
+    const size_t smem = (size_t)COPIES * P * 256 * 4;
+    auto kern = k_digit_hist<K, kHistThreads>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024));
+        attr_set = true;
+    }
+    const size_t want = (n + kHistThreads * 16 - 1) / (kHistThreads * 16);
+    const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>(want, (size_t)sm_count() * 4));
+    LaunchScope ls("hist", st);
+    kern<<<grid, kHistThreads, smem, st>>>(keys, n, P, 8, hist, zero_ptr, zero_words);
+    return RS_OK;
+}
+
+template <typename K, bool V>
+static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, int end_bit, K* out,
+                         uint32_t* vout, void* ws, cudaStream_t st) {
+    const Layout8 L = layout8(ws, sizeof(K), V, n);
+    const int P = (end_bit + 7) / 8;
+    RS_CUDA_TRY(cudaMemsetAsync(L.ctrl, 0, sizeof(Ctrl), st));
+    RS_CUDA_TRY(cudaMemsetAsync(L.hist, 0, (size_t)P * 256 * 4, st));
+    // K1 also zeroes the first pass's status region (as u32 words)
+    rs_status_t s = launch_hist<K>(keys_in, n, P, L.hist, static_cast<uint32_t*>(L.status), L.status_bytes / 4, st);
+    if (s != RS_OK) return s;
+    {
+        LaunchScope ls("plan", st);
+        k_plan<<<1, 256, 0, st>>>(L.hist, (uint32_t)n, P, L.bases, L.ctrl,
+                                  (const void*)keys_in == (const void*)out ? 1 : 0);
+    }
+    PassArgs a{};
+    a.keys_in = keys_in;
+    a.keys_out = out;
+    a.keys_alt = L.alt_keys;
+    a.vals_in = vals_in;
+    a.vals_out = vout;
+    a.vals_alt = L.alt_vals;
+    a.n = (uint32_t)n;
+    a.num_tiles = (uint32_t)L.T;
+    a.P = P;
+    a.ctrl = L.ctrl;
+    a.bases = L.bases;
+    for (int t = 0; t < P; ++t) {
+        a.pass = t;
+        a.shift = 8 * t;
+        a.status_cur = static_cast<char*>(L.status) + (size_t)(t & 1) * L.status_bytes;
+        a.status_next = static_cast<char*>(L.status) + (size_t)((t + 1) & 1) * L.status_bytes;
+        s = launch_pass<K, V>(a, L.T, L.wide, st);
+        if (s != RS_OK) return s;
+    }
+    {
+        LaunchScope ls("final_copy", st);
+        const unsigned grid = (unsigned)std::min<size_t>((n + 4095) / 4096 + 1, (size_t)sm_count() * 8);
+        k_final_copy<K><<<grid, 256, 0, st>>>(L.ctrl, keys_in, static_cast<const K*>(L.alt_keys), out, vals_in,
+                                              L.alt_vals, V ? vout : nullptr, n);
+    }
+    RS_CUDA_TRY(cudaGetLastError());
+    return RS_OK;
+}
+
+rs_status_t local_sort(int key_bytes, const void* keys_in, const uint32_t* vals_in, size_t n, int b,
+                       int end_bit, void* out, uint32_t* vout, void* ws, size_t ws_bytes,
+                       cudaStream_t st) {
+    if (n == 0) return RS_OK;
+    const bool V = vals_in != nullptr;
+    if (b == 16) return radix16_sort(key_bytes, keys_in, vals_in, n, end_bit, out, vout, ws, ws_bytes, st);
+    if (key_bytes == 4) {
+        if (V)
+            return sort8<uint32_t, true>(static_cast<const uint32_t*>(keys_in), vals_in, n, end_bit,
+                                         static_cast<uint32_t*>(out), vout, ws, st);
+        return sort8<uint32_t, false>(static_cast<const uint32_t*>(keys_in), nullptr, n, end_bit,
+                                      static_cast<uint32_t*>(out), nullptr, ws, st);
+    }
+    if (V)
+        return sort8<uint64_t, true>(static_cast<const uint64_t*>(keys_in), vals_in, n, end_bit,
+                                     static_cast<uint64_t*>(out), vout, ws, st);
+    return sort8<uint64_t, false>(static_cast<const uint64_t*>(keys_in), nullptr, n, end_bit,
+                                  static_cast<uint64_t*>(out), nullptr, ws, st);
+}
+
+rs_status_t digit_histogram(int key_bytes, const void* keys, size_t n, int b, uint32_t* hist, void* ws,
+                            size_t ws_bytes, cudaStream_t st) {
+    const int P = key_bytes * 8 / b;
+    RS_CUDA_TRY(cudaMemsetAsync(hist, 0, (size_t)P * ((size_t)1 << b) * 4, st));
+    if (n == 0) return RS_OK;
+    if (b == 16) return radix16_histogram(key_bytes, keys, n, hist, st);
+    if (key_bytes == 4) return launch_hist<uint32_t>(static_cast<const uint32_t*>(keys), n, P, hist, nullptr, 0, st);
+    return launch_hist<uint64_t>(static_cast<const uint64_t*>(keys), n, P, hist, nullptr, 0, st);
+}
+
+}  // namespace rs

@@ -1,0 +1,370 @@
+// Radix-65536 pass kernels and driver (see radix16.cuh for the design).
+#include <algorithm>
+
+#include "radix16.cuh"
+
+namespace rs {
+
+constexpr int kC16Threads = 1024;  // count kernel
+constexpr int kS16Threads = 512;   // scatter kernel
+constexpr int kS16KPT = 8;
+constexpr int kS16Chunk = kS16Threads * kS16KPT;
+
+// ------------------------------------------------------------------ C1 ----
+// smem: 32768 u32 words, each holding two 16-bit counters (digit d in word d>>1,
+// half d&1).  A round covers at most 65535 keys so no half overflows.
+template <typename K>
+__global__ void __launch_bounds__(kC16Threads) k16_count(const K* __restrict__ keys, size_t n, int shift,
+                                                         size_t part_keys, uint32_t* __restrict__ H) {
+    extern __shared__ uint32_t s_cnt[];  // [32768]
+    const int tid = threadIdx.x;
+    const size_t g = blockIdx.x;
+    const size_t lo = g * part_keys;
+    const size_t hi = min(n, lo + part_keys);
+    uint32_t* Hg = H + g * kR16;
+    int round = 0;
+    for (size_t r0 = lo; r0 < hi || round == 0; r0 += 65535, ++round) {
+        for (int i = tid; i < kR16 / 2; i += kC16Threads) s_cnt[i] = 0;
+        __syncthreads();
+        const size_t r1 = min(hi, r0 + 65535);
+        for (size_t i = r0 + tid; i < r1; i += kC16Threads) {
+            const uint32_t d = static_cast<uint32_t>(keys[i] >> shift) & 0xFFFFu;
+            atomicAdd(&s_cnt[d >> 1], 1u << ((d & 1) * 16));
+        }
+        __syncthreads();
+        for (int w = tid; w < kR16 / 2; w += kC16Threads) {
+            const uint32_t v = s_cnt[w];
+            const uint32_t c0 = v & 0xFFFFu, c1 = v >> 16;
+            if (round == 0) {
+                Hg[2 * w] = c0;
+                Hg[2 * w + 1] = c1;
+            } else if (v) {
+                Hg[2 * w] += c0;
+                Hg[2 * w + 1] += c1;
+            }
+        }
+        __syncthreads();
+        if (r1 >= hi) break;
+    }
+}
+
+// ------------------------------------------------------------------ C2 ----
+__global__ void __launch_bounds__(256) k16_total(const uint32_t* __restrict__ H, int G, uint32_t* __restrict__ tot) {
+    const int d = blockIdx.x * 256 + threadIdx.x;
+    uint32_t s = 0;
+    for (int g = 0; g < G; ++g) s += H[(size_t)g * kR16 + d];
+    tot[d] = s;
+}
+
+// ------------------------------------------------------------------ C3 ----
+__global__ void __launch_bounds__(1024) k16_scan(const uint32_t* __restrict__ tot, uint32_t* __restrict__ base) {
+    __shared__ uint32_t s_w[32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int PER = kR16 / 1024;  // 64 consecutive digits per thread
+    uint32_t loc = 0;
+    for (int i = 0; i < PER; ++i) loc += tot[tid * PER + i];
+    uint32_t x = loc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    uint32_t pre = 0;
+    for (int w = 0; w < warp; ++w) pre += s_w[w];
+    uint32_t run = pre + x - loc;
+    for (int i = 0; i < PER; ++i) {
+        const uint32_t t = tot[tid * PER + i];
+        base[tid * PER + i] = run;
+        run += t;
+    }
+}
+
+// ------------------------------------------------------------------ C4 ----
+__global__ void __launch_bounds__(256) k16_offsets(uint32_t* __restrict__ H, int G, const uint32_t* __restrict__ base) {
+    const int d = blockIdx.x * 256 + threadIdx.x;
+    uint32_t run = base[d];
+    for (int g = 0; g < G; ++g) {
+        const uint32_t h = H[(size_t)g * kR16 + d];
+        H[(size_t)g * kR16 + d] = run;
+        run += h;
+    }
+}
+
+// ------------------------------------------------------------------ C5 ----
+// Block-level stable 8-bit reorder of a chunk held in shared memory
+// (A -> B), keys warp-striped, rank by warp match, per-digit scan over warps
+// and an exclusive scan over the 256 digits.
+template <typename K, bool V>
+__device__ __forceinline__ void smem_pass8(const K* A, K* B, const uint32_t* VA, uint32_t* VB, int shift,
+                                           uint32_t* s_wcnt, uint32_t* s_aux) {
+    constexpr int T = kS16Threads, KPT = kS16KPT, W = T / 32, WK = 32 * KPT;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < W * 256; i += T) s_wcnt[i] = 0;
+    __syncthreads();
+    K key[KPT];
+    uint32_t rk[KPT];
+    uint32_t* wc = s_wcnt + warp * 256;
+    const uint32_t lt = lanemask_lt(), gt = lanemask_gt();
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+        key[j] = A[warp * WK + j * 32 + lane];
+        const uint32_t d = static_cast<uint32_t>(key[j] >> shift) & 0xFFu;
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t c = wc[d];
+        rk[j] = c + __popc(peers & lt);
+        __syncwarp();
+        if ((peers & gt) == 0) wc[d] = c + __popc(peers);
+        __syncwarp();
+    }
+    uint32_t val[V ? KPT : 1];
+    if (V) {
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) val[j] = VA[warp * WK + j * 32 + lane];
+    }
+    __syncthreads();
+    uint32_t tcnt = 0, incl = 0;
+    if (tid < 256) {
+        uint32_t run = 0;
+        for (int w = 0; w < W; ++w) {
+            const uint32_t c = s_wcnt[w * 256 + tid];
+            s_wcnt[w * 256 + tid] = run;
+            run += c;
+        }
+        tcnt = incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) s_aux[warp] = incl;
+    }
+    __syncthreads();
+    if (tid < 256) {
+        uint32_t pre = 0;
+        for (int w = 0; w < (tid >> 5); ++w) pre += s_aux[w];
+        s_aux[32 + tid] = pre + incl - tcnt;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+        const uint32_t d = static_cast<uint32_t>(key[j] >> shift) & 0xFFu;
+        const uint32_t pos = s_aux[32 + d] + wc[d] + rk[j];
+        B[pos] = key[j];
+        if (V) VB[pos] = val[j];
+    }
+    __syncthreads();
+}
+
+template <typename K, bool V>
+struct Scatter16Smem {
+    static constexpr size_t keysA = 0;
+    static constexpr size_t keysB = keysA + (size_t)kS16Chunk * sizeof(K);
+    static constexpr size_t valsA = keysB + (size_t)kS16Chunk * sizeof(K);
+    static constexpr size_t valsB = valsA + (V ? (size_t)kS16Chunk * 4 : 0);
+    static constexpr size_t wcnt = valsB + (V ? (size_t)kS16Chunk * 4 : 0);
+    static constexpr size_t aux = wcnt + (size_t)(kS16Threads / 32) * 256 * 4;
+    static constexpr size_t goff = aux + (32 + 256) * 4;
+    static constexpr size_t segs = goff + (size_t)kS16Chunk * 4;
+    static constexpr size_t bytes = segs + 64 * 4;
+};
+
+template <typename K, bool V>
+__global__ void __launch_bounds__(kS16Threads, 1)
+    k16_scatter(const K* __restrict__ src, K* __restrict__ dst, const uint32_t* __restrict__ vsrc,
+                uint32_t* __restrict__ vdst, size_t n, int shift, size_t part_keys, uint32_t* __restrict__ O) {
+    using S = Scatter16Smem<K, V>;
+    constexpr int T = kS16Threads, KPT = kS16KPT, CH = kS16Chunk;
+    extern __shared__ __align__(16) unsigned char smem[];
+    K* kA = reinterpret_cast<K*>(smem + S::keysA);
+    K* kB = reinterpret_cast<K*>(smem + S::keysB);
+    uint32_t* vA = reinterpret_cast<uint32_t*>(smem + S::valsA);
+    uint32_t* vB = reinterpret_cast<uint32_t*>(smem + S::valsB);
+    uint32_t* s_wcnt = reinterpret_cast<uint32_t*>(smem + S::wcnt);
+    uint32_t* s_aux = reinterpret_cast<uint32_t*>(smem + S::aux);
+    uint32_t* s_goff = reinterpret_cast<uint32_t*>(smem + S::goff);
+    uint32_t* s_seg = reinterpret_cast<uint32_t*>(smem + S::segs);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const size_t g = blockIdx.x;
+    const size_t lo = g * part_keys;
+    const size_t hi = min(n, lo + part_keys);
+    uint32_t* Og = O + g * kR16;
+
+    for (size_t c0 = lo; c0 < hi; c0 += CH) {
+        const uint32_t valid = (uint32_t)min((size_t)CH, hi - c0);
+        for (uint32_t i = tid; i < (uint32_t)CH; i += T) {
+            kA[i] = i < valid ? src[c0 + i] : ~K(0);
+            if (V) vA[i] = i < valid ? vsrc[c0 + i] : 0u;
+        }
+        __syncthreads();
+        // stable sort of the chunk by the 16-bit digit: low byte, then high byte
+        smem_pass8<K, V>(kA, kB, vA, vB, shift, s_wcnt, s_aux);
+        smem_pass8<K, V>(kB, kA, vB, vA, shift + 8, s_wcnt, s_aux);
+
+        // segment starts: blocked arrangement, max-scan of head positions
+        const int i0 = tid * KPT;
+        uint32_t d[KPT], st[KPT];
+        uint32_t prevd = i0 > 0 ? static_cast<uint32_t>(kA[i0 - 1] >> shift) & 0xFFFFu : 0xFFFFFFFFu;
+        uint32_t run = 0;
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            d[j] = static_cast<uint32_t>(kA[i0 + j] >> shift) & 0xFFFFu;
+            if (d[j] != prevd) run = (uint32_t)(i0 + j) + 1;  // head position + 1 (0 = none yet)
+            st[j] = run;
+            prevd = d[j];
+        }
+        uint32_t x = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x = max(x, y);
+        }
+        if (lane == 31) s_seg[warp] = x;
+        __syncthreads();
+        uint32_t carry = 0;
+        for (int w = 0; w < warp; ++w) carry = max(carry, s_seg[w]);
+        const uint32_t prev_lane = __shfl_up_sync(0xffffffffu, x, 1);
+        if (lane > 0) carry = max(carry, prev_lane);
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            st[j] = (st[j] ? st[j] : carry) - 1;  // segment start of position i0+j
+            if ((uint32_t)(i0 + j) == st[j] && (uint32_t)(i0 + j) < valid) s_goff[i0 + j] = Og[d[j]];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            const uint32_t i = (uint32_t)(i0 + j);
+            if (i >= valid) continue;
+            const uint32_t o = s_goff[st[j]] + (i - st[j]);
+            dst[o] = kA[i];
+            if (V) vdst[o] = vA[i];
+            const uint32_t dnext = j + 1 < KPT ? d[j + 1] : (i + 1 < valid ? static_cast<uint32_t>(kA[i + 1] >> shift) & 0xFFFFu : d[j]);
+            const bool last = (i + 1 == valid) || dnext != d[j];
+            if (last) Og[d[j]] = o + 1;
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------ histogram ---
+template <typename K>
+__global__ void k16_hist_all(const K* __restrict__ keys, size_t n, int P, uint32_t* __restrict__ hist) {
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const K k = keys[i];
+        for (int t = 0; t < P; ++t) atomicAdd(&hist[(size_t)t * kR16 + (static_cast<uint32_t>(k >> (16 * t)) & 0xFFFFu)], 1u);
+    }
+}
+
+// -------------------------------------------------------------- driver ----
+struct Layout16 {
+    uint32_t* H;  // [G][65536]
+    uint32_t* tot;
+    uint32_t* base;
+    void* alt_keys;
+    uint32_t* alt_vals;
+    size_t G, part, bytes;
+};
+
+static Layout16 layout16(void* ws, int key_bytes, bool has_val, size_t n) {
+    Layout16 L{};
+    L.G = (size_t)sm_count();
+    L.part = (n + L.G - 1) / L.G;
+    L.part = std::max<size_t>(1, (L.part + kS16Chunk - 1) / kS16Chunk * kS16Chunk);
+    L.G = std::max<size_t>(1, (n + L.part - 1) / L.part);
+    Carver c(ws);
+    L.H = static_cast<uint32_t*>(c.take(L.G * kR16 * 4));
+    L.tot = static_cast<uint32_t*>(c.take(kR16 * 4));
+    L.base = static_cast<uint32_t*>(c.take(kR16 * 4));
+    L.alt_keys = c.take(n * key_bytes);
+    L.alt_vals = static_cast<uint32_t*>(has_val ? c.take(n * 4) : nullptr);
+    L.bytes = c.used();
+    return L;
+}
+
+size_t radix16_ws_bytes(int key_bytes, bool has_val, size_t n) { return layout16(nullptr, key_bytes, has_val, n).bytes; }
+
+template <typename K, bool V>
+static rs_status_t sort16(const K* in, const uint32_t* vin, size_t n, int end_bit, K* out, uint32_t* vout, void* ws,
+                          cudaStream_t st) {
+    const Layout16 L = layout16(ws, sizeof(K), V, n);
+    const int P = (end_bit + 15) / 16;
+    using S = Scatter16Smem<K, V>;
+    static bool attr = false;
+    if (!attr) {
+        RS_CUDA_TRY(cudaFuncSetAttribute(k16_count<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, kR16 / 2 * 4));
+        RS_CUDA_TRY(cudaFuncSetAttribute(k16_scatter<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes));
+        attr = true;
+    }
+    K* alt = static_cast<K*>(L.alt_keys);
+    // static ping-pong: the last pass writes `out`; an in-place odd count ends in alt + copy
+    const bool inplace = (const void*)in == (const void*)out;
+    const bool flip = inplace && (P % 2 == 1);
+    const K* src = in;
+    const uint32_t* vsrc = vin;
+    for (int t = 0; t < P; ++t) {
+        const bool to_out = ((P - 1 - t) % 2 == 0) != flip;
+        K* dst = to_out ? out : alt;
+        uint32_t* vdst = V ? (to_out ? vout : L.alt_vals) : nullptr;
+        const int shift = 16 * t;
+        {
+            LaunchScope ls("r16_count", st);
+            k16_count<K><<<(unsigned)L.G, kC16Threads, kR16 / 2 * 4, st>>>(src, n, shift, L.part, L.H);
+        }
+        {
+            LaunchScope ls("r16_total", st);
+            k16_total<<<kR16 / 256, 256, 0, st>>>(L.H, (int)L.G, L.tot);
+        }
+        {
+            LaunchScope ls("r16_scan", st);
+            k16_scan<<<1, 1024, 0, st>>>(L.tot, L.base);
+        }
+        {
+            LaunchScope ls("r16_offsets", st);
+            k16_offsets<<<kR16 / 256, 256, 0, st>>>(L.H, (int)L.G, L.base);
+        }
+        {
+            LaunchScope ls("r16_scatter", st);
+            k16_scatter<K, V><<<(unsigned)L.G, kS16Threads, S::bytes, st>>>(src, dst, vsrc, vdst, n, shift, L.part, L.H);
+        }
+        src = dst;
+        vsrc = vdst;
+    }
+    if (flip) {
+        RS_CUDA_TRY(cudaMemcpyAsync(out, alt, n * sizeof(K), cudaMemcpyDeviceToDevice, st));
+        if (V) RS_CUDA_TRY(cudaMemcpyAsync(vout, L.alt_vals, n * 4, cudaMemcpyDeviceToDevice, st));
+    }
+    RS_CUDA_TRY(cudaGetLastError());
+    return RS_OK;
+}
+
+rs_status_t radix16_sort(int key_bytes, const void* keys_in, const uint32_t* vals_in, size_t n, int end_bit,
+                         void* out, uint32_t* vout, void* ws, size_t, cudaStream_t st) {
+    if (key_bytes == 4) {
+        if (vals_in)
+            return sort16<uint32_t, true>(static_cast<const uint32_t*>(keys_in), vals_in, n, end_bit,
+                                          static_cast<uint32_t*>(out), vout, ws, st);
+        return sort16<uint32_t, false>(static_cast<const uint32_t*>(keys_in), nullptr, n, end_bit,
+                                       static_cast<uint32_t*>(out), nullptr, ws, st);
+    }
+    if (vals_in)
+        return sort16<uint64_t, true>(static_cast<const uint64_t*>(keys_in), vals_in, n, end_bit,
+                                      static_cast<uint64_t*>(out), vout, ws, st);
+    return sort16<uint64_t, false>(static_cast<const uint64_t*>(keys_in), nullptr, n, end_bit,
+                                   static_cast<uint64_t*>(out), nullptr, ws, st);
+}
+
+rs_status_t radix16_histogram(int key_bytes, const void* keys, size_t n, uint32_t* hist, cudaStream_t st) {
+    const unsigned grid = (unsigned)std::min<size_t>((n + 255) / 256, (size_t)sm_count() * 8);
+    LaunchScope ls("r16_hist", st);
+    if (key_bytes == 4)
+        k16_hist_all<uint32_t><<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(keys), n, 2, hist);
+    else
+        k16_hist_all<uint64_t><<<grid, 256, 0, st>>>(static_cast<const uint64_t*>(keys), n, 4, hist);
+    RS_CUDA_TRY(cudaGetLastError());
+    return RS_OK;
+}
+
+}  // namespace rs

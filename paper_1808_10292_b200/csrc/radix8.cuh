@@ -1,0 +1,200 @@
+// Radix-256 LSD pass machinery (the paper's PR4/SR4 count-sort round,
+// PAPER.md:653-709) re-designed for sm_100a as a single-sweep pass:
+//
+//   K1 k_digit_hist   one HBM read of all keys -> every pass's 256-bin histogram
+//                     ("initial counting process", all rounds at once)
+//   K2 k_plan         exclusive prefix of the histograms -> bucket bases per pass
+//                     and portion, plus the ping-pong plan
+//                     (which passes are non-trivial, src/dst of each)
+//   K3 k_onesweep     one stable count-sort round: TMA bulk
+//                     tile load -> in-tile stable rank with warp match ->
+//                     decoupled look-back across tiles for the per-digit tile
+//                     offsets (the single-GPU form of PR's p×r counter matrix,
+//                     PAPER.md:690-694) -> shared-memory reorder ->
+//                     coalesced scatter of bucket runs.
+//   K4 k_final_copy   only when the active-pass parity leaves the result in the
+//                     scratch buffer (in-place call with an odd number of passes).
+//
+// Layout in HBM: keys SoA (u32 or u64) + optional u32 values; ping-pong between
+// the caller's `out` and the workspace `alt`; look-back status [2][T][256]
+// words, flag in the top two bits: u32 words (30-bit counts) when n < 2^30,
+// u64 words (62-bit counts) otherwise.
+#pragma once
+#include "common.cuh"
+
+namespace rs {
+
+// look-back status word: [flag P | flag A | count]
+template <typename S>
+struct Status {
+    static constexpr S kFlagA = S(1) << (sizeof(S) * 8 - 2);  // tile aggregate available
+    static constexpr S kFlagP = S(1) << (sizeof(S) * 8 - 1);  // inclusive prefix available
+    static constexpr S kValMask = kFlagA - 1;
+};
+constexpr uint64_t kNarrowStatusMaxN = (1ull << 30) - 1;  // u32 status words suffice below
+
+enum BufSel : int32_t { kSelIn = 0, kSelOut = 1, kSelAlt = 2 };
+
+struct Ctrl {
+    uint32_t tile_ctr[kMaxPasses];  // dynamic tile ids (zeroed before K1)
+    int32_t active[kMaxPasses];     // pass t is non-trivial
+    int32_t src_sel[kMaxPasses];
+    int32_t dst_sel[kMaxPasses];
+    int32_t final_copy;             // 0 none, 1 in->out, 2 alt->out
+    int32_t num_active;
+    int32_t pad[14];
+};
+
+// ------------------------------------------------------------------ K1 ----
+// hist[t][d] for pass t < P.
+// Shared-memory histograms, one copy per group of 4 warps, merged into global
+// with one atomicAdd per nonzero bin per CTA.  Also zeroes `zero_words` words
+// at `zero_ptr` (the look-back status region of the first pass).
+template <typename K, int THREADS>
+__global__ void __launch_bounds__(THREADS) k_digit_hist(const K* __restrict__ keys, size_t n, int P, int b,
+                                                       uint32_t* __restrict__ hist,
+                                                       uint32_t* __restrict__ zero_ptr,
+                                                       size_t zero_words) {
+    constexpr int COPIES = THREADS / 128;  // one histogram copy per 4 warps
+    const int R = 1 << b;                  // b == 8 here
+    extern __shared__ __align__(16) uint32_t s_hist[];  // [COPIES][P][256]
+    const int tid = threadIdx.x;
+    const size_t gtid = (size_t)blockIdx.x * THREADS + tid;
+    const size_t gstride = (size_t)gridDim.x * THREADS;
+
+    for (size_t i = gtid; i < zero_words; i += gstride) zero_ptr[i] = 0;
+
+    uint32_t* my = s_hist + (tid / 128) * P * 256;
+    const uint32_t mask = (uint32_t)R - 1;
+    for (int i = tid; i < COPIES * P * 256; i += THREADS) s_hist[i] = 0;
+    __syncthreads();
+    constexpr int VEC = 16 / sizeof(K);
+    const size_t nvec = n / VEC;
+    const uint4* vbase = reinterpret_cast<const uint4*>(keys);
+    for (size_t v = gtid; v < nvec; v += gstride) {
+        uint4 x = __ldg(vbase + v);
+        const K* ks = reinterpret_cast<const K*>(&x);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) {
+            K k = ks[e];
+            for (int t = 0; t < P; ++t) atomicAdd(&my[t * 256 + digit_of<K>(k, t * b, mask)], 1u);
+        }
+    }
+    for (size_t i = nvec * VEC + gtid; i < n; i += gstride) {
+        K k = keys[i];
+        for (int t = 0; t < P; ++t) atomicAdd(&my[t * 256 + digit_of<K>(k, t * b, mask)], 1u);
+    }
+    __syncthreads();
+    for (int i = tid; i < P * 256; i += THREADS) {
+        uint32_t s = 0;
+#pragma unroll
+        for (int c = 0; c < COPIES; ++c) s += s_hist[c * P * 256 + i];
+        if (s) atomicAdd(&hist[i], s);
+    }
+}
+
+// ------------------------------------------------------------------ K2 ----
+// One CTA of 256 threads.  bases[t][d] = Σ_{d'<d} hist[t][d'].
+// Pass t is trivial (skipped: it would be the identity permutation) iff one
+// bucket holds all n keys.  Then the ping-pong plan: the last active pass writes
+// `out`, earlier ones alternate with `alt`, the first reads `in`; an in-place
+// call with an odd count ends in `alt` and needs the final copy.
+__global__ void __launch_bounds__(256) k_plan(const uint32_t* __restrict__ hist, uint32_t n, int P,
+                                              uint32_t* __restrict__ bases, Ctrl* __restrict__ ctrl,
+                                              int inplace) {
+    __shared__ uint32_t s_warp[8];
+    __shared__ int s_active[kMaxPasses];
+    const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
+    for (int t = 0; t < P; ++t) {
+        const uint32_t tot = hist[t * 256 + d];
+        const int full = __syncthreads_or(tot == n);
+        uint32_t x = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[warp] = x;
+        __syncthreads();
+        uint32_t pre = 0;
+        for (int w = 0; w < warp; ++w) pre += s_warp[w];
+        bases[t * 256 + d] = pre + x - tot;  // exclusive over digits
+        if (d == 0) s_active[t] = !full;
+        __syncthreads();
+    }
+    if (d == 0) {
+        int k = 0;
+        for (int t = 0; t < P; ++t) k += s_active[t];
+        // dst of the i-th active pass: OUT if (k-1-i) even else ALT; flipped when
+        // in-place with odd k (the first pass must not write its own source).
+        const bool flip = inplace && (k % 2 == 1);
+        int i = 0, prev = kSelIn;
+        for (int t = 0; t < kMaxPasses; ++t) {
+            ctrl->active[t] = 0;
+            ctrl->src_sel[t] = kSelIn;
+            ctrl->dst_sel[t] = kSelIn;
+        }
+        for (int t = 0; t < P; ++t) {
+            ctrl->active[t] = s_active[t];
+            if (!s_active[t]) continue;
+            bool to_out = ((k - 1 - i) % 2 == 0) != flip;
+            int dst = to_out ? kSelOut : kSelAlt;
+            ctrl->src_sel[t] = prev;
+            ctrl->dst_sel[t] = dst;
+            prev = dst;
+            ++i;
+        }
+        ctrl->num_active = k;
+        if (k == 0) ctrl->final_copy = inplace ? 0 : 1;
+        else ctrl->final_copy = flip ? 2 : 0;
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ T* pick(int sel, T* in, T* out, T* alt) {
+    return sel == kSelIn ? in : (sel == kSelOut ? out : alt);
+}
+
+// ------------------------------------------------------------------ K3 ----
+struct PassArgs {
+    const void* keys_in;
+    void* keys_out;
+    void* keys_alt;
+    const uint32_t* vals_in;
+    uint32_t* vals_out;
+    uint32_t* vals_alt;
+    uint32_t n;
+    uint32_t num_tiles;
+    int pass;
+    int shift;
+    int P;
+    Ctrl* ctrl;
+    const uint32_t* bases;  // [P][256]
+    void* status_cur;       // [T][256] status words, zero on entry
+    void* status_next;      // [T][256], cleared here for the next pass
+};
+
+// ------------------------------------------------------------------ K4 ----
+template <typename K>
+__global__ void k_final_copy(const Ctrl* __restrict__ ctrl, const K* in, const K* alt, K* out,
+                             const uint32_t* vin, const uint32_t* valt, uint32_t* vout, size_t n) {
+    const int fc = ctrl->final_copy;
+    if (fc == 0) return;
+    const K* s = fc == 1 ? in : alt;
+    const uint32_t* vs = fc == 1 ? vin : valt;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    const size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    constexpr int VEC = 16 / sizeof(K);
+    const size_t nv = n / VEC;
+    for (size_t i = g; i < nv; i += stride)
+        reinterpret_cast<uint4*>(out)[i] = reinterpret_cast<const uint4*>(s)[i];
+    for (size_t i = nv * VEC + g; i < n; i += stride) out[i] = s[i];
+    if (vout) {
+        const size_t nv4 = n / 4;
+        for (size_t i = g; i < nv4; i += stride)
+            reinterpret_cast<uint4*>(vout)[i] = reinterpret_cast<const uint4*>(vs)[i];
+        for (size_t i = nv4 * 4 + g; i < n; i += stride) vout[i] = vs[i];
+    }
+}
+
+}  // namespace rs

@@ -1,0 +1,71 @@
+// Host-side runtime shared by the rsort translation units: error state,
+// per-kernel timing registry, device properties, workspace carving.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+
+#include "../../include/rsort.h"
+
+namespace rs {
+
+// thread-local last-error message; returns `s` for tail calls
+rs_status_t fail(rs_status_t s, const std::string& msg);
+rs_status_t cuda_fail(cudaError_t e, const char* what);
+#define RS_CUDA_TRY(expr)                                        \
+    do {                                                         \
+        cudaError_t e_ = (expr);                                 \
+        if (e_ != cudaSuccess) return ::rs::cuda_fail(e_, #expr); \
+    } while (0)
+
+// Kernel launch bookkeeping: counts every launch; when timing is enabled,
+// brackets it with events on `stream` under `name`.
+void timing_before(const char* name, cudaStream_t stream, int* slot, bool is_kernel);
+void timing_after(int slot, cudaStream_t stream);
+struct LaunchScope {
+    int slot = -1;
+    cudaStream_t st;
+    LaunchScope(const char* name, cudaStream_t s, bool is_kernel = true) : st(s) {
+        timing_before(name, s, &slot, is_kernel);
+    }
+    ~LaunchScope() { timing_after(slot, st); }
+};
+
+int sm_count();
+
+// process-wide tuning / test knobs (rs_set_option)
+struct Options {
+    bool wide_status = false;     // force 64-bit look-back status words (tests)
+    int rank_variant = 0;         // 0 ballot peers, 1 match.any, 2 atomic-OR peers
+};
+Options& options();
+
+inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// bump allocator over the caller's workspace
+struct Carver {
+    char* base;
+    size_t off = 0;
+    explicit Carver(void* b) : base(static_cast<char*>(b)) {}
+    void* take(size_t bytes) {
+        off = align_up(off, 256);
+        void* p = base ? base + off : nullptr;
+        off += bytes;
+        return p;
+    }
+    size_t used() const { return align_up(off, 256); }
+};
+
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// single-GPU sort core (radix.cu): key_bytes 4/8, vals optional, b 8/16
+size_t local_ws_bytes(int key_bytes, bool has_val, size_t n, int b);
+rs_status_t local_sort(int key_bytes, const void* keys_in, const uint32_t* vals_in, size_t n, int b,
+                       int end_bit, void* out, uint32_t* vout, void* ws, size_t ws_bytes,
+                       cudaStream_t stream);
+rs_status_t digit_histogram(int key_bytes, const void* keys, size_t n, int b, uint32_t* hist, void* ws,
+                            size_t ws_bytes, cudaStream_t stream);
+
+}  // namespace rs

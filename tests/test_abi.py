@@ -1,0 +1,101 @@
+"""C-ABI boundary checks that need no GPU: librsort.so loads, exports every
+symbol include/rsort.h declares (and nothing else), and rejects bad arguments
+before touching the device."""
+import ctypes
+import subprocess
+
+import pytest
+
+from paper_1808_10292_b200 import _abi
+from paper_1808_10292_b200.build import LIB, build
+
+RS_OK, RS_EINVAL, RS_ECAPACITY = 0, 1, 5
+
+
+@pytest.fixture(scope="module")
+def L():
+    build()
+    return _abi.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    declared = _abi.header_symbols()
+    assert len(declared) >= 20
+    for name in declared:
+        assert hasattr(L, name), name
+        assert name in _abi.SIGNATURES, f"binding lacks {name}"
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB], capture_output=True, text=True).stdout
+    exported = {ln.split()[-1] for ln in out.splitlines() if " T " in ln}
+    assert set(declared) <= exported
+    assert {s for s in exported if s.startswith("rs_")} == set(declared)
+
+
+def test_version_and_status_strings(L):
+    assert b"sm_100a" in L.rs_version()
+    assert L.rs_status_string(RS_EINVAL) == b"RS_EINVAL"
+    assert L.rs_status_string(RS_ECAPACITY) == b"RS_ECAPACITY"
+
+
+def test_workspace_sizing(L):
+    assert L.rs_workspace_bytes(4, 0, 0, 8, None) > 0
+    w8 = L.rs_workspace_bytes(4, 0, 1 << 20, 8, None)
+    assert w8 >= (1 << 20) * 4          # at least the ping-pong buffer
+    assert L.rs_workspace_bytes(8, 4, 1 << 20, 8, None) >= (1 << 20) * 12
+    assert L.rs_workspace_bytes(4, 0, 1 << 20, 16, None) >= (1 << 20) * 4
+    assert L.rs_workspace_bytes(4, 0, 100, 7, None) == 0
+    assert L.rs_workspace_bytes(3, 0, 100, 8, None) == 0
+    assert L.rs_workspace_bytes(4, 2, 100, 8, None) == 0
+    assert L.rs_output_capacity(12345, None) == 12345
+
+
+def _sort_u32(L, keys, n, b, out, cap, ws, wsb):
+    n_out = ctypes.c_size_t(0)
+    return L.rs_sort_u32(keys, n, b, None, out, cap, ctypes.byref(n_out), ws, wsb, None)
+
+
+def test_validation_before_any_launch(L):
+    fake = 0x10000  # never dereferenced: validation fails first
+    wsb = L.rs_workspace_bytes(4, 0, 1000, 8, None)
+    assert _sort_u32(L, fake, 1000, 7, fake, 1000, fake, wsb) == RS_EINVAL
+    assert b"digit_bits" in L.rs_last_error()
+    assert _sort_u32(L, None, 1000, 8, fake, 1000, fake, wsb) == RS_EINVAL
+    assert _sort_u32(L, fake + 4, 1000, 8, fake, 1000, fake, wsb) == RS_EINVAL      # misaligned
+    assert b"aligned" in L.rs_last_error()
+    assert _sort_u32(L, fake, 1000, 8, fake, 1000, fake, wsb - 1) == RS_EINVAL      # ws too small
+    assert _sort_u32(L, fake, 1 << 32, 8, fake, 1 << 32, fake, 1 << 40) == RS_EINVAL
+    assert _sort_u32(L, fake, 1000, 8, fake, 999, fake, wsb) == RS_ECAPACITY
+    assert _sort_u32(L, None, 0, 8, None, 0, None, 0) == RS_OK                       # n = 0 no-op
+    n_out = ctypes.c_size_t(0)
+    assert L.rs_sort_pairs_u64_u32(fake, None, 10, 8, None, fake, fake, 10, ctypes.byref(n_out), fake,
+                                   1 << 30, None) == RS_EINVAL
+    assert L.rs_sort_bits(4, fake, None, 10, 8, 33, fake, None, fake, 1 << 30, None) == RS_EINVAL
+    assert L.rs_sort_bits(4, fake, None, 10, 8, 0, fake, None, fake, 1 << 30, None) == RS_EINVAL
+
+
+def test_comm_argument_validation(L):
+    h = ctypes.c_void_p()
+    assert L.rs_comm_create(None, 2, 0, 0, ctypes.byref(h)) == RS_EINVAL
+    uid = (ctypes.c_char * 128)()
+    assert L.rs_comm_create(uid, 2, 2, 0, ctypes.byref(h)) == RS_EINVAL
+    assert L.rs_comm_destroy(None) == RS_OK
+    assert L.rs_comm_rank(None) == 0 and L.rs_comm_size(None) == 1
+    assert L.rs_comm_set_oversampling(None, 8) == RS_EINVAL
+
+
+def test_emulate_validation(L):
+    assert L.rs_gsd_emulate_ws_bytes(4, 0, 4, 8, 8, 1000, 1200) > 0
+    assert L.rs_gsd_emulate_ws_bytes(4, 0, 0, 8, 8, 1000, 1200) == 0
+    n_out = (ctypes.c_size_t * 2)()
+    n = (ctypes.c_size_t * 2)(10, 10)
+    arr = (ctypes.c_void_p * 2)(0x10000, 0x10000)
+    assert L.rs_gsd_emulate(4, 2, 8, 12, arr, None, n, arr, None, 100, n_out, None, None, 0x10000, 1 << 30,
+                            None) == RS_EINVAL
+
+
+def test_timing_api_without_gpu(L):
+    L.rs_timing_reset()
+    ms = ctypes.c_double(-1)
+    cnt = ctypes.c_int(-1)
+    assert L.rs_timing_query(b"", ctypes.byref(ms), ctypes.byref(cnt)) == RS_OK
+    assert cnt.value == 0 and ms.value == 0.0
+    assert L.rs_launch_count() == 0

@@ -1,0 +1,80 @@
+"""GPU parity of the GSD kernels and host plan (rs_gsd_emulate: every rank's
+steps on this GPU, device copies in place of NCCL) against the CPU GSD
+simulator (oracle/gsd.c): splitters, the p×p count matrix
+and every Y_j bit-exact."""
+import numpy as np
+import pytest
+
+import inputs
+import oracle
+import paper_1808_10292_b200 as rs
+from tests.gpu_util import dev, host
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(blocks_np, r, b, vals_np=None):
+    p = len(blocks_np)
+    dt = blocks_np[0].dtype
+    want = oracle.gsd(blocks_np, r=r, b=b, vals=vals_np)
+    got = rs.gsd_emulate([dev(x) for x in blocks_np], r=r, digit_bits=b,
+                         vals=[dev(v) for v in vals_np] if vals_np is not None else None)
+    assert got["counts"].tolist() == want["counts"].tolist()
+    assert got["splitters"].tolist() == want["splitters"].tolist()
+    for j in range(p):
+        assert (host(got["Y"][j], dt) == want["Y"][j]).all(), j
+        if vals_np is not None:
+            assert (host(got["Yv"][j], np.uint32) == want["Yv"][j]).all(), j
+    nmax = max(x.size for x in blocks_np)
+    if min(x.size for x in blocks_np) >= r * p:
+        assert max(got["n_out"]) <= nmax + nmax // r          # balance bound (R18)
+    return got
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+@pytest.mark.parametrize("dist", ["uniform", "mod16", "equal", "sorted"])
+def test_gsd_u32_matches_simulator(p, dist):
+    total = 40000 + p
+    a = inputs.gen_u32(total, 40 + p, dist)
+    cuts = np.linspace(0, total, p + 1).astype(int)
+    _check([a[cuts[k]:cuts[k + 1]] for k in range(p)], r=8, b=8)
+
+
+def test_gsd_hand_trace_spec290():
+    blocks = [np.arange(1, 16, 2, dtype=np.uint32), np.arange(2, 17, 2, dtype=np.uint32)]
+    got = _check(blocks, r=1, b=8)
+    assert [host(y, np.uint32).tolist() for y in got["Y"]] == [list(range(1, 9)), list(range(9, 17))]
+
+
+@pytest.mark.parametrize("b", [8, 16])
+def test_gsd_pairs_global_stability(b):
+    p, N = 4, 30000
+    k = inputs.gen_u64(p * N, 5, "mod1024")
+    v = inputs.iota_u32(p * N)
+    got = _check([k[i * N:(i + 1) * N] for i in range(p)], r=8, b=b, vals_np=[v[i * N:(i + 1) * N] for i in range(p)])
+    K = np.concatenate([host(y, np.uint64) for y in got["Y"]])
+    V = np.concatenate([host(y, np.uint32) for y in got["Yv"]])
+    assert oracle.pairs_stable(K, V)
+
+
+def test_gsd_uneven_and_empty_blocks():
+    blocks = [inputs.gen_u32(n, 50 + n) for n in (0, 5, 12345, 0, 70000, 3)]
+    _check(blocks, r=8, b=8)
+
+
+def test_gsd_u64_radix16():
+    p = 4
+    k = inputs.gen_u64(4 * 25000, 60)
+    _check([k[i * 25000:(i + 1) * 25000] for i in range(p)], r=8, b=16)
+
+
+def test_gsd_config4_shape_reduced():
+    """configs[3] shape (uniform u32, r=8, p=8) at 2^24 total keys."""
+    p, n = 8, 1 << 24
+    a = inputs.gen_u32(n, 4)
+    N = n // p
+    blocks = [a[k * N:(k + 1) * N] for k in range(p)]
+    got = rs.gsd_emulate([dev(x) for x in blocks], r=8, digit_bits=8)
+    Y = np.concatenate([host(y, np.uint32) for y in got["Y"]])
+    assert (Y == oracle.sr(a, 8)).all()
+    assert max(got["n_out"]) <= N + N // 8

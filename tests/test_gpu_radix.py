@@ -1,0 +1,257 @@
+"""GPU parity of the single-GPU radix sort (through the C ABI) against the
+serial oracle: bit-exact after every pass, for every key type, digit width,
+size edge case and BASELINE distribution (configs 1-3 at full size; configs
+4-5 at p = 1 by invariants and sampled order statistics)."""
+import numpy as np
+import pytest
+import torch
+
+import inputs
+import oracle
+import paper_1808_10292_b200 as rs
+from tests.gpu_util import dev, free_dev_gb, free_host_gb, host
+
+pytestmark = pytest.mark.gpu
+
+TILE32 = 512 * 12   # u32 keys-only tile (radix.cu Tune)
+TILE64 = 512 * 8    # u64 keys / pairs tile
+
+
+def _sort_u32(a, b, inplace=True):
+    t = dev(a)
+    if inplace:
+        rs.sort(t, digit_bits=b)
+        return host(t, np.uint32)
+    out = torch.empty_like(t)
+    rs.sort(t, digit_bits=b, out=out)
+    assert (host(t, np.uint32) == a).all(), "input clobbered by an out-of-place sort"
+    return host(out, np.uint32)
+
+
+def test_native_library_runs():
+    a = inputs.gen_u32(5000, 1)
+    rs.lib().rs_timing_reset()
+    got = _sort_u32(a, 8)
+    torch.cuda.synchronize()
+    assert rs.lib().rs_launch_count() >= 6
+    assert (got == oracle.sr(a, 8)).all()
+
+
+@pytest.mark.parametrize("b", [8, 16])
+def test_histogram_parity(b):
+    a = inputs.gen_u32(3 * TILE32 + 1234, 21)
+    h = rs.digit_histogram(dev(a), b).cpu().numpy().view(np.uint32)
+    assert (h.astype(np.uint64) == oracle.hist(a, b)).all()
+    k = inputs.gen_u64(2 * TILE64 + 77, 22)
+    h = rs.digit_histogram(dev(k), b).cpu().numpy().view(np.uint32)
+    assert (h.astype(np.uint64) == oracle.hist(k, b)).all()
+
+
+@pytest.mark.parametrize("n", [3 * TILE32 + 1234, (1 << 20) + 7])
+@pytest.mark.parametrize("b", [8, 16])
+def test_every_pass_u32(n, b):
+    """After pass t the array equals the oracle's array after round t (bit-exact)."""
+    a = inputs.gen_u32(n, 23)
+    for t in range(1, 32 // b + 1):
+        got = host(rs.sort_bits(dev(a), end_bit=b * t, digit_bits=b), np.uint32)
+        assert (got == oracle.sr(a, b, rounds=t)).all(), f"pass {t}"
+
+
+@pytest.mark.parametrize("b", [8, 16])
+def test_every_pass_u64_and_pairs(b):
+    n = 5 * TILE64 + 999
+    k = inputs.gen_u64(n, 24)
+    v = inputs.iota_u32(n)
+    for t in range(1, 64 // b + 1):
+        got = host(rs.sort_bits(dev(k), end_bit=b * t, digit_bits=b), np.uint64)
+        assert (got == oracle.sr(k, b, rounds=t)).all(), f"u64 pass {t}"
+        gk, gv = rs.sort_bits(dev(k), end_bit=b * t, digit_bits=b, vals=dev(v))
+        wk, wv = oracle.sr(k, b, rounds=t, vals=v)
+        assert (host(gk, np.uint64) == wk).all() and (host(gv, np.uint32) == wv).all(), f"pairs pass {t}"
+
+
+EDGE_N = [1, 2, 3, 31, 32, 33, 1000, TILE64 - 1, TILE64, TILE64 + 1, TILE32 - 1, TILE32, TILE32 + 1,
+          2 * TILE32 + 3, 7 * TILE32 + 4095]
+
+
+@pytest.mark.parametrize("b", [8, 16])
+@pytest.mark.parametrize("inplace", [True, False])
+def test_edge_sizes_u32(b, inplace):
+    for n in EDGE_N:
+        a = inputs.gen_u32(n, 25 + n)
+        assert (_sort_u32(a, b, inplace) == oracle.sr(a, b)).all(), n
+
+
+@pytest.mark.parametrize("b", [8, 16])
+def test_edge_sizes_u64_and_pairs(b):
+    for n in EDGE_N:
+        k = inputs.gen_u64(n, 26 + n, "mod1024" if n % 2 else "uniform")
+        v = inputs.iota_u32(n)
+        t = dev(k)
+        rs.sort(t, digit_bits=b)
+        assert (host(t, np.uint64) == oracle.sr(k, b)).all(), n
+        tk, tv = dev(k), dev(v)
+        ok_, ov_ = torch.empty_like(tk), torch.empty_like(tv)
+        rs.sort_pairs(tk, tv, digit_bits=b, out_keys=ok_, out_vals=ov_)
+        wk, wv = oracle.sr(k, b, vals=v)
+        assert (host(ok_, np.uint64) == wk).all() and (host(ov_, np.uint32) == wv).all(), n
+        assert oracle.pairs_stable(host(ok_, np.uint64), host(ov_, np.uint32))
+
+
+def test_empty_input():
+    t = torch.empty(0, dtype=torch.int32, device="cuda")
+    rs.sort(t)
+    k = torch.empty(0, dtype=torch.int64, device="cuda")
+    v = torch.empty(0, dtype=torch.int32, device="cuda")
+    rs.sort_pairs(k, v)
+
+
+@pytest.mark.parametrize("dist", ["uniform", "mod16", "gauss", "sorted", "reversed", "equal", "half"])
+@pytest.mark.parametrize("b", [8, 16])
+def test_distributions(dist, b):
+    a = inputs.gen_u32((1 << 20) + 3, 3, dist)
+    want = oracle.sr(a, b)
+    assert (_sort_u32(a, b, True) == want).all()
+    assert (_sort_u32(a, b, False) == want).all()
+
+
+def test_extreme_keys():
+    a = inputs.gen_u32(100003, 9)
+    a = np.where(a & np.uint32(1), np.uint32(0xFFFFFFFF), np.uint32(0)).astype(np.uint32)
+    for b in (8, 16):
+        assert (_sort_u32(a, b) == np.sort(a)).all()
+    k = inputs.gen_u64(50001, 9)
+    k = np.where(k & np.uint64(1), np.uint64(0xFFFFFFFFFFFFFFFF), np.uint64(0)).astype(np.uint64)
+    t = dev(k)
+    rs.sort(t)
+    assert (host(t, np.uint64) == np.sort(k)).all()
+
+
+def test_config1():
+    """BASELINE configs[0]: n=2^20 uniform u32 seed 1, radix-256, bit-exact."""
+    a = inputs.gen_u32(1 << 20, 1, "uniform")
+    assert (_sort_u32(a, 8) == oracle.sr(a, 8)).all()
+
+
+def test_config2_radix256_vs_radix65536():
+    """BASELINE configs[1]: 2^24 keys in [0,2^31) seed 2; PR4 and PR2 both bit-exact."""
+    a = inputs.gen_u32(1 << 24, 2, "half")
+    want = oracle.sr(a, 8)
+    g8 = _sort_u32(a, 8)
+    g16 = _sort_u32(a, 16)
+    assert (g8 == want).all() and (g16 == want).all()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("dist", ["uniform", "mod16", "gauss", "sorted", "reversed", "equal"])
+def test_config3_full_size(dist):
+    """BASELINE configs[2]: 2^27 u32 keys, six distributions, seed 3, bit-exact."""
+    a = inputs.gen_u32(1 << 27, 3, dist)
+    want = oracle.sr(a, 8)
+    assert (_sort_u32(a, 8) == want).all()
+
+
+@pytest.mark.slow
+def test_config4_single_gpu_full_size():
+    """BASELINE configs[3] at p=1 (the bench.py N=1 workload): 2^31 u32 keys,
+    seed 4.  Too large for the serial oracle in a test: sortedness, multiset hash
+    against the input, and 64 sampled order statistics checked one by one."""
+    n = 1 << 31
+    if free_host_gb() < 20 or free_dev_gb() < 20:
+        pytest.skip(f"needs ~20 GB host/device (host {free_host_gb():.0f}, dev {free_dev_gb():.0f})")
+    a = inputs.gen_u32(n, 4)
+    h_in = oracle.multiset_hash(a)
+    t = dev(a)
+    rs.sort(t, digit_bits=8)
+    got = host(t, np.uint32)
+    del t
+    torch.cuda.empty_cache()
+    assert oracle.is_nondecreasing(got)
+    assert oracle.multiset_hash(got) == h_in
+    pos = np.unique(np.linspace(0, n - 1, 64).astype(np.uint64))
+    assert oracle.check_order_stats_u32(a, pos, got[pos.astype(np.int64)]) == 0
+
+
+@pytest.mark.slow
+def test_config5_single_gpu_full_size():
+    """BASELINE configs[4] at p=1: 2^30 (u64 key, u32 payload = index) pairs,
+    seed 5, 8 radix-256 passes; stability via payload order."""
+    n = 1 << 30
+    if free_host_gb() < 30 or free_dev_gb() < 30:
+        pytest.skip("needs ~30 GB host/device")
+    k = inputs.gen_u64(n, 5)
+    v = inputs.iota_u32(n)
+    h_in = oracle.multiset_hash(k, v)
+    tk, tv = dev(k), dev(v)
+    del k, v
+    rs.sort_pairs(tk, tv, digit_bits=8)
+    gk, gv = host(tk, np.uint64), host(tv, np.uint32)
+    del tk, tv
+    torch.cuda.empty_cache()
+    assert oracle.pairs_stable(gk, gv)
+    assert oracle.multiset_hash(gk, gv) == h_in
+
+
+def test_narrow_pairs_stability_at_scale():
+    """configs[4] narrow-range variant: key = z mod 1024, many equal keys."""
+    n = (1 << 22) + 5
+    k = inputs.gen_u64(n, 5, "mod1024")
+    v = inputs.iota_u32(n)
+    for b in (8, 16):
+        tk, tv = dev(k), dev(v)
+        rs.sort_pairs(tk, tv, digit_bits=b)
+        wk, wv = oracle.sr(k, b, vals=v)
+        assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
+
+
+@pytest.fixture
+def option():
+    set_ = []
+
+    def _set(name, value):
+        assert rs.lib().rs_set_option(name.encode(), value) == 0
+        set_.append(name)
+    yield _set
+    for name in set_:
+        rs.lib().rs_set_option(name.encode(), 0)
+
+
+@pytest.mark.parametrize("kind", ["u32", "u64", "pairs"])
+def test_wide_status_lookback(option, kind):
+    """64-bit look-back status words (used when n >= 2^30, configs 4/5 at p = 1)
+    forced at small n, every pass checked, ragged tail."""
+    option("wide_status", 1)
+    tile = TILE32 if kind == "u32" else TILE64
+    n = 11 * tile + 517
+    if kind == "u32":
+        a = inputs.gen_u32(n, 31)
+        for t in range(1, 5):
+            got = host(rs.sort_bits(dev(a), end_bit=8 * t, digit_bits=8), np.uint32)
+            assert (got == oracle.sr(a, 8, rounds=t)).all(), t
+        assert (_sort_u32(a, 8) == oracle.sr(a, 8)).all()
+    else:
+        k = inputs.gen_u64(n, 32, "mod1024" if kind == "pairs" else "uniform")
+        v = inputs.iota_u32(n)
+        if kind == "u64":
+            t = dev(k)
+            rs.sort(t)
+            assert (host(t, np.uint64) == oracle.sr(k, 8)).all()
+        else:
+            tk, tv = dev(k), dev(v)
+            rs.sort_pairs(tk, tv)
+            wk, wv = oracle.sr(k, 8, vals=v)
+            assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_rank_variants(option, variant):
+    """match.any (1) and atomic-OR (2) peer masks give the same stable ranks."""
+    option("rank_variant", variant)
+    a = inputs.gen_u32(5 * TILE32 + 3, 33)
+    assert (_sort_u32(a, 8) == oracle.sr(a, 8)).all()
+    k = inputs.gen_u64(3 * TILE64 + 5, 34, "mod1024")
+    v = inputs.iota_u32(k.size)
+    tk, tv = dev(k), dev(v)
+    rs.sort_pairs(tk, tv)
+    wk, wv = oracle.sr(k, 8, vals=v)
+    assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
