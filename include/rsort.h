@@ -164,6 +164,12 @@ rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits,
  *   "rank_variant"   in-tile ranking: 0 = ballot peer masks (default), 2 = peer
  *                    masks by shared-memory atomic OR,
  *                    1 = match.any.
+ *   "pass_design"    radix-256 pass kernel: 2 = early counts + tile prefetch,
+ *                    look-back after ranking (default); 1 = early counts + tile
+ *                    prefetch with a dedicated look-back warp; 0 = classic single
+ *                    sweep (rank, look-back, reorder, store).
+ *   "debug_skip"     timing ablations, OUTPUT INVALID: bit 0 no look-back,
+ *                    bit 1 no ranking, bit 2 no global store, bit 3 no reorder.
  * Returns RS_EINVAL for an unknown name or a negative value. */
 rs_status_t rs_set_option(const char* name, long long value);
 

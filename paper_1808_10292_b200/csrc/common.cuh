@@ -20,6 +20,11 @@ __device__ __forceinline__ uint32_t lanemask_gt() {
     return m;
 }
 
+// named barrier over `count` threads (a multiple of 32) of the CTA
+__device__ __forceinline__ void named_barrier_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+
 // ------------------------------------------------ GPU-scope status words --
 // Look-back status words pack flag and value in one 32-bit word, so a single
 // relaxed access is atomic; no ordering with other data is needed.

@@ -152,7 +152,13 @@ __global__ void __launch_bounds__(THREADS, MINB) k_onesweep(PassArgs a) {
         for (int j = 0; j < KPT; ++j) key[j] = s_keys[warp * WK + j * 32 + lane];
         // running count of digit d in this warp lives at wc[d * CS + CS - 1]
         uint32_t* wc = s_wcnt + warp * R * CS + (CS - 1);
-        if (VARIANT == 2) {
+        if (a.debug_skip & 2) {  // ablation: no ranking
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) {
+                if (j & 1) rk[j >> 1] |= (uint32_t)(j * 32 + lane) << 16;
+                else rk[j >> 1] = (uint32_t)(j * 32 + lane);
+            }
+        } else if (VARIANT == 2) {
             // peers by atomic OR of lane bits into a per-warp, per-digit mask word
             // that sits next to the digit's running count: (mask, count) pairs
             uint2* wmc = reinterpret_cast<uint2*>(s_wcnt) + warp * R;
@@ -225,6 +231,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_onesweep(PassArgs a) {
         // ---- a5 (reorder into shared memory)
 #pragma unroll
         for (int j = 0; j < KPT; ++j) {
+            if (a.debug_skip & 8) break;  // ablation: no reorder
             const uint32_t d = digit_of<K>(key[j], shift, mask);
             const uint32_t r = (rk[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu;
             const uint32_t pos = s_texcl[d] + wc[d * CS] + r;
@@ -235,7 +242,9 @@ __global__ void __launch_bounds__(THREADS, MINB) k_onesweep(PassArgs a) {
         // ---- a4: decoupled look-back
         if (tid < R) {
             S excl = 0;
-            if (tile != 0) {
+            if (tile != 0 && (a.debug_skip & 1)) {
+                st_relaxed_gpu(my_status, ST::kFlagP | (S)cnt_pub);  // ablation: no look-back
+            } else if (tile != 0) {
                 // windowed walk: LB predecessors per L2 round trip (tile 0 always
                 // holds an inclusive prefix, so the walk never passes it)
                 constexpr int LB = 8;
@@ -265,6 +274,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_onesweep(PassArgs a) {
         // ---- a5 (store): bucket runs leave as coalesced bursts
 #pragma unroll 4
         for (uint32_t i = tid; i < valid; i += THREADS) {
+            if (a.debug_skip & 4) break;  // ablation: no global store
             const K k = s_keys[i];
             const uint32_t g = s_gofs[digit_of<K>(k, shift, mask)] + i;
             dst[g] = k;

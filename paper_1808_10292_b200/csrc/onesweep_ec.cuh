@@ -1,0 +1,325 @@
+// K3 (early counts) — one stable count-sort round of radix 256,
+// pipelined so that the cross-tile look-back and the next tile's load overlap
+// the in-tile ranking.  Persistent CTAs of RT ranking threads + 1 look-back warp:
+//
+//   [load]   TMA bulk copy of tile k into s_in (issued during tile k-1's store)
+//   [count]  ranking warps: per-warp digit histogram by shared-memory atomics
+//   [offset] thread d: tile count, in-tile digit offset (scan over digits),
+//            per-warp start offsets (scan over warps); publish the tile count to
+//            the look-back status (flag A, or P for tile 0)  — PAPER.md:690-694
+//   [rank]   ranking warps: stable warp rank from 8 ballots, key written straight
+//            to its in-tile sorted slot in s_out
+//            ‖ look-back warp: windowed decoupled look-back for all 256 digits,
+//              publishes the inclusive prefix (flag P), computes store offsets
+//   [next]   thread 0 takes the next tile id and starts its TMA load into s_in
+//   [store]  consecutive threads store consecutive s_out slots: each bucket run
+//            is a coalesced burst at base[d] + prefix[d] + offset
+#pragma once
+#include "radix8.cuh"
+
+namespace rs {
+
+template <typename K, bool HAS_VAL, int RT, int KPT, bool LBW = true>
+struct OnesweepEcCfg {
+    static constexpr int R = 256;
+    static constexpr int W = RT / 32;                 // ranking warps
+    static constexpr int THREADS = RT + (LBW ? 32 : 0);  // + one look-back warp (LBW)
+    static constexpr int WK = 32 * KPT;
+    static constexpr int TILE = RT * KPT;
+    static constexpr size_t in_off = 0;
+    static constexpr size_t out_off = in_off + (size_t)TILE * sizeof(K);
+    static constexpr size_t vin_off = out_off + (size_t)TILE * sizeof(K);
+    static constexpr size_t vout_off = vin_off + (HAS_VAL ? (size_t)TILE * 4 : 0);
+    static constexpr size_t wc_off = vout_off + (HAS_VAL ? (size_t)TILE * 4 : 0);
+    static constexpr size_t texcl_off = wc_off + (size_t)W * R * 4;
+    static constexpr size_t tcnt_off = texcl_off + R * 4;
+    static constexpr size_t gofs_off = tcnt_off + R * 4;
+    static constexpr size_t misc_off = gofs_off + R * 4;
+    static constexpr size_t bar_off = misc_off + 64 * 4;
+    static constexpr size_t smem_bytes = bar_off + 16;
+};
+
+template <typename K>
+__device__ __forceinline__ uint32_t digit8(K k, int shift) {
+    return static_cast<uint32_t>(k >> shift) & 0xFFu;
+}
+template <>
+__device__ __forceinline__ uint32_t digit8<uint32_t>(uint32_t k, int shift) {
+    return __byte_perm(k, 0u, 0x4440u + (uint32_t)(shift >> 3));  // byte shift/8, zero-extended
+}
+
+// peers with the same 8-bit digit in this warp (8 ballots; see onesweep.cuh)
+__device__ __forceinline__ uint32_t peers8(uint32_t d) {
+    // Lanes that disagree with me on bit b are the set bits of ballot(bit b) ^ s_b,
+    // s_b = my bit b as 0 / 0xffffffff; peers = ~OR_b(...).  s_b in one PRMT: a
+    // multiply by 0x10204080 moves nibble bit i to the MSB of byte i, and PRMT's
+    // sign-replicate selector broadcasts that MSB to all four bytes.
+    uint32_t dis;
+    asm("{\n"
+        ".reg .pred p;\n"
+        ".reg .b32 t, s, m, ylo, yhi;\n"
+        "and.b32 t, %1, 15;\n"
+        "mul.lo.u32 ylo, t, 0x10204080;\n"
+        "shr.u32 t, %1, 4;\n"
+        "mul.lo.u32 yhi, t, 0x10204080;\n"
+        "mov.b32 %0, 0;\n"
+#define RS_PEER_BIT(B, Y, SEL)                     \
+    "and.b32 t, %1, " #B ";\n"                    \
+    "setp.ne.u32 p, t, 0;\n"                      \
+    "vote.sync.ballot.b32 m, p, 0xffffffff;\n"    \
+    "prmt.b32 s, " #Y ", 0, " #SEL ";\n"          \
+    "xor.b32 m, m, s;\n"                          \
+    "or.b32 %0, %0, m;\n"
+        RS_PEER_BIT(1, ylo, 0x8888) RS_PEER_BIT(2, ylo, 0x9999)
+        RS_PEER_BIT(4, ylo, 0xAAAA) RS_PEER_BIT(8, ylo, 0xBBBB)
+        RS_PEER_BIT(16, yhi, 0x8888) RS_PEER_BIT(32, yhi, 0x9999)
+        RS_PEER_BIT(64, yhi, 0xAAAA) RS_PEER_BIT(128, yhi, 0xBBBB)
+#undef RS_PEER_BIT
+        "}\n"
+        : "=r"(dis)
+        : "r"(d));
+    return ~dis;
+}
+
+// LBW: a dedicated look-back warp runs the look-back concurrently with the
+// ranking; otherwise the ranking threads run it (one digit each) after ranking.
+template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, bool LBW>
+__global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassArgs a) {
+    using ST = Status<S>;
+    using C = OnesweepEcCfg<K, HAS_VAL, RT, KPT, LBW>;
+    constexpr int R = C::R, W = C::W, WK = C::WK, TILE = C::TILE, THREADS = C::THREADS;
+    static_assert(RT >= R, "one ranking thread per digit in the offset phase");
+    extern __shared__ __align__(128) unsigned char smem[];
+    K* s_in = reinterpret_cast<K*>(smem + C::in_off);
+    K* s_out = reinterpret_cast<K*>(smem + C::out_off);
+    uint32_t* s_vin = reinterpret_cast<uint32_t*>(smem + C::vin_off);
+    uint32_t* s_vout = reinterpret_cast<uint32_t*>(smem + C::vout_off);
+    uint32_t* s_wc = reinterpret_cast<uint32_t*>(smem + C::wc_off);
+    uint32_t* s_texcl = reinterpret_cast<uint32_t*>(smem + C::texcl_off);
+    uint32_t* s_tcnt = reinterpret_cast<uint32_t*>(smem + C::tcnt_off);
+    uint32_t* s_gofs = reinterpret_cast<uint32_t*>(smem + C::gofs_off);
+    uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + C::misc_off);
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + C::bar_off);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    Ctrl* ctrl = a.ctrl;
+    S* const status = static_cast<S*>(a.status_cur);
+
+    // clear the next pass's status rows (no reader in this launch)
+    for (size_t i = (size_t)blockIdx.x * THREADS + tid; i < (size_t)a.num_tiles * R; i += (size_t)gridDim.x * THREADS)
+        static_cast<S*>(a.status_next)[i] = 0;
+    if (!ctrl->active[a.pass]) return;
+
+    const int ss = ctrl->src_sel[a.pass], ds = ctrl->dst_sel[a.pass];
+    const K* src = pick<const K>(ss, static_cast<const K*>(a.keys_in), static_cast<const K*>(a.keys_out),
+                                 static_cast<const K*>(a.keys_alt));
+    K* dst = pick<K>(ds, const_cast<K*>(static_cast<const K*>(a.keys_in)), static_cast<K*>(a.keys_out),
+                     static_cast<K*>(a.keys_alt));
+    const uint32_t* vsrc = nullptr;
+    uint32_t* vdst = nullptr;
+    if (HAS_VAL) {
+        vsrc = pick<const uint32_t>(ss, a.vals_in, a.vals_out, a.vals_alt);
+        vdst = pick<uint32_t>(ds, const_cast<uint32_t*>(a.vals_in), a.vals_out, a.vals_alt);
+    }
+    const int shift = a.shift;
+    const uint32_t lt = lanemask_lt(), gt = lanemask_gt();
+
+    // issue the bulk load of `t` into s_in (thread 0 only)
+    auto issue_load = [&](uint32_t t) {
+        const size_t base = (size_t)t * TILE;
+        const uint32_t valid = (uint32_t)min((size_t)TILE, (size_t)a.n - base);
+        const uint32_t kbytes = (valid * (uint32_t)sizeof(K)) & ~15u;
+        const uint32_t vbytes = HAS_VAL ? ((valid * 4u) & ~15u) : 0u;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(s_bar, kbytes + vbytes);
+        if (kbytes) bulk_g2s(s_in, src + base, kbytes, s_bar);
+        if (HAS_VAL && vbytes) bulk_g2s(s_vin, vsrc + base, vbytes, s_bar);
+    };
+
+    if (tid == 0) {
+        mbar_init(s_bar, 1);
+        fence_mbar_init();
+        const uint32_t t0 = atomicAdd(&ctrl->tile_ctr[a.pass], 1u);
+        s_misc[0] = t0;
+        if (t0 < a.num_tiles) issue_load(t0);
+    }
+    for (int i = tid; i < W * R; i += THREADS) s_wc[i] = 0;
+    __syncthreads();
+    uint32_t tile = s_misc[0];
+    uint32_t phase = 0;
+
+    while (tile < a.num_tiles) {
+        const size_t base = (size_t)tile * TILE;
+        const uint32_t valid = (uint32_t)min((size_t)TILE, (size_t)a.n - base);
+
+        // ---- [load] wait for the tile; ragged tail by scalar loads, all-ones padding
+        if (valid < (uint32_t)TILE) {
+            const uint32_t kdone = ((valid * (uint32_t)sizeof(K)) & ~15u) / sizeof(K);
+            for (uint32_t i = kdone + tid; i < (uint32_t)TILE; i += THREADS)
+                s_in[i] = i < valid ? src[base + i] : ~K(0);
+            if (HAS_VAL) {
+                const uint32_t vdone = ((valid * 4u) & ~15u) / 4;
+                for (uint32_t i = vdone + tid; i < (uint32_t)TILE; i += THREADS)
+                    s_vin[i] = i < valid ? vsrc[base + i] : 0u;
+            }
+        }
+        mbar_wait_parity(s_bar, phase);
+        phase ^= 1u;
+        __syncthreads();
+
+        // ---- [count] per-warp digit histograms
+        if (warp < W) {
+            uint32_t* wc = s_wc + warp * R;
+            const K* in = s_in + warp * WK + lane;
+#pragma unroll 8
+            for (int j = 0; j < KPT; ++j) atomicAdd(&wc[digit8<K>(in[j * 32], shift)], 1u);
+        }
+        __syncthreads();
+
+        // ---- [offset] thread d: tile count, in-tile offset, warp start offsets; publish
+        if (tid < R) {
+            uint32_t c[W];
+            uint32_t tcnt = 0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                c[w] = s_wc[w * R + tid];
+                tcnt += c[w];
+            }
+            uint32_t incl = tcnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) s_misc[8 + warp] = incl;
+            const uint32_t pub = tcnt - (tid == R - 1 ? (uint32_t)TILE - valid : 0u);  // drop padding
+            s_tcnt[tid] = pub;
+            st_relaxed_gpu(status + (size_t)tile * R + tid, (tile == 0 ? ST::kFlagP : ST::kFlagA) | (S)pub);
+            named_barrier_sync(1, R);
+            uint32_t pre = 0;
+            for (int w = 0; w < (tid >> 5); ++w) pre += s_misc[8 + w];
+            uint32_t run = pre + incl - tcnt;  // in-tile offset of digit tid
+            s_texcl[tid] = run;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                s_wc[w * R + tid] = run;
+                run += c[w];
+            }
+        }
+        __syncthreads();
+
+        if (LBW && warp == W) {
+            // ---- [look-back] one warp, 8 digits per lane (in G groups), windowed walk
+            constexpr int DPL = R / 32, G = sizeof(S) == 4 ? 1 : 2, DG = DPL / G, LB = 4;
+#pragma unroll 1
+            for (int g = 0; g < G; ++g) {
+                S excl[DG];
+#pragma unroll
+                for (int k = 0; k < DG; ++k) excl[k] = 0;
+                const int d0 = lane + 32 * DG * g;  // digits d0 + 32k, k < DG
+                if (tile != 0) {
+                    uint32_t done = 0;  // bit k: digit d0 + 32k finished
+                    int64_t off = 1;    // next predecessor distance to read
+                    while (done != (1u << DG) - 1) {
+                        S v[DG][LB];
+#pragma unroll
+                        for (int k = 0; k < DG; ++k)
+#pragma unroll
+                            for (int i = 0; i < LB; ++i)
+                                v[k][i] = (!(done >> k & 1) && off + i <= (int64_t)tile)
+                                              ? ld_relaxed_gpu(status + (size_t)(tile - off - i) * R + d0 + 32 * k)
+                                              : ST::kFlagP;
+#pragma unroll
+                        for (int k = 0; k < DG; ++k) {
+#pragma unroll
+                            for (int i = 0; i < LB; ++i) {
+                                if (done >> k & 1) break;
+                                S s = v[k][i];
+                                while ((s & (ST::kFlagA | ST::kFlagP)) == 0)
+                                    s = ld_relaxed_gpu(status + (size_t)(tile - off - i) * R + d0 + 32 * k);
+                                excl[k] += s & ST::kValMask;
+                                if (s & ST::kFlagP) done |= 1u << k;
+                            }
+                        }
+                        off += LB;
+                    }
+#pragma unroll
+                    for (int k = 0; k < DG; ++k)
+                        st_relaxed_gpu(status + (size_t)tile * R + d0 + 32 * k,
+                                       ST::kFlagP | (excl[k] + (S)s_tcnt[d0 + 32 * k]));
+                }
+#pragma unroll
+                for (int k = 0; k < DG; ++k) {
+                    const int d = d0 + 32 * k;
+                    s_gofs[d] = a.bases[a.pass * R + d] + (uint32_t)excl[k] - s_texcl[d];
+                }
+            }
+        } else {
+            // ---- [rank] stable warp rank, straight to the sorted slot
+            uint32_t* wc = s_wc + warp * R;
+            const int ibase = warp * WK + lane;
+#pragma unroll 4
+            for (int j = 0; j < KPT; ++j) {
+                const int idx = ibase + j * 32;
+                const K k = s_in[idx];
+                const uint32_t d = digit8<K>(k, shift);
+                const uint32_t peers = peers8(d);
+                const uint32_t cnt = wc[d];
+                const uint32_t pos = cnt + __popc(peers & lt);
+                s_out[pos] = k;
+                if (HAS_VAL) s_vout[pos] = s_vin[idx];
+                __syncwarp();
+                if ((peers & gt) == 0) wc[d] = cnt + __popc(peers);
+                __syncwarp();
+            }
+        }
+        if (!LBW && tid < R) {
+            // ---- [look-back] after ranking, one digit per thread, windowed walk
+            S excl = 0;
+            if (tile != 0) {
+                constexpr int LB = 8;
+                const S* sp = status + (size_t)(tile - 1) * R + tid;
+                int64_t left = (int64_t)tile;
+                bool done = false;
+                while (!done) {
+                    S v[LB];
+#pragma unroll
+                    for (int i = 0; i < LB; ++i) v[i] = i < left ? ld_relaxed_gpu(sp - (size_t)i * R) : ST::kFlagP;
+#pragma unroll
+                    for (int i = 0; i < LB; ++i) {
+                        if (done) break;
+                        while ((v[i] & (ST::kFlagA | ST::kFlagP)) == 0) v[i] = ld_relaxed_gpu(sp - (size_t)i * R);
+                        excl += v[i] & ST::kValMask;
+                        done = (v[i] & ST::kFlagP) != 0;
+                    }
+                    sp -= (size_t)LB * R;
+                    left -= LB;
+                }
+                st_relaxed_gpu(status + (size_t)tile * R + tid, ST::kFlagP | (excl + (S)s_tcnt[tid]));
+            }
+            s_gofs[tid] = a.bases[a.pass * R + tid] + (uint32_t)excl - s_texcl[tid];
+        }
+        __syncthreads();
+
+        // ---- [next] take the next tile and start its load; s_in is free now
+        if (tid == 0) {
+            const uint32_t nt = atomicAdd(&ctrl->tile_ctr[a.pass], 1u);
+            s_misc[0] = nt;
+            if (nt < a.num_tiles) issue_load(nt);
+        }
+        for (int i = tid; i < W * R; i += THREADS) s_wc[i] = 0;
+
+        // ---- [store] bucket runs leave as coalesced bursts
+#pragma unroll 4
+        for (uint32_t i = tid; i < valid; i += THREADS) {
+            const K k = s_out[i];
+            const uint32_t g = s_gofs[digit8<K>(k, shift)] + i;
+            dst[g] = k;
+            if (HAS_VAL) vdst[g] = s_vout[i];
+        }
+        __syncthreads();
+        tile = s_misc[0];
+    }
+}
+
+}  // namespace rs

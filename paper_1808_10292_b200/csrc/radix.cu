@@ -7,6 +7,7 @@
 #include <cstring>
 
 #include "onesweep.cuh"
+#include "onesweep_ec.cuh"
 #include "radix16.cuh"
 #include "runtime.h"
 
@@ -20,6 +21,26 @@ namespace rs {
 #define RS_U32_MINB 2
 #endif
 #define RS_TUNE_U32 RS_U32_T, RS_U32_KPT, RS_U32_MINB
+// early-counts design: (ranking threads, keys per thread, min CTAs per SM)
+#ifndef RS_EC_U32_T
+#define RS_EC_U32_T 256
+#define RS_EC_U32_KPT 24
+#define RS_EC_U32_MINB 3
+#endif
+#define RS_EC_U32 RS_EC_U32_T, RS_EC_U32_KPT, RS_EC_U32_MINB
+#ifndef RS_EC_U64_T
+#define RS_EC_U64_T 256
+#define RS_EC_U64_KPT 12
+#define RS_EC_U64_MINB 3
+#endif
+#define RS_EC_U64 RS_EC_U64_T, RS_EC_U64_KPT, RS_EC_U64_MINB
+#ifndef RS_EC_PAIRS_T
+#define RS_EC_PAIRS_T 256
+#define RS_EC_PAIRS_KPT 12
+#define RS_EC_PAIRS_MINB 2
+#endif
+#define RS_EC_PAIRS RS_EC_PAIRS_T, RS_EC_PAIRS_KPT, RS_EC_PAIRS_MINB
+#define RS_EC_U32V 256, 12, 3
 #define RS_TUNE_U64 512, 8, 2
 #define RS_TUNE_PAIRS 512, 8, 2
 #define RS_TUNE_U32V 512, 8, 2
@@ -41,7 +62,19 @@ struct Tune<uint32_t, true> : TuneT<RS_TUNE_U32V> {};
 constexpr int kHistThreads = 512;
 
 template <typename K, bool V>
-static constexpr int tile_keys() {
+struct TuneEc;
+template <>
+struct TuneEc<uint32_t, false> : TuneT<RS_EC_U32> {};
+template <>
+struct TuneEc<uint64_t, false> : TuneT<RS_EC_U64> {};
+template <>
+struct TuneEc<uint64_t, true> : TuneT<RS_EC_PAIRS> {};
+template <>
+struct TuneEc<uint32_t, true> : TuneT<RS_EC_U32V> {};
+
+template <typename K, bool V>
+static int tile_keys() {
+    if (options().pass_design >= 1) return TuneEc<K, V>::THREADS * TuneEc<K, V>::KPT;
     return Tune<K, V>::THREADS * Tune<K, V>::KPT;
 }
 
@@ -102,8 +135,34 @@ static rs_status_t launch_pass_v(const PassArgs& a, size_t T, cudaStream_t st) {
     return RS_OK;
 }
 
+template <typename K, bool V, typename S, bool LBW>
+static rs_status_t launch_pass_ec(const PassArgs& a, size_t T, cudaStream_t st) {
+    using TN = TuneEc<K, V>;
+    using C = OnesweepEcCfg<K, V, TN::THREADS, TN::KPT, LBW>;
+    auto kern = k_onesweep_ec<K, V, TN::THREADS, TN::KPT, TN::MINB, S, LBW>;
+    static int grid_cap = 0;
+    if (!grid_cap) {
+        RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
+        int per_sm = 0;
+        RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::smem_bytes));
+        grid_cap = std::max(1, per_sm) * sm_count();
+    }
+    const unsigned grid = (unsigned)std::min<size_t>(T, (size_t)grid_cap);  // persistent CTAs
+    LaunchScope ls("onesweep", st);
+    kern<<<grid, C::THREADS, C::smem_bytes, st>>>(a);
+    return RS_OK;
+}
+
 template <typename K, bool V>
 static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStream_t st) {
+    if (options().pass_design == 1) {
+        if (wide) return launch_pass_ec<K, V, uint64_t, true>(a, T, st);
+        return launch_pass_ec<K, V, uint32_t, true>(a, T, st);
+    }
+    if (options().pass_design == 2) {
+        if (wide) return launch_pass_ec<K, V, uint64_t, false>(a, T, st);
+        return launch_pass_ec<K, V, uint32_t, false>(a, T, st);
+    }
     const int rv = options().rank_variant;
     if (wide) {
         if (rv == 1) return launch_pass_v<K, V, 1, uint64_t>(a, T, st);
@@ -160,6 +219,7 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
     a.P = P;
     a.ctrl = L.ctrl;
     a.bases = L.bases;
+    a.debug_skip = options().debug_skip;
     for (int t = 0; t < P; ++t) {
         a.pass = t;
         a.shift = 8 * t;

@@ -172,6 +172,7 @@ struct PassArgs {
     const uint32_t* bases;  // [P][256]
     void* status_cur;       // [T][256] status words, zero on entry
     void* status_next;      // [T][256], cleared here for the next pass
+    uint32_t debug_skip;    // timing ablations only (rs_set_option "debug_skip"); 0 in normal use
 };
 
 // ------------------------------------------------------------------ K4 ----

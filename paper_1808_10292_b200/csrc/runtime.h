@@ -38,7 +38,10 @@ int sm_count();
 // process-wide tuning / test knobs (rs_set_option)
 struct Options {
     bool wide_status = false;     // force 64-bit look-back status words (tests)
-    int rank_variant = 0;         // 0 ballot peers, 1 match.any, 2 atomic-OR peers
+    unsigned debug_skip = 0;      // timing ablations (invalid output): 1 look-back, 2 rank, 4 store, 8 reorder
+    int rank_variant = 0;
+    int pass_design = 2;          // 0 classic single sweep; early counts + prefetch with
+                                  // 1 a look-back warp, 2 look-back after ranking         // 0 ballot peers, 1 match.any, 2 atomic-OR peers
 };
 Options& options();
 

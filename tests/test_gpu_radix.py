@@ -13,8 +13,8 @@ from tests.gpu_util import dev, free_dev_gb, free_host_gb, host
 
 pytestmark = pytest.mark.gpu
 
-TILE32 = 512 * 12   # u32 keys-only tile (radix.cu Tune)
-TILE64 = 512 * 8    # u64 keys / pairs tile
+TILE32 = 256 * 24   # u32 keys-only tile (radix.cu TuneEc; classic Tune is 512 * 12, same size)
+TILE64 = 256 * 12   # u64 keys / pairs tile (TuneEc)
 
 
 def _sort_u32(a, b, inplace=True):
@@ -250,6 +250,30 @@ def test_rank_variants(option, variant):
     a = inputs.gen_u32(5 * TILE32 + 3, 33)
     assert (_sort_u32(a, 8) == oracle.sr(a, 8)).all()
     k = inputs.gen_u64(3 * TILE64 + 5, 34, "mod1024")
+    v = inputs.iota_u32(k.size)
+    tk, tv = dev(k), dev(v)
+    rs.sort_pairs(tk, tv)
+    wk, wv = oracle.sr(k, 8, vals=v)
+    assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
+
+
+@pytest.mark.parametrize("design", [0, 1, 2])
+@pytest.mark.parametrize("wide", [0, 1])
+def test_pass_designs(option, design, wide):
+    """Every radix-256 pass kernel design (classic; early counts with a
+    look-back warp; early counts with look-back after ranking) is bit-exact
+    after every pass, for u32 keys and (u64, u32) pairs, narrow and wide status."""
+    option("pass_design", design)
+    option("wide_status", wide)
+    n = 9 * TILE32 + 4321
+    a = inputs.gen_u32(n, 41)
+    for t in range(1, 5):
+        got = host(rs.sort_bits(dev(a), end_bit=8 * t, digit_bits=8), np.uint32)
+        assert (got == oracle.sr(a, 8, rounds=t)).all(), t
+    for dist in ("mod16", "sorted"):
+        b = inputs.gen_u32(n, 42, dist)
+        assert (_sort_u32(b, 8) == oracle.sr(b, 8)).all(), dist
+    k = inputs.gen_u64(5 * TILE64 + 77, 43, "mod1024")
     v = inputs.iota_u32(k.size)
     tk, tv = dev(k), dev(v)
     rs.sort_pairs(tk, tv)
