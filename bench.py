@@ -1,0 +1,364 @@
+"""Benchmark of the B200 radix sort / GSD sample sort (arXiv 1808.10292 hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+Workload (default, BASELINE.json configs[3]): n = 2^31 uint32 keys, uniform over
+[0, 2^32) from seed 4 (SplitMix64 counter stream, inputs/), radix-256.  N = 1:
+single-GPU LSD radix sort of all 2^31 keys; N > 1 (torchrun, one rank per GPU):
+rank k holds keys [k·n/N, (k+1)·n/N) and the ranks run GSD with oversampling
+r = 8 (s = 8N samples per rank) over NCCL.  A step = one full sort of the
+workload (K1 histogram, K2 plan, 4 radix passes [, GSD sample / splitters /
+split / all-to-all / merge]).  Inputs are larger than L2, so no flush is needed.
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the serial C oracle
+(oracle/, the paper's SR4) on the host instead, on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+CONFIGS = {
+    # name: (kind, n_total, seed, dist, digit_bits, description)
+    "c4": ("u32", 1 << 31, 4, "uniform", 8, "BASELINE configs[3]: 2^31 u32 uniform seed 4, radix-256, GSD r=8 over N GPUs"),
+    "c3": ("u32", 1 << 27, 3, "uniform", 8, "BASELINE configs[2] (uniform): 2^27 u32 seed 3, radix-256"),
+    "c2": ("u32", 1 << 24, 2, "half", 8, "BASELINE configs[1]: 2^24 u32 in [0,2^31) seed 2, radix-256"),
+    "c2b16": ("u32", 1 << 24, 2, "half", 16, "BASELINE configs[1]: 2^24 u32 in [0,2^31) seed 2, radix-65536"),
+    "c5": ("pairs", 1 << 30, 5, "uniform", 8, "BASELINE configs[4]: 2^30 (u64 key, u32 index) pairs seed 5, radix-256"),
+}
+BYTES_PER_KEY_PASS = {"u32": 8, "pairs": 24}      # algorithmic bytes of one pass (read + write)
+KEY_BYTES = {"u32": 4, "pairs": 8}
+PASSES = {("u32", 8): 4, ("u32", 16): 2, ("pairs", 8): 8}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """SM clock and clock-event (throttle) reasons sampled every 5 ms during the
+    timed region through NVML (the data nvidia-smi's clocks query reports)."""
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, device_index: int):
+        self.idx = device_index
+        self.samples = []
+        self.smax = None
+        self._stop = None
+
+    def __enter__(self):
+        import threading
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            return self
+        self._stop = threading.Event()
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                                         pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                except Exception:
+                    pass
+                self._stop.wait(0.005)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self._stop is not None:
+            self._stop.set()
+            self._t.join(timeout=2)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.smax, "reasons": [], "samples": 0, "source": "nvml"}
+        sm = [s for s, _ in self.samples]
+        reasons = sorted(n for n, bit in self.REASONS.items() if any(r & bit for _, r in self.samples))
+        loaded = [x for x in sm if x > 0.5 * (self.smax or max(sm))] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": self.smax, "sm_min_mhz": min(sm),
+                "reasons": reasons, "samples": len(sm), "source": "nvml, 5 ms"}
+
+
+def host_info():
+    info = {"cores": os.cpu_count()}
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                info["cpu"] = ln.split(":", 1)[1].strip()
+                break
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal"):
+                info["mem_gb"] = round(int(ln.split()[1]) / 2 ** 20, 1)
+    except Exception:
+        pass
+    return info
+
+
+def oracle_baseline(kind, seed, dist, b, target_s=10.0):
+    """The serial C oracle (SR-b) as it stands, on a bounded
+    sample of the workload's stream, one host core, until >= target_s elapsed."""
+    import inputs
+    import oracle
+    n = 1 << 25
+    if kind == "u32":
+        a = inputs.gen_u32(n, seed, dist)
+        vals = None
+    else:
+        a = inputs.gen_u64(n, seed, dist)
+        vals = inputs.iota_u32(n)
+    done, t_total = 0, 0.0
+    while t_total < target_s:
+        t0 = time.perf_counter()
+        if vals is None:
+            oracle.sr(a, b)
+        else:
+            oracle.sr(a, b, vals=vals)
+        t_total += time.perf_counter() - t0
+        done += n
+    return {"value": done / t_total / 1e9, "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
+            "sample": f"first 2^25 keys of the workload stream (seed {seed}, {dist}), serial SR-{b} oracle "
+                      f"(oracle/sr.c, gcc -O2), {done // n} repetition(s), {t_total:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle on the host (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    kind, n_total, seed, dist, b, desc = CONFIGS[args.config]
+    import inputs
+    import oracle
+    n = 1 << 25 if kind == "u32" else 1 << 24
+    a = inputs.gen_u32(n, seed, dist) if kind == "u32" else inputs.gen_u64(n, seed, dist)
+    vals = inputs.iota_u32(n) if kind == "pairs" else None
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.sr(a, b) if vals is None else oracle.sr(a, b, vals=vals)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    t = sum(times) / len(times)
+    v = n / t / 1e9
+    sample = f"first 2^{n.bit_length() - 1} keys of the workload stream per step, serial SR-{b} oracle, 1 core"
+    print(json.dumps({
+        "impl": "reference", "metric": "sorted keys/sec", "value": round(v, 6), "unit": "Gkeys/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32" if kind == "u32" else "u64+u32",
+        "data": "synthetic", "config": {"workload": args.config, "description": desc, "sample_keys": n},
+        "cpu_baseline": {"value": round(v, 6), "unit": "Gkeys/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": round(v, 6), "unit": "Gkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "host": host_info()}))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import inputs
+    import paper_1808_10292_b200 as rs
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    kind, n_total, seed, dist_name, b, desc = CONFIGS[args.config]
+    p = world
+    lo, hi = rank * n_total // p, (rank + 1) * n_total // p
+    n = hi - lo
+    L = rs.lib()
+
+    # ---- inputs resident in HBM: pristine copy + working buffer
+    host_keys = torch.empty(n, dtype=torch.int32 if kind == "u32" else torch.int64, pin_memory=True)
+    if kind == "u32":
+        inputs.gen_u32(n, seed, dist_name, start=lo, n_total=n_total, out=host_keys.data_ptr())
+    else:
+        inputs.gen_u64(n, seed, dist_name, start=lo, out=host_keys.data_ptr())
+    pristine = host_keys.to(dev, non_blocking=False)
+    work = torch.empty_like(pristine)
+    vals_pristine = vals_work = None
+    if kind == "pairs":
+        hv = torch.empty(n, dtype=torch.int32, pin_memory=True)
+        inputs.iota_u32(n, start=lo, out=hv.data_ptr())
+        vals_pristine = hv.to(dev)
+        vals_work = torch.empty_like(vals_pristine)
+    comm = rs.Comm() if p > 1 else None
+    if comm is not None:
+        comm.set_oversampling(8)
+        cap = comm.capacity(n)
+        out = torch.empty(cap, dtype=work.dtype, device=dev)
+        vout = torch.empty(cap, dtype=torch.int32, device=dev) if kind == "pairs" else None
+        ws = torch.empty(rs.workspace_bytes(KEY_BYTES[kind], 4 if kind == "pairs" else 0, comm.ws_n(n), b, comm),
+                         dtype=torch.uint8, device=dev)
+    else:
+        out = work
+        vout = vals_work
+        ws = torch.empty(rs.workspace_bytes(KEY_BYTES[kind], 4 if kind == "pairs" else 0, n, b),
+                         dtype=torch.uint8, device=dev)
+
+    out_cap = out.numel()
+
+    def one_sort():
+        if kind == "u32":
+            return rs.sort(work, digit_bits=b, comm=comm, out=out, ws=ws, out_cap=out_cap)
+        return rs.sort_pairs(work, vals_work, digit_bits=b, comm=comm, out_keys=out, out_vals=vout, ws=ws,
+                             out_cap=out_cap)
+
+    def barrier():
+        if p > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def reset():
+        work.copy_(pristine)
+        if vals_work is not None:
+            vals_work.copy_(vals_pristine)
+
+    # ---- warm-up (includes a full GSD exchange when p > 1: NCCL connects lazily)
+    for _ in range(args.warmup):
+        reset()
+        barrier()
+        one_sort()
+    barrier()
+
+    # ---- timed steps: inputs reset outside the timed region, each step bracketed
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ms = []
+    L.rs_timing_reset()
+    L.rs_timing_enable(1)
+    launches = 0
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        for _ in range(args.steps):
+            reset()
+            barrier()
+            c0 = L.rs_launch_count()
+            e0.record()
+            one_sort()
+            e1.record()
+            barrier()
+            launches += L.rs_launch_count() - c0
+            step_ms.append(e0.elapsed_time(e1))
+    L.rs_timing_enable(0)
+    clocks = clk.summary()
+    ms_q, cnt_q = ctypes.c_double(), ctypes.c_int()
+    L.rs_timing_query(b"onesweep", ctypes.byref(ms_q), ctypes.byref(cnt_q))
+    pass_ms = ms_q.value / max(cnt_q.value, 1)
+    L.rs_timing_query(b"", ctypes.byref(ms_q), ctypes.byref(cnt_q))
+    all_kernels_ms = ms_q.value
+    total_ms = sum(step_ms)
+    if p > 1:
+        t = torch.tensor([total_ms, pass_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, pass_ms = float(t[0]), float(t[1])
+    ms_per_step = total_ms / args.steps
+    value = n_total / (ms_per_step / 1e3) / 1e9
+
+    # ---- e2e through the public API: pinned host keys -> device -> sort -> host
+    e2e = None
+    if args.e2e_steps > 0:
+        res_host = torch.empty_like(host_keys, pin_memory=True)
+        e2e_ms = []
+        for i in range(args.e2e_steps + 1):
+            barrier()
+            t0 = time.perf_counter()
+            work.copy_(host_keys, non_blocking=True)
+            if vals_work is not None:
+                vals_work.copy_(hv, non_blocking=True)
+            res = one_sort()
+            res_keys = res if kind == "u32" else res[0]
+            res_host[: res_keys.numel()].copy_(res_keys, non_blocking=True)
+            barrier()
+            if i > 0:
+                e2e_ms.append((time.perf_counter() - t0) * 1e3)
+        e_ms = sum(e2e_ms) / len(e2e_ms)
+        if p > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t[0])
+        kb = KEY_BYTES[kind]
+        e2e = {"value": round(n_total / (e_ms / 1e3) / 1e9, 4), "unit": "Gkeys/s",
+               "h2d_bytes_per_step": n * (kb + (4 if kind == "pairs" else 0)), "d2h_bytes_per_step": n * kb,
+               "ms_per_step": round(e_ms, 3), "steps": args.e2e_steps,
+               "note": "host clock around pinned H2D copy + sort + D2H of the sorted keys (per rank; max over ranks)"}
+
+    if rank != 0:
+        if p > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = peaks()
+    bpk = BYTES_PER_KEY_PASS[kind]
+    n_local = n
+    achieved = bpk * n_local / (pass_ms / 1e3) / 1e9 if kind in BYTES_PER_KEY_PASS and b == 8 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(f"{args.config}:p{p}")
+    roofline = {"kernel": "k_onesweep_ec (one radix-256 count-sort pass)", "bound": "hbm",
+                "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
+                "algorithmic_bytes_per_launch": bpk * n_local, "launch_ms": round(pass_ms, 4),
+                "peak_source": peak_src,
+                "pass_share_of_step": round(pass_ms * PASSES.get((kind, b), 4) / ms_per_step, 4)}
+    cpu = None
+    if not args.no_cpu_baseline:
+        cpu = oracle_baseline(kind, seed, dist_name, b)
+        cpu["host"] = host_info()
+    line = {
+        "metric": "sorted keys/sec", "value": round(value, 4), "unit": "Gkeys/s", "n_gpus": p,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u32" if kind == "u32" else "u64+u32", "data": "synthetic",
+        "config": {"workload": args.config, "description": desc, "n": n_total, "keys_per_gpu": n,
+                   "digit_bits": b, "seed": seed, "dist": dist_name,
+                   "parallelism": f"gsd-p{p} (r=8)" if p > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (no flush)", "inputs": "resident in HBM, reset outside timed region"},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clocks, "kernel_ms_per_step": round(all_kernels_ms / args.steps, 4),
+    }
+    print(json.dumps(line))
+    if p > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
