@@ -135,6 +135,19 @@ int rs_comm_size(void* comm);
  * return).  The call blocks the host once, on the p×p count exchange; *n_out is
  * valid on return.  out_cap < |Y_j| → RS_ECAPACITY (on that rank). */
 
+/* rs_gsd_exchange_plan: the host-side plan of GSD's all-to-all (PAPER.md:797-803,
+ * "Processor k sends to processor j sequence X_{k,j}") from the all-gathered
+ * count matrix counts[k*p + j] = |X_{k,j}| (host, p×p).  For `rank`:
+ *   send_off[0..p]: X_{rank,j} = sorted block [send_off[j], send_off[j+1])
+ *   recv_off[0..p]: X_{k,rank} lands at [recv_off[k], recv_off[k+1]) of the
+ *                   receive buffer, runs in source-rank order (reading R16)
+ *   *total = |Y_rank|.
+ * caps (host, p entries, may be NULL): every rank's output capacity; any
+ * |Y_j| > caps[j] returns RS_ECAPACITY, identically on every rank.
+ * Pure host function (no device access); used by the GSD call itself. */
+rs_status_t rs_gsd_exchange_plan(int p, int rank, const uint64_t* counts, const uint64_t* caps,
+                                 uint64_t* send_off, uint64_t* recv_off, uint64_t* total);
+
 /* ---------------------------------------------------------- GSD emulation -- */
 /* rs_gsd_emulate: GSD over p ranks whose blocks all live on THIS GPU, run rank
  * by rank in one stream (no NCCL, nothing waits on another rank): the same

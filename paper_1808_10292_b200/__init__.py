@@ -147,6 +147,35 @@ def digit_histogram(keys: torch.Tensor, digit_bits: int = 8, stream=None) -> tor
     return hist.view(P, 1 << digit_bits)
 
 
+def max_over_ranks(n_local: int, group=None) -> int:
+    """Largest local n over the process group (sizes the GSD workspace and
+    receive capacity; every rank must agree on them)."""
+    import torch.distributed as dist
+    t = torch.tensor([n_local], dtype=torch.int64)
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return int(t.item())
+
+
+def exchange_plan(counts, rank: int, caps=None):
+    """rs_gsd_exchange_plan on a (p, p) count matrix: (send_off, recv_off, total)."""
+    import numpy as np
+    c = np.ascontiguousarray(counts, dtype=np.uint64)
+    p = c.shape[0]
+    so = np.zeros(p + 1, dtype=np.uint64)
+    ro = np.zeros(p + 1, dtype=np.uint64)
+    tot = np.zeros(1, dtype=np.uint64)
+    cp = None
+    if caps is not None:
+        caps = np.ascontiguousarray(caps, dtype=np.uint64)
+        cp = caps.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+    u = ctypes.POINTER(ctypes.c_uint64)
+    check(lib().rs_gsd_exchange_plan(p, rank, c.ctypes.data_as(u), cp, so.ctypes.data_as(u), ro.ctypes.data_as(u),
+                                     tot.ctypes.data_as(u)), "rs_gsd_exchange_plan")
+    return so, ro, int(tot[0])
+
+
 class Comm:
     """GSD communicator: an NCCL comm owned by librsort, bootstrapped over a
     torch.distributed process group (only the 128-byte unique id travels)."""
@@ -178,12 +207,7 @@ class Comm:
         return lib().rs_output_capacity(self.ws_n(n_local), self.handle)
 
     def ws_n(self, n_local: int) -> int:
-        import torch.distributed as dist
-        t = torch.tensor([n_local], dtype=torch.int64)
-        if dist.get_backend(self._group) == "nccl":
-            t = t.cuda()
-        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self._group)
-        return int(t.item())
+        return max_over_ranks(n_local, self._group)
 
     def close(self):
         if self.handle:

@@ -35,6 +35,7 @@ SIGNATURES = {
     "rs_comm_set_oversampling": (_i32, [_vp, _i32]),
     "rs_comm_rank": (_i32, [_vp]),
     "rs_comm_size": (_i32, [_vp]),
+    "rs_gsd_exchange_plan": (_i32, [_i32, _i32, _u64p, _u64p, _u64p, _u64p, _u64p]),
     "rs_gsd_emulate_ws_bytes": (_sz, [_i32, _i32, _i32, _i32, _i32, _sz, _sz]),
     "rs_gsd_emulate": (_i32, [_i32, _i32, _i32, _i32, _vpp, _vpp, _szp, _vpp, _vpp, _sz, _szp, _u64p, _u64p,
                               _vp, _sz, _vp]),

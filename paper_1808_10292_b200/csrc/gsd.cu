@@ -257,17 +257,10 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
     RS_CUDA_TRY(cudaMemcpyAsync(h, L.counts_all, (size_t)p * p * 8, cudaMemcpyDeviceToHost, st));
     RS_CUDA_TRY(cudaStreamSynchronize(st));
     std::vector<uint64_t> cnt(h, h + (size_t)p * p);
-    for (int j = 0; j < p; ++j) {
-        uint64_t tot = 0;
-        for (int k = 0; k < p; ++k) tot += cnt[(size_t)k * p + j];
-        if (tot > caps[j])
-            return fail(RS_ECAPACITY, "rank " + std::to_string(j) + " receives " + std::to_string(tot) +
-                                          " keys > out_cap " + std::to_string(caps[j]));
-    }
     std::vector<uint64_t> soff(p + 1, 0), roff(p + 1, 0);
-    for (int j = 0; j < p; ++j) soff[j + 1] = soff[j] + cnt[(size_t)rank * p + j];
-    for (int k = 0; k < p; ++k) roff[k + 1] = roff[k] + cnt[(size_t)k * p + rank];
-    const size_t total = roff[p];
+    uint64_t total = 0;
+    if ((sst = rs_gsd_exchange_plan(p, rank, cnt.data(), caps.data(), soff.data(), roff.data(), &total)) != RS_OK)
+        return sst;
     // exchange X_{k,j}: grouped send/recv; the self slice is a device copy
     char* kx = static_cast<char*>(keys);
     char* rk = static_cast<char*>(L.recv_keys);
@@ -308,6 +301,26 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
 using namespace rs;
 
 extern "C" {
+
+rs_status_t rs_gsd_exchange_plan(int p, int rank, const uint64_t* counts, const uint64_t* caps,
+                                 uint64_t* send_off, uint64_t* recv_off, uint64_t* total) {
+    if (p < 1 || rank < 0 || rank >= p || !counts || !send_off || !recv_off)
+        return fail(RS_EINVAL, "rs_gsd_exchange_plan: bad arguments");
+    // every rank checks every rank's capacity, so all ranks fail together
+    if (caps)
+        for (int j = 0; j < p; ++j) {
+            uint64_t tot = 0;
+            for (int k = 0; k < p; ++k) tot += counts[(size_t)k * p + j];
+            if (tot > caps[j])
+                return fail(RS_ECAPACITY, "rank " + std::to_string(j) + " receives " + std::to_string(tot) +
+                                              " keys > out_cap " + std::to_string(caps[j]));
+        }
+    send_off[0] = recv_off[0] = 0;
+    for (int j = 0; j < p; ++j) send_off[j + 1] = send_off[j] + counts[(size_t)rank * p + j];
+    for (int k = 0; k < p; ++k) recv_off[k + 1] = recv_off[k] + counts[(size_t)k * p + rank];
+    if (total) *total = recv_off[p];
+    return RS_OK;
+}
 
 rs_status_t rs_get_unique_id(void* uid128) {
     if (!uid128) return fail(RS_EINVAL, "NULL uid");
@@ -424,11 +437,15 @@ rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits, void* co
         cut[(size_t)k * (p + 1)] = 0;
         for (int j = 0; j < p; ++j) cut[(size_t)k * (p + 1) + j + 1] = cut[(size_t)k * (p + 1) + j] + cnt[(size_t)k * p + j];
     }
-    for (int j = 0; j < p; ++j) {
-        uint64_t tot = 0;
-        for (int k = 0; k < p; ++k) tot += cnt[(size_t)k * p + j];
-        n_out[j] = tot;
-        if (tot > out_cap) return fail(RS_ECAPACITY, "rank " + std::to_string(j) + " exceeds out_cap");
+    {
+        const std::vector<uint64_t> caps(p, out_cap);
+        std::vector<uint64_t> so(p + 1), ro(p + 1);
+        for (int j = 0; j < p; ++j) {
+            uint64_t tot = 0;
+            if ((sst = rs_gsd_exchange_plan(p, j, cnt.data(), caps.data(), so.data(), ro.data(), &tot)) != RS_OK)
+                return sst;
+            n_out[j] = tot;
+        }
     }
     for (int j = 0; j < p; ++j) {  // step 4 exchange + step 5 merge, rank by rank
         char* rk = static_cast<char*>(L.recv_keys);
