@@ -174,13 +174,15 @@ rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits,
  *   "wide_status"    1 = use 64-bit look-back status words at any n (they are
  *                    used automatically when n >= 2^30, where 30-bit counts
  *                    could overflow); lets the tests run that path on small n.
- *   "rank_variant"   in-tile ranking: 0 = ballot peer masks (default), 2 = peer
- *                    masks by shared-memory atomic OR,
- *                    1 = match.any.
+ *   "rank_variant"   in-tile ranking: 3 = pairs of keys, one by 8 ballots and one
+ *                    by a shared-memory atomic-OR peer mask (default); 0 = ballots;
+ *                    2 = atomic-OR masks; 1 = match.any (classic design only).
  *   "pass_design"    radix-256 pass kernel: 2 = early counts + tile prefetch,
  *                    look-back after ranking (default); 1 = early counts + tile
  *                    prefetch with a dedicated look-back warp; 0 = classic single
  *                    sweep (rank, look-back, reorder, store).
+ *   "match_every"    0, 4, 6 or 8: in the default pass (u32 keys) every k-th key is
+ *                    ranked with match.any (ADU pipe) instead of ballots (ALU pipe).
  *   "debug_skip"     timing ablations, OUTPUT INVALID: bit 0 no look-back,
  *                    bit 1 no ranking, bit 2 no global store, bit 3 no reorder.
  * Returns RS_EINVAL for an unknown name or a negative value. */

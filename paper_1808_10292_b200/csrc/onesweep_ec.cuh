@@ -31,7 +31,8 @@ struct OnesweepEcCfg {
     static constexpr size_t vin_off = out_off + (size_t)TILE * sizeof(K);
     static constexpr size_t vout_off = vin_off + (HAS_VAL ? (size_t)TILE * 4 : 0);
     static constexpr size_t wc_off = vout_off + (HAS_VAL ? (size_t)TILE * 4 : 0);
-    static constexpr size_t texcl_off = wc_off + (size_t)W * R * 4;
+    static constexpr size_t wm_off = wc_off + (size_t)W * R * 4;        // peer masks (RANKV 1)
+    static constexpr size_t texcl_off = wm_off + (size_t)W * R * 4;
     static constexpr size_t tcnt_off = texcl_off + R * 4;
     static constexpr size_t gofs_off = tcnt_off + R * 4;
     static constexpr size_t misc_off = gofs_off + R * 4;
@@ -83,7 +84,12 @@ __device__ __forceinline__ uint32_t peers8(uint32_t d) {
 
 // LBW: a dedicated look-back warp runs the look-back concurrently with the
 // ranking; otherwise the ranking threads run it (one digit each) after ranking.
-template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, bool LBW>
+// ME > 0: every ME-th key (ME even) is ranked with match.any instead of ballots.
+// RANKV 1: peer masks by shared-memory atomic OR of lane bits (order-independent,
+// so stable by construction) instead of ballots.
+// DBG: compile in the timing-ablation switches (a.debug_skip); off in normal builds.
+template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, bool LBW, int ME = 0, int RANKV = 0,
+          bool DBG = false>
 __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassArgs a) {
     using ST = Status<S>;
     using C = OnesweepEcCfg<K, HAS_VAL, RT, KPT, LBW>;
@@ -95,6 +101,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
     uint32_t* s_vin = reinterpret_cast<uint32_t*>(smem + C::vin_off);
     uint32_t* s_vout = reinterpret_cast<uint32_t*>(smem + C::vout_off);
     uint32_t* s_wc = reinterpret_cast<uint32_t*>(smem + C::wc_off);
+    uint32_t* s_wm = reinterpret_cast<uint32_t*>(smem + C::wm_off);
     uint32_t* s_texcl = reinterpret_cast<uint32_t*>(smem + C::texcl_off);
     uint32_t* s_tcnt = reinterpret_cast<uint32_t*>(smem + C::tcnt_off);
     uint32_t* s_gofs = reinterpret_cast<uint32_t*>(smem + C::gofs_off);
@@ -144,6 +151,8 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
         if (t0 < a.num_tiles) issue_load(t0);
     }
     for (int i = tid; i < W * R; i += THREADS) s_wc[i] = 0;
+    if (RANKV != 0)
+        for (int i = tid; i < W * R; i += THREADS) s_wm[i] = 0;  // kept zero by the group leaders
     __syncthreads();
     uint32_t tile = s_misc[0];
     uint32_t phase = 0;
@@ -168,7 +177,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
         __syncthreads();
 
         // ---- [count] per-warp digit histograms
-        if (warp < W) {
+        if (warp < W && !(DBG && (a.debug_skip & 8))) {  // (bit 3: ablation, no counting)
             uint32_t* wc = s_wc + warp * R;
             const K* in = s_in + warp * WK + lane;
 #pragma unroll 8
@@ -255,15 +264,13 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
                 }
             }
         } else {
-            // ---- [rank] stable warp rank, straight to the sorted slot
+            // ---- [rank] stable warp rank, straight to the sorted slot.  Keys are
+            // taken in pairs: both peer masks are computed before either counter
+            // update so their independent ALU chains interleave; every ME-th key
+            // uses match.any instead (ADU pipe) to offload the ALU pipe.
             uint32_t* wc = s_wc + warp * R;
             const int ibase = warp * WK + lane;
-#pragma unroll 4
-            for (int j = 0; j < KPT; ++j) {
-                const int idx = ibase + j * 32;
-                const K k = s_in[idx];
-                const uint32_t d = digit8<K>(k, shift);
-                const uint32_t peers = peers8(d);
+            auto place = [&](const K k, const uint32_t d, const uint32_t peers, const int idx) {
                 const uint32_t cnt = wc[d];
                 const uint32_t pos = cnt + __popc(peers & lt);
                 s_out[pos] = k;
@@ -271,12 +278,73 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
                 __syncwarp();
                 if ((peers & gt) == 0) wc[d] = cnt + __popc(peers);
                 __syncwarp();
+            };
+            static_assert(KPT % 2 == 0, "keys are ranked in pairs");
+            if (DBG && (a.debug_skip & 2)) {  // ablation: no ranking, identity placement
+                for (int j = 0; j < KPT; ++j) s_out[ibase + j * 32] = s_in[ibase + j * 32];
+            } else if (RANKV == 1) {
+                uint32_t* wm = s_wm + warp * R;
+#pragma unroll 4
+                for (int j = 0; j < KPT; ++j) {
+                    const int idx = ibase + j * 32;
+                    const K k = s_in[idx];
+                    const uint32_t d = digit8<K>(k, shift);
+                    atomicOr(&wm[d], 1u << lane);
+                    __syncwarp();
+                    const uint32_t peers = wm[d];
+                    const uint32_t cnt = wc[d];
+                    const uint32_t pos = cnt + __popc(peers & lt);
+                    s_out[pos] = k;
+                    if (HAS_VAL) s_vout[pos] = s_vin[idx];
+                    __syncwarp();
+                    if ((peers & gt) == 0) {
+                        wc[d] = cnt + __popc(peers);
+                        wm[d] = 0;
+                    }
+                    __syncwarp();
+                }
+            } else if (RANKV == 2) {
+                // hybrid pairs: key j by ballots (ALU pipe), key j+1 by an atomic-OR
+                // peer mask (shared-memory pipe) whose latency hides behind the ballots
+                uint32_t* wm = s_wm + warp * R;
+#pragma unroll 2
+                for (int j = 0; j < KPT; j += 2) {
+                    const int i0 = ibase + j * 32, i1 = i0 + 32;
+                    const K k0 = s_in[i0], k1 = s_in[i1];
+                    const uint32_t d0 = digit8<K>(k0, shift), d1 = digit8<K>(k1, shift);
+                    atomicOr(&wm[d1], 1u << lane);
+                    const uint32_t p0 = peers8(d0);
+                    place(k0, d0, p0, i0);  // ends with __syncwarp: the ORs are complete
+                    const uint32_t p1 = wm[d1];
+                    const uint32_t cnt = wc[d1];
+                    const uint32_t pos = cnt + __popc(p1 & lt);
+                    s_out[pos] = k1;
+                    if (HAS_VAL) s_vout[pos] = s_vin[i1];
+                    __syncwarp();
+                    if ((p1 & gt) == 0) {
+                        wc[d1] = cnt + __popc(p1);
+                        wm[d1] = 0;
+                    }
+                    __syncwarp();
+                }
+            } else
+#pragma unroll 2
+            for (int j = 0; j < KPT; j += 2) {
+                const int i0 = ibase + j * 32, i1 = i0 + 32;
+                const K k0 = s_in[i0], k1 = s_in[i1];
+                const uint32_t d0 = digit8<K>(k0, shift), d1 = digit8<K>(k1, shift);
+                const uint32_t p0 = (ME > 0 && (j % ME) == 0) ? __match_any_sync(0xffffffffu, d0) : peers8(d0);
+                const uint32_t p1 = peers8(d1);
+                place(k0, d0, p0, i0);
+                place(k1, d1, p1, i1);
             }
         }
         if (!LBW && tid < R) {
             // ---- [look-back] after ranking, one digit per thread, windowed walk
             S excl = 0;
-            if (tile != 0) {
+            if (tile != 0 && DBG && (a.debug_skip & 1)) {
+                st_relaxed_gpu(status + (size_t)tile * R + tid, ST::kFlagP | (S)s_tcnt[tid]);  // ablation
+            } else if (tile != 0) {
                 constexpr int LB = 8;
                 const S* sp = status + (size_t)(tile - 1) * R + tid;
                 int64_t left = (int64_t)tile;
@@ -312,6 +380,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
         // ---- [store] bucket runs leave as coalesced bursts
 #pragma unroll 4
         for (uint32_t i = tid; i < valid; i += THREADS) {
+            if (DBG && (a.debug_skip & 4)) break;  // ablation: no global store
             const K k = s_out[i];
             const uint32_t g = s_gofs[digit8<K>(k, shift)] + i;
             dst[g] = k;

@@ -5,9 +5,11 @@
 // caller's stream; no host synchronisation, no allocation.
 #include <algorithm>
 #include <cstring>
+#include <type_traits>
 
 #include "onesweep.cuh"
 #include "onesweep_ec.cuh"
+#include "onesweep_cr.cuh"
 #include "radix16.cuh"
 #include "runtime.h"
 
@@ -72,8 +74,36 @@ struct TuneEc<uint64_t, true> : TuneT<RS_EC_PAIRS> {};
 template <>
 struct TuneEc<uint32_t, true> : TuneT<RS_EC_U32V> {};
 
+// counter-ranking design (3): (threads, keys per thread, min CTAs per SM)
+#ifndef RS_CR_U32_T
+#define RS_CR_U32_T 256
+#define RS_CR_U32_KPT 24
+#define RS_CR_U32_MINB 3
+#endif
+#ifndef RS_CR_U64_T
+#define RS_CR_U64_T 256
+#define RS_CR_U64_KPT 12
+#define RS_CR_U64_MINB 3
+#endif
+#ifndef RS_CR_PAIRS_T
+#define RS_CR_PAIRS_T 256
+#define RS_CR_PAIRS_KPT 12
+#define RS_CR_PAIRS_MINB 2
+#endif
+template <typename K, bool V>
+struct TuneCr;
+template <>
+struct TuneCr<uint32_t, false> : TuneT<RS_CR_U32_T, RS_CR_U32_KPT, RS_CR_U32_MINB> {};
+template <>
+struct TuneCr<uint64_t, false> : TuneT<RS_CR_U64_T, RS_CR_U64_KPT, RS_CR_U64_MINB> {};
+template <>
+struct TuneCr<uint64_t, true> : TuneT<RS_CR_PAIRS_T, RS_CR_PAIRS_KPT, RS_CR_PAIRS_MINB> {};
+template <>
+struct TuneCr<uint32_t, true> : TuneT<256, 12, 3> {};
+
 template <typename K, bool V>
 static int tile_keys() {
+    if (options().pass_design == 3) return TuneCr<K, V>::THREADS * TuneCr<K, V>::KPT;
     if (options().pass_design >= 1) return TuneEc<K, V>::THREADS * TuneEc<K, V>::KPT;
     return Tune<K, V>::THREADS * Tune<K, V>::KPT;
 }
@@ -135,11 +165,11 @@ static rs_status_t launch_pass_v(const PassArgs& a, size_t T, cudaStream_t st) {
     return RS_OK;
 }
 
-template <typename K, bool V, typename S, bool LBW>
+template <typename K, bool V, typename S, bool LBW, int ME, int RANKV = 0, bool DBG = false>
 static rs_status_t launch_pass_ec(const PassArgs& a, size_t T, cudaStream_t st) {
     using TN = TuneEc<K, V>;
     using C = OnesweepEcCfg<K, V, TN::THREADS, TN::KPT, LBW>;
-    auto kern = k_onesweep_ec<K, V, TN::THREADS, TN::KPT, TN::MINB, S, LBW>;
+    auto kern = k_onesweep_ec<K, V, TN::THREADS, TN::KPT, TN::MINB, S, LBW, ME, RANKV, DBG>;
     static int grid_cap = 0;
     if (!grid_cap) {
         RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
@@ -153,15 +183,54 @@ static rs_status_t launch_pass_ec(const PassArgs& a, size_t T, cudaStream_t st) 
     return RS_OK;
 }
 
+// match-every variants are instantiated for u32 keys only (the tuned case)
+template <typename K, bool V, typename S, bool LBW>
+static rs_status_t launch_pass_ec_me(const PassArgs& a, size_t T, cudaStream_t st) {
+    if (options().debug_skip) return launch_pass_ec<K, V, S, LBW, 0, 0, true>(a, T, st);
+    if (options().rank_variant == 2) return launch_pass_ec<K, V, S, LBW, 0, 1>(a, T, st);
+    if (options().rank_variant == 3) return launch_pass_ec<K, V, S, LBW, 0, 2>(a, T, st);
+    if (std::is_same<K, uint32_t>::value && !V) {
+        switch (options().match_every) {
+            case 4: return launch_pass_ec<K, V, S, LBW, 4>(a, T, st);
+            case 6: return launch_pass_ec<K, V, S, LBW, 6>(a, T, st);
+            case 8: return launch_pass_ec<K, V, S, LBW, 8>(a, T, st);
+            default: break;
+        }
+    }
+    return launch_pass_ec<K, V, S, LBW, 0>(a, T, st);
+}
+
+template <typename K, bool V, typename S>
+static rs_status_t launch_pass_cr(const PassArgs& a, size_t T, cudaStream_t st) {
+    using TN = TuneCr<K, V>;
+    using C = OnesweepCrCfg<K, V, TN::THREADS, TN::KPT>;
+    auto kern = k_onesweep_cr<K, V, TN::THREADS, TN::KPT, TN::MINB, S>;
+    static int grid_cap = 0;
+    if (!grid_cap) {
+        RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
+        int per_sm = 0;
+        RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TN::THREADS, C::smem_bytes));
+        grid_cap = std::max(1, per_sm) * sm_count();
+    }
+    const unsigned grid = (unsigned)std::min<size_t>(T, (size_t)grid_cap);  // persistent CTAs
+    LaunchScope ls("onesweep", st);
+    kern<<<grid, TN::THREADS, C::smem_bytes, st>>>(a);
+    return RS_OK;
+}
+
 template <typename K, bool V>
 static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStream_t st) {
+    if (options().pass_design == 3) {
+        if (wide) return launch_pass_cr<K, V, uint64_t>(a, T, st);
+        return launch_pass_cr<K, V, uint32_t>(a, T, st);
+    }
     if (options().pass_design == 1) {
-        if (wide) return launch_pass_ec<K, V, uint64_t, true>(a, T, st);
-        return launch_pass_ec<K, V, uint32_t, true>(a, T, st);
+        if (wide) return launch_pass_ec<K, V, uint64_t, true, 0>(a, T, st);
+        return launch_pass_ec<K, V, uint32_t, true, 0>(a, T, st);
     }
     if (options().pass_design == 2) {
-        if (wide) return launch_pass_ec<K, V, uint64_t, false>(a, T, st);
-        return launch_pass_ec<K, V, uint32_t, false>(a, T, st);
+        if (wide) return launch_pass_ec_me<K, V, uint64_t, false>(a, T, st);
+        return launch_pass_ec_me<K, V, uint32_t, false>(a, T, st);
     }
     const int rv = options().rank_variant;
     if (wide) {

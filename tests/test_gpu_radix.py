@@ -243,7 +243,7 @@ def test_wide_status_lookback(option, kind):
             assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
 
 
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 3])
 def test_rank_variants(option, variant):
     """match.any (1) and atomic-OR (2) peer masks give the same stable ranks."""
     option("rank_variant", variant)
@@ -257,7 +257,7 @@ def test_rank_variants(option, variant):
     assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
 
 
-@pytest.mark.parametrize("design", [0, 1, 2])
+@pytest.mark.parametrize("design", [0, 1, 2, 3])
 @pytest.mark.parametrize("wide", [0, 1])
 def test_pass_designs(option, design, wide):
     """Every radix-256 pass kernel design (classic; early counts with a
@@ -279,3 +279,13 @@ def test_pass_designs(option, design, wide):
     rs.sort_pairs(tk, tv)
     wk, wv = oracle.sr(k, 8, vals=v)
     assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
+
+
+@pytest.mark.parametrize("me", [4, 6, 8])
+def test_match_every_hybrid_ranking(option, me):
+    """u32 pass with every me-th key ranked by match.any, the rest by ballots."""
+    option("match_every", me)
+    a = inputs.gen_u32(7 * TILE32 + 999, 44)
+    for t in range(1, 5):
+        got = host(rs.sort_bits(dev(a), end_bit=8 * t, digit_bits=8), np.uint32)
+        assert (got == oracle.sr(a, 8, rounds=t)).all(), t
