@@ -49,41 +49,6 @@ __device__ __forceinline__ uint32_t digit8<uint32_t>(uint32_t k, int shift) {
     return __byte_perm(k, 0u, 0x4440u + (uint32_t)(shift >> 3));  // byte shift/8, zero-extended
 }
 
-// peers with the same 8-bit digit in this warp (8 ballots; see onesweep.cuh)
-__device__ __forceinline__ uint32_t peers8(uint32_t d) {
-    // Lanes that disagree with me on bit b are the set bits of ballot(bit b) ^ s_b,
-    // s_b = my bit b as 0 / 0xffffffff; peers = ~OR_b(...).  s_b in one PRMT: a
-    // multiply by 0x10204080 moves nibble bit i to the MSB of byte i, and PRMT's
-    // sign-replicate selector broadcasts that MSB to all four bytes.
-    uint32_t dis;
-    asm("{\n"
-        ".reg .pred p;\n"
-        ".reg .b32 t, s, m, ylo, yhi;\n"
-        "and.b32 t, %1, 15;\n"
-        "mul.lo.u32 ylo, t, 0x10204080;\n"
-        "shr.u32 t, %1, 4;\n"
-        "mul.lo.u32 yhi, t, 0x10204080;\n"
-        "mov.b32 %0, 0;\n"
-#define RS_PEER_BIT(B, Y, SEL)                     \
-    "and.b32 t, %1, " #B ";\n"                    \
-    "setp.ne.u32 p, t, 0;\n"                      \
-    "vote.sync.ballot.b32 m, p, 0xffffffff;\n"    \
-    "prmt.b32 s, " #Y ", 0, " #SEL ";\n"          \
-    "xor.b32 m, m, s;\n"                          \
-    "or.b32 %0, %0, m;\n"
-        RS_PEER_BIT(1, ylo, 0x8888) RS_PEER_BIT(2, ylo, 0x9999)
-        RS_PEER_BIT(4, ylo, 0xAAAA) RS_PEER_BIT(8, ylo, 0xBBBB)
-        RS_PEER_BIT(16, yhi, 0x8888) RS_PEER_BIT(32, yhi, 0x9999)
-        RS_PEER_BIT(64, yhi, 0xAAAA) RS_PEER_BIT(128, yhi, 0xBBBB)
-#undef RS_PEER_BIT
-        "}\n"
-        : "=r"(dis)
-        : "r"(d));
-    return ~dis;
-}
-
-// LBW: a dedicated look-back warp runs the look-back concurrently with the
-// ranking; otherwise the ranking threads run it (one digit each) after ranking.
 // ME > 0: every ME-th key (ME even) is ranked with match.any instead of ballots.
 // RANKV 1: peer masks by shared-memory atomic OR of lane bits (order-independent,
 // so stable by construction) instead of ballots.

@@ -1,5 +1,6 @@
 // Radix-65536 pass kernels and driver (see radix16.cuh for the design).
 #include <algorithm>
+#include <type_traits>
 
 #include "radix16.cuh"
 
@@ -82,19 +83,23 @@ __global__ void __launch_bounds__(1024) k16_scan(const uint32_t* __restrict__ to
 }
 
 // ------------------------------------------------------------------ C4 ----
-__global__ void __launch_bounds__(256) k16_offsets(uint32_t* __restrict__ H, int G, const uint32_t* __restrict__ base) {
+// also flags partitions with a digit count >= 2^16 (they cannot use 16-bit
+// shared-memory running counts in k16_scatter_fast); big[] zeroed beforehand
+__global__ void __launch_bounds__(256) k16_offsets(uint32_t* __restrict__ H, int G, const uint32_t* __restrict__ base,
+                                                   uint32_t* __restrict__ big) {
     const int d = blockIdx.x * 256 + threadIdx.x;
     uint32_t run = base[d];
     for (int g = 0; g < G; ++g) {
         const uint32_t h = H[(size_t)g * kR16 + d];
         H[(size_t)g * kR16 + d] = run;
         run += h;
+        if (h >= 65536u) atomicOr(&big[g], 1u);
     }
 }
 
 // ------------------------------------------------------------------ C5 ----
 // Block-level stable 8-bit reorder of a chunk held in shared memory
-// (A -> B), keys warp-striped, rank by warp match, per-digit scan over warps
+// (A -> B), keys warp-striped, rank by warp ballots, per-digit scan over warps
 // and an exclusive scan over the 256 digits.
 template <typename K, bool V>
 __device__ __forceinline__ void smem_pass8(const K* A, K* B, const uint32_t* VA, uint32_t* VB, int shift,
@@ -111,7 +116,7 @@ __device__ __forceinline__ void smem_pass8(const K* A, K* B, const uint32_t* VA,
     for (int j = 0; j < KPT; ++j) {
         key[j] = A[warp * WK + j * 32 + lane];
         const uint32_t d = static_cast<uint32_t>(key[j] >> shift) & 0xFFu;
-        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t peers = peers8(d);
         const uint32_t c = wc[d];
         rk[j] = c + __popc(peers & lt);
         __syncwarp();
@@ -248,6 +253,123 @@ __global__ void __launch_bounds__(kS16Threads, 1)
     }
 }
 
+// ------------------------------------------------------------ C5 (fast) ---
+// u32 keys without values: the partition's running count per digit lives in
+// shared memory (16-bit; partitions whose count matrix row has an entry
+// >= 65536 — skewed data — take the global read-modify-write path), so the
+// offset matrix is read-only; chunks are loaded by the TMA engine into a third
+// buffer while the current chunk is sorted and written.
+struct Scatter16FastSmem {
+    static constexpr int CH = kS16Chunk;
+    static constexpr size_t cnt16 = 0;                                   // u16[65536]
+    static constexpr size_t buf0 = cnt16 + (size_t)kR16 * 2;             // 3 chunk buffers
+    static constexpr size_t wcnt = buf0 + 3 * (size_t)CH * 4;
+    static constexpr size_t aux = wcnt + (size_t)(kS16Threads / 32) * 256 * 4;
+    static constexpr size_t goff = aux + (32 + 256) * 4;
+    static constexpr size_t segs = goff + (size_t)CH * 4;
+    static constexpr size_t bar = segs + 64 * 4;
+    static constexpr size_t bytes = bar + 16;
+};
+
+__global__ void __launch_bounds__(kS16Threads, 1)
+    k16_scatter_fast(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, size_t n, int shift,
+                     size_t part_keys, uint32_t* __restrict__ O, const uint32_t* __restrict__ big) {
+    using S = Scatter16FastSmem;
+    constexpr int T = kS16Threads, KPT = kS16KPT, CH = S::CH;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint16_t* s_cnt = reinterpret_cast<uint16_t*>(smem + S::cnt16);
+    uint32_t* bufA = reinterpret_cast<uint32_t*>(smem + S::buf0);
+    uint32_t* bufB = bufA + CH;
+    uint32_t* bufC = bufB + CH;
+    uint32_t* s_wcnt = reinterpret_cast<uint32_t*>(smem + S::wcnt);
+    uint32_t* s_aux = reinterpret_cast<uint32_t*>(smem + S::aux);
+    uint32_t* s_goff = reinterpret_cast<uint32_t*>(smem + S::goff);
+    uint32_t* s_seg = reinterpret_cast<uint32_t*>(smem + S::segs);
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + S::bar);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const size_t g = blockIdx.x;
+    const size_t lo = g * part_keys;
+    const size_t hi = min(n, lo + part_keys);
+    uint32_t* Og = O + g * kR16;
+    const bool gpath = big[g] != 0;  // some digit count of this partition needs > 16 bits
+    if (!gpath)
+        for (int i = tid; i < kR16 / 2; i += T) reinterpret_cast<uint32_t*>(s_cnt)[i] = 0;
+    auto issue = [&](size_t c0, uint32_t* buf) {
+        const uint32_t valid = (uint32_t)min((size_t)CH, hi - c0);
+        const uint32_t bytes = (valid * 4u) & ~15u;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(s_bar, bytes);
+        if (bytes) bulk_g2s(buf, src + c0, bytes, s_bar);
+    };
+    if (tid == 0) {
+        mbar_init(s_bar, 1);
+        fence_mbar_init();
+        if (lo < hi) issue(lo, bufA);
+    }
+    __syncthreads();
+    uint32_t phase = 0;
+    for (size_t c0 = lo; c0 < hi; c0 += CH) {
+        const uint32_t valid = (uint32_t)min((size_t)CH, hi - c0);
+        if (valid < (uint32_t)CH)
+            for (uint32_t i = ((valid * 4u) & ~15u) / 4 + tid; i < (uint32_t)CH; i += T)
+                bufA[i] = i < valid ? src[c0 + i] : ~0u;
+        mbar_wait_parity(s_bar, phase);
+        phase ^= 1u;
+        __syncthreads();
+        if (tid == 0 && c0 + CH < hi) issue(c0 + CH, bufC);  // prefetch the next chunk
+        smem_pass8<uint32_t, false>(bufA, bufB, nullptr, nullptr, shift, s_wcnt, s_aux);
+        smem_pass8<uint32_t, false>(bufB, bufA, nullptr, nullptr, shift + 8, s_wcnt, s_aux);
+
+        const int i0 = tid * KPT;
+        uint32_t d[KPT], st[KPT];
+        uint32_t prevd = i0 > 0 ? (bufA[i0 - 1] >> shift) & 0xFFFFu : 0xFFFFFFFFu;
+        uint32_t run = 0;
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            d[j] = (bufA[i0 + j] >> shift) & 0xFFFFu;
+            if (d[j] != prevd) run = (uint32_t)(i0 + j) + 1;
+            st[j] = run;
+            prevd = d[j];
+        }
+        uint32_t x = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x = max(x, y);
+        }
+        if (lane == 31) s_seg[warp] = x;
+        __syncthreads();
+        uint32_t carry = 0;
+        for (int w = 0; w < warp; ++w) carry = max(carry, s_seg[w]);
+        const uint32_t prev_lane = __shfl_up_sync(0xffffffffu, x, 1);
+        if (lane > 0) carry = max(carry, prev_lane);
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            st[j] = (st[j] ? st[j] : carry) - 1;
+            if ((uint32_t)(i0 + j) == st[j] && (uint32_t)(i0 + j) < valid)
+                s_goff[i0 + j] = Og[d[j]] + (gpath ? 0u : (uint32_t)s_cnt[d[j]]);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < KPT; ++j) {
+            const uint32_t i = (uint32_t)(i0 + j);
+            if (i >= valid) continue;
+            const uint32_t o = s_goff[st[j]] + (i - st[j]);
+            dst[o] = bufA[i];
+            const uint32_t dnext = j + 1 < KPT ? d[j + 1] : (i + 1 < valid ? (bufA[i + 1] >> shift) & 0xFFFFu : d[j]);
+            if ((i + 1 == valid) || dnext != d[j]) {
+                if (gpath) Og[d[j]] = o + 1;
+                else s_cnt[d[j]] = (uint16_t)(s_cnt[d[j]] + (i - st[j] + 1));
+            }
+        }
+        __syncthreads();
+        uint32_t* t = bufA;  // the next chunk is in C
+        bufA = bufC;
+        bufC = t;
+    }
+}
+
 // ------------------------------------------------------------ histogram ---
 template <typename K>
 __global__ void k16_hist_all(const K* __restrict__ keys, size_t n, int P, uint32_t* __restrict__ hist) {
@@ -263,6 +385,7 @@ struct Layout16 {
     uint32_t* H;  // [G][65536]
     uint32_t* tot;
     uint32_t* base;
+    uint32_t* big;  // [G]
     void* alt_keys;
     uint32_t* alt_vals;
     size_t G, part, bytes;
@@ -278,6 +401,7 @@ static Layout16 layout16(void* ws, int key_bytes, bool has_val, size_t n) {
     L.H = static_cast<uint32_t*>(c.take(L.G * kR16 * 4));
     L.tot = static_cast<uint32_t*>(c.take(kR16 * 4));
     L.base = static_cast<uint32_t*>(c.take(kR16 * 4));
+    L.big = static_cast<uint32_t*>(c.take(L.G * 4));
     L.alt_keys = c.take(n * key_bytes);
     L.alt_vals = static_cast<uint32_t*>(has_val ? c.take(n * 4) : nullptr);
     L.bytes = c.used();
@@ -296,6 +420,8 @@ static rs_status_t sort16(const K* in, const uint32_t* vin, size_t n, int end_bi
     if (!attr) {
         RS_CUDA_TRY(cudaFuncSetAttribute(k16_count<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, kR16 / 2 * 4));
         RS_CUDA_TRY(cudaFuncSetAttribute(k16_scatter<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes));
+        RS_CUDA_TRY(cudaFuncSetAttribute(k16_scatter_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)Scatter16FastSmem::bytes));
         attr = true;
     }
     K* alt = static_cast<K*>(L.alt_keys);
@@ -323,11 +449,18 @@ static rs_status_t sort16(const K* in, const uint32_t* vin, size_t n, int end_bi
         }
         {
             LaunchScope ls("r16_offsets", st);
-            k16_offsets<<<kR16 / 256, 256, 0, st>>>(L.H, (int)L.G, L.base);
+            RS_CUDA_TRY(cudaMemsetAsync(L.big, 0, L.G * 4, st));
+            k16_offsets<<<kR16 / 256, 256, 0, st>>>(L.H, (int)L.G, L.base, L.big);
         }
         {
             LaunchScope ls("r16_scatter", st);
-            k16_scatter<K, V><<<(unsigned)L.G, kS16Threads, S::bytes, st>>>(src, dst, vsrc, vdst, n, shift, L.part, L.H);
+            if (std::is_same<K, uint32_t>::value && !V)
+                k16_scatter_fast<<<(unsigned)L.G, kS16Threads, Scatter16FastSmem::bytes, st>>>(
+                    reinterpret_cast<const uint32_t*>(src), reinterpret_cast<uint32_t*>(dst), n, shift, L.part, L.H,
+                    L.big);
+            else
+                k16_scatter<K, V><<<(unsigned)L.G, kS16Threads, S::bytes, st>>>(src, dst, vsrc, vdst, n, shift,
+                                                                                 L.part, L.H);
         }
         src = dst;
         vsrc = vdst;
