@@ -183,6 +183,10 @@ rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits,
  *                    sweep (rank, look-back, reorder, store).
  *   "match_every"    0, 4, 6 or 8: in the default pass (u32 keys) every k-th key is
  *                    ranked with match.any (ADU pipe) instead of ballots (ALU pipe).
+ *   "gsd_merge"      GSD step 5: 0 = tree of stable 2-way merge-path merges (default),
+ *                    1 = stable radix re-sort of the received runs (same result).
+ *   "compact"        1 = default pass with 16-bit per-warp counters (smaller
+ *                    shared-memory footprint; ballots only).
  *   "debug_skip"     timing ablations, OUTPUT INVALID: bit 0 no look-back,
  *                    bit 1 no ranking, bit 2 no global store, bit 3 no reorder.
  * Returns RS_EINVAL for an unknown name or a negative value. */

@@ -13,14 +13,16 @@
 //                          C3 grouped ncclSend/ncclRecv of the X_{k,j} slices (the
 //                          sorted block is already grouped by destination: zero-copy)
 //   step 5 Merging         Y_j from the p received runs, ties to the lower source rank
-//                          (R16): a stable radix re-sort of the concatenation, which is
-//                          identical to the p-way merge (R17).
+//                          (R16): a tree of stable 2-way merge-path merges (merge.cu),
+//                          or optionally a stable radix re-sort of the concatenation,
+//                          which gives the identical result (R17).
 #include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "gsd.h"
+#include "merge.h"
 
 namespace rs {
 
@@ -123,6 +125,9 @@ struct GsdLayout {
     Comp* splitters;      // p-1
     uint64_t* counts_local;  // p
     uint64_t* counts_all;    // p*p (or p slots of p for the emulation)
+    void* merge_keys;        // merge-tree scratch: cap keys (+ values)
+    uint32_t* merge_vals;
+    size_t* merge_split;
     size_t bytes;
 };
 
@@ -142,6 +147,9 @@ static GsdLayout gsd_layout(void* ws, int key_bytes, bool has_val, size_t n, siz
     L.splitters = static_cast<Comp*>(c.take((size_t)p * sizeof(Comp)));
     L.counts_local = static_cast<uint64_t*>(c.take((size_t)p * 8));
     L.counts_all = static_cast<uint64_t*>(c.take((size_t)p * p * 8));
+    L.merge_keys = c.take(cap * key_bytes);
+    L.merge_vals = static_cast<uint32_t*>(has_val ? c.take(cap * 4) : nullptr);
+    L.merge_split = static_cast<size_t*>(c.take(merge_scratch_bytes(cap)));
     L.bytes = c.used();
     return L;
 }
@@ -196,11 +204,16 @@ static rs_status_t launch_split(int key_bytes, const void* X, size_t N, int rank
     return RS_OK;
 }
 
-// step 5: Y_j from the concatenated runs (source-rank order) by a stable sort
-static rs_status_t merge_runs(int key_bytes, void* runs, uint32_t* vruns, size_t total, int b, void* out,
-                              uint32_t* vout, const GsdLayout& L, cudaStream_t st) {
+// step 5: Y_j from the p received runs (source-rank order): the merge tree
+// (default) or a stable radix re-sort of the concatenation (option gsd_merge=1);
+// both give the identical result (reading R17)
+static rs_status_t merge_runs(int key_bytes, void* runs, uint32_t* vruns, const std::vector<uint64_t>& roff, int b,
+                              void* out, uint32_t* vout, const GsdLayout& L, cudaStream_t st) {
+    const size_t total = roff.back();
     if (total == 0) return RS_OK;
-    return local_sort(key_bytes, runs, vruns, total, b, key_bytes * 8, out, vout, L.local_ws, L.local_ws_bytes, st);
+    if (options().gsd_merge == 1)
+        return local_sort(key_bytes, runs, vruns, total, b, key_bytes * 8, out, vout, L.local_ws, L.local_ws_bytes, st);
+    return merge_runs_tree(key_bytes, runs, vruns, roff, L.merge_keys, L.merge_vals, out, vout, L.merge_split, st);
 }
 
 #define RS_NCCL_TRY(expr)                                                                     \
@@ -290,7 +303,7 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
         }
     }
     // step 5: merge
-    if ((sst = merge_runs(key_bytes, L.recv_keys, L.recv_vals, total, b, out, vout, L, st)) != RS_OK) return sst;
+    if ((sst = merge_runs(key_bytes, L.recv_keys, L.recv_vals, roff, b, out, vout, L, st)) != RS_OK) return sst;
     if (n_out) *n_out = total;
     RS_CUDA_TRY(cudaGetLastError());
     return RS_OK;
@@ -450,20 +463,23 @@ rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits, void* co
     for (int j = 0; j < p; ++j) {  // step 4 exchange + step 5 merge, rank by rank
         char* rk = static_cast<char*>(L.recv_keys);
         uint64_t off = 0;
+        std::vector<uint64_t> roff(1, 0);
         {
             LaunchScope ls("gsd_exchange", st, false);
             for (int k = 0; k < p; ++k) {
                 const uint64_t c = cnt[(size_t)k * p + j];
-                if (!c) continue;
-                const uint64_t so = cut[(size_t)k * (p + 1) + j];
-                RS_CUDA_TRY(cudaMemcpyAsync(rk + off * key_bytes, static_cast<char*>(keys[k]) + so * key_bytes,
-                                            c * key_bytes, cudaMemcpyDeviceToDevice, st));
-                if (hv)
-                    RS_CUDA_TRY(cudaMemcpyAsync(L.recv_vals + off, vals[k] + so, c * 4, cudaMemcpyDeviceToDevice, st));
-                off += c;
+                if (c) {
+                    const uint64_t so = cut[(size_t)k * (p + 1) + j];
+                    RS_CUDA_TRY(cudaMemcpyAsync(rk + off * key_bytes, static_cast<char*>(keys[k]) + so * key_bytes,
+                                                c * key_bytes, cudaMemcpyDeviceToDevice, st));
+                    if (hv)
+                        RS_CUDA_TRY(cudaMemcpyAsync(L.recv_vals + off, vals[k] + so, c * 4, cudaMemcpyDeviceToDevice, st));
+                    off += c;
+                }
+                roff.push_back(off);
             }
         }
-        if ((sst = merge_runs(key_bytes, L.recv_keys, L.recv_vals, off, digit_bits, out_keys[j],
+        if ((sst = merge_runs(key_bytes, L.recv_keys, L.recv_vals, roff, digit_bits, out_keys[j],
                               hv ? out_vals[j] : nullptr, L, st)) != RS_OK)
             return sst;
     }

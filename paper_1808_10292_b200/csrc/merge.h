@@ -1,0 +1,17 @@
+// GSD step 5: stable p-way merge of the received runs (merge.cu).
+#pragma once
+#include <cstdint>
+#include <vector>
+
+#include "runtime.h"
+
+namespace rs {
+
+// scratch (device) bytes for the co-rank table of one 2-way merge of `total` keys
+size_t merge_scratch_bytes(size_t total);
+// runs: p sorted runs at [roff[k], roff[k+1]) (source-rank order), clobbered;
+// tmp: scratch of roff[p] keys (+ values); out: Y_j.  Ties go to the lower run.
+rs_status_t merge_runs_tree(int key_bytes, void* runs, uint32_t* vruns, const std::vector<uint64_t>& roff, void* tmp,
+                            uint32_t* vtmp, void* out, uint32_t* vout, size_t* split, cudaStream_t st);
+
+}  // namespace rs

@@ -15,11 +15,14 @@
 //   [store]  consecutive threads store consecutive s_out slots: each bucket run
 //            is a coalesced burst at base[d] + prefix[d] + offset
 #pragma once
+#include <type_traits>
+
 #include "radix8.cuh"
 
 namespace rs {
 
-template <typename K, bool HAS_VAL, int RT, int KPT, bool LBW = true>
+// COMPACT: 16-bit per-warp counters and no atomic-OR mask array (fits 4 CTAs/SM)
+template <typename K, bool HAS_VAL, int RT, int KPT, bool LBW = true, bool COMPACT = false>
 struct OnesweepEcCfg {
     static constexpr int R = 256;
     static constexpr int W = RT / 32;                 // ranking warps
@@ -31,8 +34,8 @@ struct OnesweepEcCfg {
     static constexpr size_t vin_off = out_off + (size_t)TILE * sizeof(K);
     static constexpr size_t vout_off = vin_off + (HAS_VAL ? (size_t)TILE * 4 : 0);
     static constexpr size_t wc_off = vout_off + (HAS_VAL ? (size_t)TILE * 4 : 0);
-    static constexpr size_t wm_off = wc_off + (size_t)W * R * 4;        // peer masks (RANKV 1)
-    static constexpr size_t texcl_off = wm_off + (size_t)W * R * 4;
+    static constexpr size_t wm_off = wc_off + (size_t)W * R * (COMPACT ? 2 : 4);   // peer masks (RANKV 1, 2)
+    static constexpr size_t texcl_off = wm_off + (COMPACT ? 0 : (size_t)W * R * 4);
     static constexpr size_t tcnt_off = texcl_off + R * 4;
     static constexpr size_t gofs_off = tcnt_off + R * 4;
     static constexpr size_t misc_off = gofs_off + R * 4;
@@ -54,10 +57,12 @@ __device__ __forceinline__ uint32_t digit8<uint32_t>(uint32_t k, int shift) {
 // so stable by construction) instead of ballots.
 // DBG: compile in the timing-ablation switches (a.debug_skip); off in normal builds.
 template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, bool LBW, int ME = 0, int RANKV = 0,
-          bool DBG = false>
+          bool DBG = false, bool COMPACT = false>
 __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassArgs a) {
     using ST = Status<S>;
-    using C = OnesweepEcCfg<K, HAS_VAL, RT, KPT, LBW>;
+    using C = OnesweepEcCfg<K, HAS_VAL, RT, KPT, LBW, COMPACT>;
+    using CT = typename std::conditional<COMPACT, uint16_t, uint32_t>::type;  // per-warp counter type
+    static_assert(!COMPACT || RANKV == 0, "the compact layout has no mask array");
     constexpr int R = C::R, W = C::W, WK = C::WK, TILE = C::TILE, THREADS = C::THREADS;
     static_assert(RT >= R, "one ranking thread per digit in the offset phase");
     extern __shared__ __align__(128) unsigned char smem[];
@@ -65,7 +70,9 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
     K* s_out = reinterpret_cast<K*>(smem + C::out_off);
     uint32_t* s_vin = reinterpret_cast<uint32_t*>(smem + C::vin_off);
     uint32_t* s_vout = reinterpret_cast<uint32_t*>(smem + C::vout_off);
-    uint32_t* s_wc = reinterpret_cast<uint32_t*>(smem + C::wc_off);
+    CT* s_wc = reinterpret_cast<CT*>(smem + C::wc_off);
+    uint32_t* s_wc32 = reinterpret_cast<uint32_t*>(smem + C::wc_off);
+    constexpr int WCW = W * R * (int)sizeof(CT) / 4;  // counter words
     uint32_t* s_wm = reinterpret_cast<uint32_t*>(smem + C::wm_off);
     uint32_t* s_texcl = reinterpret_cast<uint32_t*>(smem + C::texcl_off);
     uint32_t* s_tcnt = reinterpret_cast<uint32_t*>(smem + C::tcnt_off);
@@ -115,7 +122,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
         s_misc[0] = t0;
         if (t0 < a.num_tiles) issue_load(t0);
     }
-    for (int i = tid; i < W * R; i += THREADS) s_wc[i] = 0;
+    for (int i = tid; i < WCW; i += THREADS) s_wc32[i] = 0;
     if (RANKV != 0)
         for (int i = tid; i < W * R; i += THREADS) s_wm[i] = 0;  // kept zero by the group leaders
     __syncthreads();
@@ -143,10 +150,19 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
 
         // ---- [count] per-warp digit histograms
         if (warp < W && !(DBG && (a.debug_skip & 8))) {  // (bit 3: ablation, no counting)
-            uint32_t* wc = s_wc + warp * R;
             const K* in = s_in + warp * WK + lane;
+            if (COMPACT) {
+                uint32_t* wc = s_wc32 + warp * (R / 2);
 #pragma unroll 8
-            for (int j = 0; j < KPT; ++j) atomicAdd(&wc[digit8<K>(in[j * 32], shift)], 1u);
+                for (int j = 0; j < KPT; ++j) {
+                    const uint32_t d = digit8<K>(in[j * 32], shift);
+                    atomicAdd(&wc[d >> 1], 1u << ((d & 1) << 4));
+                }
+            } else {
+                uint32_t* wc = s_wc32 + warp * R;
+#pragma unroll 8
+                for (int j = 0; j < KPT; ++j) atomicAdd(&wc[digit8<K>(in[j * 32], shift)], 1u);
+            }
         }
         __syncthreads();
 
@@ -156,7 +172,8 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
             uint32_t tcnt = 0;
 #pragma unroll
             for (int w = 0; w < W; ++w) {
-                c[w] = s_wc[w * R + tid];
+                c[w] = COMPACT ? (s_wc32[w * (R / 2) + (tid >> 1)] >> ((tid & 1) << 4)) & 0xFFFFu
+                               : s_wc32[w * R + tid];
                 tcnt += c[w];
             }
             uint32_t incl = tcnt;
@@ -176,7 +193,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
             s_texcl[tid] = run;
 #pragma unroll
             for (int w = 0; w < W; ++w) {
-                s_wc[w * R + tid] = run;
+                s_wc[w * R + tid] = (CT)run;
                 run += c[w];
             }
         }
@@ -233,7 +250,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
             // taken in pairs: both peer masks are computed before either counter
             // update so their independent ALU chains interleave; every ME-th key
             // uses match.any instead (ADU pipe) to offload the ALU pipe.
-            uint32_t* wc = s_wc + warp * R;
+            CT* wc = s_wc + warp * R;
             const int ibase = warp * WK + lane;
             auto place = [&](const K k, const uint32_t d, const uint32_t peers, const int idx) {
                 const uint32_t cnt = wc[d];
@@ -241,7 +258,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
                 s_out[pos] = k;
                 if (HAS_VAL) s_vout[pos] = s_vin[idx];
                 __syncwarp();
-                if ((peers & gt) == 0) wc[d] = cnt + __popc(peers);
+                if ((peers & gt) == 0) wc[d] = (CT)(cnt + __popc(peers));
                 __syncwarp();
             };
             static_assert(KPT % 2 == 0, "keys are ranked in pairs");
@@ -263,7 +280,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
                     if (HAS_VAL) s_vout[pos] = s_vin[idx];
                     __syncwarp();
                     if ((peers & gt) == 0) {
-                        wc[d] = cnt + __popc(peers);
+                        wc[d] = (CT)(cnt + __popc(peers));
                         wm[d] = 0;
                     }
                     __syncwarp();
@@ -287,7 +304,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
                     if (HAS_VAL) s_vout[pos] = s_vin[i1];
                     __syncwarp();
                     if ((p1 & gt) == 0) {
-                        wc[d1] = cnt + __popc(p1);
+                        wc[d1] = (CT)(cnt + __popc(p1));
                         wm[d1] = 0;
                     }
                     __syncwarp();
@@ -340,7 +357,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
             s_misc[0] = nt;
             if (nt < a.num_tiles) issue_load(nt);
         }
-        for (int i = tid; i < W * R; i += THREADS) s_wc[i] = 0;
+        for (int i = tid; i < WCW; i += THREADS) s_wc32[i] = 0;
 
         // ---- [store] bucket runs leave as coalesced bursts
 #pragma unroll 4

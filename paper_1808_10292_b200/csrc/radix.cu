@@ -165,11 +165,11 @@ static rs_status_t launch_pass_v(const PassArgs& a, size_t T, cudaStream_t st) {
     return RS_OK;
 }
 
-template <typename K, bool V, typename S, bool LBW, int ME, int RANKV = 0, bool DBG = false>
+template <typename K, bool V, typename S, bool LBW, int ME, int RANKV = 0, bool DBG = false, bool COMPACT = false>
 static rs_status_t launch_pass_ec(const PassArgs& a, size_t T, cudaStream_t st) {
     using TN = TuneEc<K, V>;
-    using C = OnesweepEcCfg<K, V, TN::THREADS, TN::KPT, LBW>;
-    auto kern = k_onesweep_ec<K, V, TN::THREADS, TN::KPT, TN::MINB, S, LBW, ME, RANKV, DBG>;
+    using C = OnesweepEcCfg<K, V, TN::THREADS, TN::KPT, LBW, COMPACT>;
+    auto kern = k_onesweep_ec<K, V, TN::THREADS, TN::KPT, TN::MINB, S, LBW, ME, RANKV, DBG, COMPACT>;
     static int grid_cap = 0;
     if (!grid_cap) {
         RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
@@ -187,6 +187,7 @@ static rs_status_t launch_pass_ec(const PassArgs& a, size_t T, cudaStream_t st) 
 template <typename K, bool V, typename S, bool LBW>
 static rs_status_t launch_pass_ec_me(const PassArgs& a, size_t T, cudaStream_t st) {
     if (options().debug_skip) return launch_pass_ec<K, V, S, LBW, 0, 0, true>(a, T, st);
+    if (options().compact) return launch_pass_ec<K, V, S, LBW, 0, 0, false, true>(a, T, st);
     if (options().rank_variant == 2) return launch_pass_ec<K, V, S, LBW, 0, 1>(a, T, st);
     if (options().rank_variant == 3) return launch_pass_ec<K, V, S, LBW, 0, 2>(a, T, st);
     if (std::is_same<K, uint32_t>::value && !V) {

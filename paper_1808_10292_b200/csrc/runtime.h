@@ -40,6 +40,8 @@ struct Options {
     bool wide_status = false;     // force 64-bit look-back status words (tests)
     unsigned debug_skip = 0;      // timing ablations (invalid output): 1 look-back, 2 rank, 4 store, 8 reorder
     int rank_variant = 3;         // 0 ballot peers, 1 match.any, 2 atomic-OR peers, 3 hybrid pairs
+    int gsd_merge = 0;            // GSD step 5: 0 merge tree, 1 stable radix re-sort
+    bool compact = false;         // design 2: 16-bit per-warp counters, ballots only (4 CTAs/SM)
     int match_every = 0;          // design 2, u32 keys: every k-th key ranked by match.any (0 = none)
     int pass_design = 2;          // 0 classic single sweep; early counts + prefetch with 1 a look-back
                                   // warp, 2 look-back after ranking; 3 counter-ranked nibble sub-passes

@@ -78,3 +78,40 @@ def test_gsd_config4_shape_reduced():
     Y = np.concatenate([host(y, np.uint32) for y in got["Y"]])
     assert (Y == oracle.sr(a, 8)).all()
     assert max(got["n_out"]) <= N + N // 8
+
+
+@pytest.fixture
+def option():
+    names = []
+
+    def _set(name, value):
+        assert rs.lib().rs_set_option(name.encode(), value) == 0
+        names.append(name)
+    yield _set
+    for name in names:
+        rs.lib().rs_set_option(name.encode(), 0)
+
+
+@pytest.mark.parametrize("merge", [0, 1])
+@pytest.mark.parametrize("p", [2, 3, 5, 6, 7, 8])
+def test_gsd_merge_tree_and_resort(option, merge, p):
+    """Step 5 as the merge tree (0) and as a stable re-sort (1): identical Y_j,
+    for odd run counts too; narrow pair keys check the tie rule (lower rank first)."""
+    option("gsd_merge", merge)
+    N = 9000 + 37 * p
+    k = inputs.gen_u64(p * N, 70 + p, "mod1024")
+    v = inputs.iota_u32(p * N)
+    got = _check([k[i * N:(i + 1) * N] for i in range(p)], r=8, b=8, vals_np=[v[i * N:(i + 1) * N] for i in range(p)])
+    K = np.concatenate([host(y, np.uint64) for y in got["Y"]])
+    V = np.concatenate([host(y, np.uint32) for y in got["Yv"]])
+    assert oracle.pairs_stable(K, V)
+    a = inputs.gen_u32(p * N, 80 + p)
+    _check([a[i * N:(i + 1) * N] for i in range(p)], r=8, b=8)
+
+
+def test_merge_tree_large_runs(option):
+    """Merge tree over big uneven runs (several merge tiles per pair)."""
+    option("gsd_merge", 0)
+    blocks = [inputs.gen_u32(n, 90 + i, "sorted" if i % 2 else "uniform") for i, n in
+              enumerate((300000, 17, 250001, 0, 123457))]
+    _check(blocks, r=8, b=8)

@@ -289,3 +289,18 @@ def test_match_every_hybrid_ranking(option, me):
     for t in range(1, 5):
         got = host(rs.sort_bits(dev(a), end_bit=8 * t, digit_bits=8), np.uint32)
         assert (got == oracle.sr(a, 8, rounds=t)).all(), t
+
+
+def test_compact_layout(option):
+    """design 2 with 16-bit per-warp counters (compact shared-memory layout)."""
+    option("compact", 1)
+    a = inputs.gen_u32(9 * TILE32 + 77, 45)
+    for t in range(1, 5):
+        got = host(rs.sort_bits(dev(a), end_bit=8 * t, digit_bits=8), np.uint32)
+        assert (got == oracle.sr(a, 8, rounds=t)).all(), t
+    k = inputs.gen_u64(5 * TILE64 + 7, 46, "mod1024")
+    v = inputs.iota_u32(k.size)
+    tk, tv = dev(k), dev(v)
+    rs.sort_pairs(tk, tv)
+    wk, wv = oracle.sr(k, 8, vals=v)
+    assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
