@@ -28,8 +28,10 @@
  *     on a sort call: scratch comes from `ws` (size from rs_workspace_bytes).
  *   - Calls are asynchronous on `stream` unless stated; they never abort or
  *     throw.  Arguments are validated before anything is enqueued, so on
- *     RS_EINVAL / RS_ECAPACITY the inputs are untouched.  On RS_ECUDA /
- *     RS_ENCCL buffer contents are undefined (and a comm must be destroyed).
+ *     RS_EINVAL the inputs are untouched (single GPU: also on RS_ECAPACITY; the
+ *     GSD collective detects RS_ECAPACITY after its local sort, so `keys` then
+ *     holds the rank's sorted block).  On RS_ECUDA / RS_ENCCL buffer contents
+ *     are undefined (and a comm must be destroyed).
  *   - rs_last_error() returns a thread-local message for the last failure.
  *   - n = 0 is a no-op returning RS_OK (a rank with n = 0 still participates
  *     in a collective call).  n must be < 2^32 per GPU.

@@ -4,6 +4,15 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Checked builds (-DRS_CHECKED, tests only): bounds asserts on computed store
+// indices (compute-sanitizer is not available on the GPU pool).
+#ifdef RS_CHECKED
+#include <cassert>
+#define RS_DCHECK(cond) assert(cond)
+#else
+#define RS_DCHECK(cond) ((void)0)
+#endif
+
 namespace rs {
 
 constexpr int kMaxPasses = 16;

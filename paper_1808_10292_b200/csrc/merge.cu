@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "common.cuh"
 #include "merge.h"
 
 namespace rs {
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(kMT) k_merge_tile(const K* __restrict__ A, con
         }
     __syncthreads();
     for (int i = threadIdx.x; i < len; i += kMT) {
+        RS_DCHECK(d0 + i < na + nb);
         out[d0 + i] = s_k[mpad(i)];
         if (V) vout[d0 + i] = s_v[mpad(i)];
     }

@@ -235,6 +235,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_onesweep(PassArgs a) {
             const uint32_t d = digit_of<K>(key[j], shift, mask);
             const uint32_t r = (rk[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu;
             const uint32_t pos = s_texcl[d] + wc[d * CS] + r;
+            RS_DCHECK(pos < (uint32_t)TILE);
             s_keys[pos] = key[j];
             if (HAS_VAL) s_vals[pos] = val[j];
         }
@@ -277,6 +278,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_onesweep(PassArgs a) {
             if (a.debug_skip & 4) break;  // ablation: no global store
             const K k = s_keys[i];
             const uint32_t g = s_gofs[digit_of<K>(k, shift, mask)] + i;
+            RS_DCHECK(g < a.n);
             dst[g] = k;
             if (HAS_VAL) vdst[g] = s_vals[i];
         }

@@ -96,6 +96,7 @@ __device__ __forceinline__ void nibble_subpass(const K (&k)[KPT], const uint32_t
     for (int j = 0; j < KPT; ++j) {
         const uint32_t nb = static_cast<uint32_t>(k[j] >> nshift) & 0xFu;
         const uint32_t r = (uint32_t)s_cnt[nb * RT + tid] + ((pre[j >> 1] >> ((j & 1) * 16)) & 0xFFFFu);
+        RS_DCHECK(r < (uint32_t)(RT * KPT));
         dst[r] = k[j];
         if (HAS_VAL) vdst[r] = v[j];
     }
@@ -307,6 +308,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_cr(PassArgs a) {
         for (uint32_t i = tid; i < valid; i += THREADS) {
             const K key = bufA[i];
             const uint32_t g = s_gofs[digit8<K>(key, shift)] + i;
+            RS_DCHECK(g < a.n);
             dst[g] = key;
             if (HAS_VAL) vdst[g] = vbufA[i];
         }

@@ -255,6 +255,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
             auto place = [&](const K k, const uint32_t d, const uint32_t peers, const int idx) {
                 const uint32_t cnt = wc[d];
                 const uint32_t pos = cnt + __popc(peers & lt);
+                RS_DCHECK(pos < (uint32_t)TILE);
                 s_out[pos] = k;
                 if (HAS_VAL) s_vout[pos] = s_vin[idx];
                 __syncwarp();
@@ -276,6 +277,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
                     const uint32_t peers = wm[d];
                     const uint32_t cnt = wc[d];
                     const uint32_t pos = cnt + __popc(peers & lt);
+                    RS_DCHECK(pos < (uint32_t)TILE);
                     s_out[pos] = k;
                     if (HAS_VAL) s_vout[pos] = s_vin[idx];
                     __syncwarp();
@@ -300,6 +302,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
                     const uint32_t p1 = wm[d1];
                     const uint32_t cnt = wc[d1];
                     const uint32_t pos = cnt + __popc(p1 & lt);
+                    RS_DCHECK(pos < (uint32_t)TILE);
                     s_out[pos] = k1;
                     if (HAS_VAL) s_vout[pos] = s_vin[i1];
                     __syncwarp();
@@ -365,6 +368,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
             if (DBG && (a.debug_skip & 4)) break;  // ablation: no global store
             const K k = s_out[i];
             const uint32_t g = s_gofs[digit8<K>(k, shift)] + i;
+            RS_DCHECK(g < a.n);
             dst[g] = k;
             if (HAS_VAL) vdst[g] = s_vout[i];
         }

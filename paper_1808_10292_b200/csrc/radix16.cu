@@ -156,6 +156,7 @@ __device__ __forceinline__ void smem_pass8(const K* A, K* B, const uint32_t* VA,
     for (int j = 0; j < KPT; ++j) {
         const uint32_t d = static_cast<uint32_t>(key[j] >> shift) & 0xFFu;
         const uint32_t pos = s_aux[32 + d] + wc[d] + rk[j];
+        RS_DCHECK(pos < (uint32_t)kS16Chunk);
         B[pos] = key[j];
         if (V) VB[pos] = val[j];
     }
@@ -243,6 +244,7 @@ __global__ void __launch_bounds__(kS16Threads, 1)
             const uint32_t i = (uint32_t)(i0 + j);
             if (i >= valid) continue;
             const uint32_t o = s_goff[st[j]] + (i - st[j]);
+            RS_DCHECK(o < n);
             dst[o] = kA[i];
             if (V) vdst[o] = vA[i];
             const uint32_t dnext = j + 1 < KPT ? d[j + 1] : (i + 1 < valid ? static_cast<uint32_t>(kA[i + 1] >> shift) & 0xFFFFu : d[j]);
@@ -356,6 +358,7 @@ __global__ void __launch_bounds__(kS16Threads, 1)
             const uint32_t i = (uint32_t)(i0 + j);
             if (i >= valid) continue;
             const uint32_t o = s_goff[st[j]] + (i - st[j]);
+            RS_DCHECK(o < n);
             dst[o] = bufA[i];
             const uint32_t dnext = j + 1 < KPT ? d[j + 1] : (i + 1 < valid ? (bufA[i + 1] >> shift) & 0xFFFFu : d[j]);
             if ((i + 1 == valid) || dnext != d[j]) {

@@ -1,0 +1,66 @@
+"""The NCCL GSD path (rs_sort_* with a communicator) on one GPU with a 1-rank
+NCCL communicator bootstrapped over a torch.distributed process group: header
+all-gather, local sort, sample/splitters/split, count all-gather, the
+(self-)exchange and the merge all run through the multi-GPU code."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+
+import inputs
+import oracle
+import paper_1808_10292_b200 as rs
+from tests.gpu_util import dev, host
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def comm():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    c = rs.Comm(oversampling=8)
+    yield c
+    c.close()
+    dist.destroy_process_group()
+
+
+def test_comm_bootstrap(comm):
+    assert rs.lib().rs_comm_rank(comm.handle) == 0 and rs.lib().rs_comm_size(comm.handle) == 1
+    assert comm.capacity(1000) == 1000 + 1000 // 8 + 1
+
+
+@pytest.mark.parametrize("n", [0, 1, 4097, 100003])
+def test_gsd_p1_u32(comm, n):
+    a = inputs.gen_u32(n, 50 + n)
+    t = dev(a) if n else torch.empty(0, dtype=torch.int32, device="cuda")
+    y = rs.sort(t, comm=comm)
+    assert y.numel() == n
+    if n:
+        assert (host(y, np.uint32) == oracle.sr(a, 8)).all()
+
+
+@pytest.mark.parametrize("b", [8, 16])
+def test_gsd_p1_pairs_and_u64(comm, b):
+    n = 50001
+    k = inputs.gen_u64(n, 60, "mod1024")
+    v = inputs.iota_u32(n)
+    yk, yv = rs.sort_pairs(dev(k), dev(v), digit_bits=b, comm=comm)
+    wk, wv = oracle.sr(k, b, vals=v)
+    assert (host(yk, np.uint64) == wk).all() and (host(yv, np.uint32) == wv).all()
+    y = rs.sort(dev(k), digit_bits=b, comm=comm)
+    assert (host(y, np.uint64) == np.sort(k)).all()
+
+
+def test_gsd_capacity_error(comm):
+    a = inputs.gen_u32(1000, 61)
+    with pytest.raises(rs.RSortError) as e:
+        rs.sort(dev(a), comm=comm, out_cap=999)
+    assert e.value.status == 5
