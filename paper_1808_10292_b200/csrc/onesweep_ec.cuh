@@ -287,6 +287,33 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
                     }
                     __syncwarp();
                 }
+            } else if (RANKV == 3) {
+                // ballot peers; the group's leader (highest lane) advances the warp
+                // counter with one atomicAdd returning the old value, which the
+                // group reads by shuffle: no load->store chain through shared memory
+#pragma unroll 2
+                for (int j = 0; j < KPT; j += 2) {
+                    const int i0 = ibase + j * 32, i1 = i0 + 32;
+                    const K k0 = s_in[i0], k1 = s_in[i1];
+                    const uint32_t d0 = digit8<K>(k0, shift), d1 = digit8<K>(k1, shift);
+                    const uint32_t p0 = peers8(d0), p1 = peers8(d1);
+                    const int l0 = 31 - __clz(p0), l1 = 31 - __clz(p1);
+                    uint32_t o0 = 0, o1 = 0;
+                    if (lane == l0) o0 = atomicAdd(reinterpret_cast<uint32_t*>(&wc[d0]), (uint32_t)__popc(p0));
+                    __syncwarp();
+                    if (lane == l1) o1 = atomicAdd(reinterpret_cast<uint32_t*>(&wc[d1]), (uint32_t)__popc(p1));
+                    o0 = __shfl_sync(0xffffffffu, o0, l0);
+                    o1 = __shfl_sync(0xffffffffu, o1, l1);
+                    const uint32_t pos0 = o0 + __popc(p0 & lt), pos1 = o1 + __popc(p1 & lt);
+                    RS_DCHECK(pos0 < (uint32_t)TILE && pos1 < (uint32_t)TILE);
+                    s_out[pos0] = k0;
+                    s_out[pos1] = k1;
+                    if (HAS_VAL) {
+                        s_vout[pos0] = s_vin[i0];
+                        s_vout[pos1] = s_vin[i1];
+                    }
+                    __syncwarp();
+                }
             } else if (RANKV == 2) {
                 // hybrid pairs: key j by ballots (ALU pipe), key j+1 by an atomic-OR
                 // peer mask (shared-memory pipe) whose latency hides behind the ballots
@@ -320,6 +347,12 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
                 const uint32_t d0 = digit8<K>(k0, shift), d1 = digit8<K>(k1, shift);
                 const uint32_t p0 = (ME > 0 && (j % ME) == 0) ? __match_any_sync(0xffffffffu, d0) : peers8(d0);
                 const uint32_t p1 = peers8(d1);
+                if (DBG && (a.debug_skip & 16)) {  // experiment: one extra random shared load per key
+                    uint32_t x0, x1;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x0) : "r"(smem_addr(wc + ((d0 * 37u) & 255u))));
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x1) : "r"(smem_addr(wc + ((d1 * 37u) & 255u))));
+                    if ((x0 ^ x1) == 0xDEADBEEFu) s_misc[63] = x0;
+                }
                 place(k0, d0, p0, i0);
                 place(k1, d1, p1, i1);
             }

@@ -10,6 +10,7 @@
 #include "onesweep.cuh"
 #include "onesweep_ec.cuh"
 #include "onesweep_cr.cuh"
+#include "onesweep_n4.cuh"
 #include "radix16.cuh"
 #include "runtime.h"
 
@@ -101,8 +102,26 @@ struct TuneCr<uint64_t, true> : TuneT<RS_CR_PAIRS_T, RS_CR_PAIRS_KPT, RS_CR_PAIR
 template <>
 struct TuneCr<uint32_t, true> : TuneT<256, 12, 3> {};
 
+// register-nibble-counter design (4)
+#ifndef RS_N4_U32_T
+#define RS_N4_U32_T 256
+#define RS_N4_U32_KPT 24
+#define RS_N4_U32_MINB 3
+#endif
+template <typename K, bool V>
+struct TuneN4;
+template <>
+struct TuneN4<uint32_t, false> : TuneT<RS_N4_U32_T, RS_N4_U32_KPT, RS_N4_U32_MINB> {};
+template <>
+struct TuneN4<uint64_t, false> : TuneT<256, 12, 3> {};
+template <>
+struct TuneN4<uint64_t, true> : TuneT<256, 12, 2> {};
+template <>
+struct TuneN4<uint32_t, true> : TuneT<256, 12, 3> {};
+
 template <typename K, bool V>
 static int tile_keys() {
+    if (options().pass_design == 4) return TuneN4<K, V>::THREADS * TuneN4<K, V>::KPT;
     if (options().pass_design == 3) return TuneCr<K, V>::THREADS * TuneCr<K, V>::KPT;
     if (options().pass_design >= 1) return TuneEc<K, V>::THREADS * TuneEc<K, V>::KPT;
     return Tune<K, V>::THREADS * Tune<K, V>::KPT;
@@ -190,6 +209,7 @@ static rs_status_t launch_pass_ec_me(const PassArgs& a, size_t T, cudaStream_t s
     if (options().compact) return launch_pass_ec<K, V, S, LBW, 0, 0, false, true>(a, T, st);
     if (options().rank_variant == 2) return launch_pass_ec<K, V, S, LBW, 0, 1>(a, T, st);
     if (options().rank_variant == 3) return launch_pass_ec<K, V, S, LBW, 0, 2>(a, T, st);
+    if (options().rank_variant == 4) return launch_pass_ec<K, V, S, LBW, 0, 3>(a, T, st);
     if (std::is_same<K, uint32_t>::value && !V) {
         switch (options().match_every) {
             case 4: return launch_pass_ec<K, V, S, LBW, 4>(a, T, st);
@@ -219,8 +239,30 @@ static rs_status_t launch_pass_cr(const PassArgs& a, size_t T, cudaStream_t st) 
     return RS_OK;
 }
 
+template <typename K, bool V, typename S>
+static rs_status_t launch_pass_n4(const PassArgs& a, size_t T, cudaStream_t st) {
+    using TN = TuneN4<K, V>;
+    using C = OnesweepN4Cfg<K, V, TN::THREADS, TN::KPT>;
+    auto kern = k_onesweep_n4<K, V, TN::THREADS, TN::KPT, TN::MINB, S>;
+    static int grid_cap = 0;
+    if (!grid_cap) {
+        RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
+        int per_sm = 0;
+        RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TN::THREADS, C::smem_bytes));
+        grid_cap = std::max(1, per_sm) * sm_count();
+    }
+    const unsigned grid = (unsigned)std::min<size_t>(T, (size_t)grid_cap);  // persistent CTAs
+    LaunchScope ls("onesweep", st);
+    kern<<<grid, TN::THREADS, C::smem_bytes, st>>>(a);
+    return RS_OK;
+}
+
 template <typename K, bool V>
 static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStream_t st) {
+    if (options().pass_design == 4) {
+        if (wide) return launch_pass_n4<K, V, uint64_t>(a, T, st);
+        return launch_pass_n4<K, V, uint32_t>(a, T, st);
+    }
     if (options().pass_design == 3) {
         if (wide) return launch_pass_cr<K, V, uint64_t>(a, T, st);
         return launch_pass_cr<K, V, uint32_t>(a, T, st);

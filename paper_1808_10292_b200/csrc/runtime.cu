@@ -133,13 +133,13 @@ rs_status_t rs_set_option(const char* name, long long value) {
     if (!name || value < 0) return fail(RS_EINVAL, "rs_set_option: bad name / negative value");
     const std::string n(name);
     if (n == "wide_status" && value <= 1) options().wide_status = value != 0;
-    else if (n == "debug_skip" && value <= 15) options().debug_skip = (unsigned)value;
+    else if (n == "debug_skip" && value <= 31) options().debug_skip = (unsigned)value;
     else if (n == "gsd_merge" && value <= 1) options().gsd_merge = (int)value;
     else if (n == "compact" && value <= 1) options().compact = value != 0;
     else if (n == "match_every" && (value == 0 || value == 4 || value == 6 || value == 8))
         options().match_every = (int)value;
-    else if (n == "pass_design" && value <= 3) options().pass_design = (int)value;
-    else if (n == "rank_variant" && value <= 3) options().rank_variant = (int)value;
+    else if (n == "pass_design" && value <= 4) options().pass_design = (int)value;
+    else if (n == "rank_variant" && value <= 4) options().rank_variant = (int)value;
     else return fail(RS_EINVAL, "rs_set_option: unknown option or value: " + n);
     return RS_OK;
 }

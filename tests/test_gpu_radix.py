@@ -243,7 +243,7 @@ def test_wide_status_lookback(option, kind):
             assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
 
 
-@pytest.mark.parametrize("variant", [1, 2, 3])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4])
 def test_rank_variants(option, variant):
     """match.any (1) and atomic-OR (2) peer masks give the same stable ranks."""
     option("rank_variant", variant)
@@ -257,7 +257,7 @@ def test_rank_variants(option, variant):
     assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
 
 
-@pytest.mark.parametrize("design", [0, 1, 2, 3])
+@pytest.mark.parametrize("design", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("wide", [0, 1])
 def test_pass_designs(option, design, wide):
     """Every radix-256 pass kernel design (classic; early counts with a
