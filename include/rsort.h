@@ -174,8 +174,9 @@ rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits,
 /* --------------------------------------------------------------- options -- */
 /* Process-wide tuning / test knobs (not needed for normal use):
  *   "wide_status"    1 = use 64-bit look-back status words at any n (they are
- *                    used automatically when n >= 2^30, where 30-bit counts
- *                    could overflow); lets the tests run that path on small n.
+ *                    used automatically when n > 2^31, where a 31-bit
+ *                    inclusive prefix could overflow); lets the tests run that
+ *                    path on small n.
  *   "rank_variant"   in-tile ranking: 3 = pairs of keys, one by 8 ballots and one
  *                    by a shared-memory atomic-OR peer mask (default); 0 = ballots;
  *                    2 = atomic-OR masks; 1 = match.any (classic design only).

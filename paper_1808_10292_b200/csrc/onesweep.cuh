@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(THREADS, MINB) k_onesweep(PassArgs a) {
                     for (int i = 0; i < LB; ++i) {
                         if (done) break;
                         while ((v[i] & (ST::kFlagA | ST::kFlagP)) == 0) v[i] = ld_relaxed_gpu(sp - (size_t)i * R);
-                        excl += v[i] & ST::kValMask;
+                        excl += ST::val(v[i]);
                         done = (v[i] & ST::kFlagP) != 0;
                     }
                     sp -= (size_t)LB * R;

@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_cr(PassArgs a) {
                             __nanosleep(64);
                             vv[i] = ld_relaxed_gpu(sp - (size_t)i * R);
                         }
-                        excl += vv[i] & ST::kValMask;
+                        excl += ST::val(vv[i]);
                         done = (vv[i] & ST::kFlagP) != 0;
                     }
                     sp -= (size_t)LB * R;

@@ -128,6 +128,10 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
     __syncthreads();
     uint32_t tile = s_misc[0];
     uint32_t phase = 0;
+    // KREG: the ranking warps keep their keys in registers from [count] to [rank]
+    // (one shared-memory read of the tile instead of two)
+    constexpr bool KREG = !DBG && !COMPACT && ME == 0 && (RANKV == 0 || RANKV == 2);
+    K kr[KREG ? KPT : 1];
 
     while (tile < a.num_tiles) {
         const size_t base = (size_t)tile * TILE;
@@ -157,6 +161,13 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
                 for (int j = 0; j < KPT; ++j) {
                     const uint32_t d = digit8<K>(in[j * 32], shift);
                     atomicAdd(&wc[d >> 1], 1u << ((d & 1) << 4));
+                }
+            } else if (KREG) {
+                uint32_t* wc = s_wc32 + warp * R;
+#pragma unroll
+                for (int j = 0; j < KPT; ++j) {
+                    kr[j] = in[j * 32];
+                    atomicAdd(&wc[digit8<K>(kr[j], shift)], 1u);
                 }
             } else {
                 uint32_t* wc = s_wc32 + warp * R;
@@ -228,7 +239,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
                                 S s = v[k][i];
                                 while ((s & (ST::kFlagA | ST::kFlagP)) == 0)
                                     s = ld_relaxed_gpu(status + (size_t)(tile - off - i) * R + d0 + 32 * k);
-                                excl[k] += s & ST::kValMask;
+                                excl[k] += ST::val(s);
                                 if (s & ST::kFlagP) done |= 1u << k;
                             }
                         }
@@ -318,10 +329,10 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
                 // hybrid pairs: key j by ballots (ALU pipe), key j+1 by an atomic-OR
                 // peer mask (shared-memory pipe) whose latency hides behind the ballots
                 uint32_t* wm = s_wm + warp * R;
-#pragma unroll 2
+#pragma unroll
                 for (int j = 0; j < KPT; j += 2) {
                     const int i0 = ibase + j * 32, i1 = i0 + 32;
-                    const K k0 = s_in[i0], k1 = s_in[i1];
+                    const K k0 = KREG ? kr[KREG ? j : 0] : s_in[i0], k1 = KREG ? kr[KREG ? j + 1 : 0] : s_in[i1];
                     const uint32_t d0 = digit8<K>(k0, shift), d1 = digit8<K>(k1, shift);
                     atomicOr(&wm[d1], 1u << lane);
                     const uint32_t p0 = peers8(d0);
@@ -340,10 +351,10 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
                     __syncwarp();
                 }
             } else
-#pragma unroll 2
+#pragma unroll
             for (int j = 0; j < KPT; j += 2) {
                 const int i0 = ibase + j * 32, i1 = i0 + 32;
-                const K k0 = s_in[i0], k1 = s_in[i1];
+                const K k0 = KREG ? kr[KREG ? j : 0] : s_in[i0], k1 = KREG ? kr[KREG ? j + 1 : 0] : s_in[i1];
                 const uint32_t d0 = digit8<K>(k0, shift), d1 = digit8<K>(k1, shift);
                 const uint32_t p0 = (ME > 0 && (j % ME) == 0) ? __match_any_sync(0xffffffffu, d0) : peers8(d0);
                 const uint32_t p1 = peers8(d1);
@@ -375,7 +386,7 @@ __global__ void __launch_bounds__(RT + (LBW ? 32 : 0), MINB) k_onesweep_ec(PassA
                     for (int i = 0; i < LB; ++i) {
                         if (done) break;
                         while ((v[i] & (ST::kFlagA | ST::kFlagP)) == 0) v[i] = ld_relaxed_gpu(sp - (size_t)i * R);
-                        excl += v[i] & ST::kValMask;
+                        excl += ST::val(v[i]);
                         done = (v[i] & ST::kFlagP) != 0;
                     }
                     sp -= (size_t)LB * R;

@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_n4(PassArgs a) {
                     for (int i = 0; i < LB; ++i) {
                         if (done) break;
                         while ((w8[i] & (ST::kFlagA | ST::kFlagP)) == 0) w8[i] = ld_relaxed_gpu(sp - (size_t)i * R);
-                        excl += w8[i] & ST::kValMask;
+                        excl += ST::val(w8[i]);
                         done = (w8[i] & ST::kFlagP) != 0;
                     }
                     sp -= (size_t)LB * R;

@@ -148,7 +148,7 @@ static Layout8 layout8(void* ws, int key_bytes, bool has_val, size_t n) {
     const size_t tile = (size_t)tile_for(key_bytes, has_val);
     const int P = key_bytes * 8 / 8;
     L.T = std::max<size_t>(1, (n + tile - 1) / tile);
-    L.wide = n > kNarrowStatusMaxN || options().wide_status;  // counts need > 30 bits
+    L.wide = n > kNarrowStatusMaxN || options().wide_status;  // P values need > 31 bits
     L.status_bytes = L.T * 256 * (L.wide ? 8 : 4);            // one region
     Carver c(ws);
     L.ctrl = static_cast<Ctrl*>(c.take(sizeof(Ctrl)));

@@ -17,21 +17,27 @@
 //
 // Layout in HBM: keys SoA (u32 or u64) + optional u32 values; ping-pong between
 // the caller's `out` and the workspace `alt`; look-back status [2][T][256]
-// words, flag in the top two bits: u32 words (30-bit counts) when n < 2^30,
+// words, flags in the top bits: u32 words (31-bit prefixes) when n <= 2^31,
 // u64 words (62-bit counts) otherwise.
 #pragma once
 #include "common.cuh"
 
 namespace rs {
 
-// look-back status word: [flag P | flag A | count]
+// look-back status word: 0 = not ready; [0 | 1 | tile count] = aggregate (A);
+// [1 | inclusive prefix] = prefix (P).  A tile count is <= TILE; an inclusive
+// prefix is <= the digit's total, which is <= n - 1 in every active pass (a
+// digit holding all n keys makes the pass trivial and it is skipped), so u32
+// words hold every P value for n <= 2^31 (31 value bits).
 template <typename S>
 struct Status {
     static constexpr S kFlagA = S(1) << (sizeof(S) * 8 - 2);  // tile aggregate available
     static constexpr S kFlagP = S(1) << (sizeof(S) * 8 - 1);  // inclusive prefix available
-    static constexpr S kValMask = kFlagA - 1;
+    static constexpr S kValMask = kFlagA - 1;                 // value bits of an A word
+    static constexpr S kPMask = kFlagP - 1;                   // value bits of a P word
+    __device__ __forceinline__ static S val(S s) { return s & ((s & kFlagP) ? kPMask : kValMask); }
 };
-constexpr uint64_t kNarrowStatusMaxN = (1ull << 30) - 1;  // u32 status words suffice below
+constexpr uint64_t kNarrowStatusMaxN = 1ull << 31;  // u32 status words suffice up to here
 
 enum BufSel : int32_t { kSelIn = 0, kSelOut = 1, kSelAlt = 2 };
 

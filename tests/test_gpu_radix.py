@@ -173,6 +173,29 @@ def test_config4_single_gpu_full_size():
 
 
 @pytest.mark.slow
+def test_31bit_lookback_prefixes():
+    """2^31 - 1001 u32 keys whose low byte is zeroed for the first 3/4: in pass 0
+    digit 0 holds > 2^30 keys, so its inclusive look-back prefixes need the 31st
+    value bit of the narrow (u32) status words (radix8.cuh Status).  Checked by
+    sortedness, multiset hash and sampled order statistics (full size)."""
+    n = (1 << 31) - 1001
+    if free_host_gb() < 20 or free_dev_gb() < 20:
+        pytest.skip("needs ~20 GB host/device")
+    a = inputs.gen_u32(n, 7)
+    a[: 3 * n // 4] &= np.uint32(0xFFFFFF00)
+    h_in = oracle.multiset_hash(a)
+    t = dev(a)
+    rs.sort(t, digit_bits=8)
+    got = host(t, np.uint32)
+    del t
+    torch.cuda.empty_cache()
+    assert oracle.is_nondecreasing(got)
+    assert oracle.multiset_hash(got) == h_in
+    pos = np.unique(np.linspace(0, n - 1, 64).astype(np.uint64))
+    assert oracle.check_order_stats_u32(a, pos, got[pos.astype(np.int64)]) == 0
+
+
+@pytest.mark.slow
 def test_config5_single_gpu_full_size():
     """BASELINE configs[4] at p=1: 2^30 (u64 key, u32 payload = index) pairs,
     seed 5, 8 radix-256 passes; stability via payload order."""
