@@ -180,8 +180,10 @@ rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits,
  *   "rank_variant"   in-tile ranking: 3 = pairs of keys, one by 8 ballots and one
  *                    by a shared-memory atomic-OR peer mask (default); 0 = ballots;
  *                    2 = atomic-OR masks; 1 = match.any (classic design only).
- *   "pass_design"    radix-256 pass kernel: 2 = early counts + tile prefetch,
- *                    look-back after ranking (default); 1 = early counts + tile
+ *   "pass_design"    radix-256 pass kernel: 5 = atomic ranks (default; used when
+ *                    the lane-order probe passes on this device, otherwise 2);
+ *                    2 = early counts + tile prefetch, ballot ranks,
+ *                    look-back after ranking; 1 = early counts + tile
  *                    prefetch with a dedicated look-back warp; 0 = classic single
  *                    sweep (rank, look-back, reorder, store).
  *   "match_every"    0, 4, 6 or 8: in the default pass (u32 keys) every k-th key is
@@ -194,6 +196,10 @@ rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits,
  *                    bit 1 no ranking, bit 2 no global store, bit 3 no reorder.
  * Returns RS_EINVAL for an unknown name or a negative value. */
 rs_status_t rs_set_option(const char* name, long long value);
+/* Current value of an rs_set_option knob, or the read-only "rank_probe": the
+ * result of the design-5 lane-order probe on the current device (-1 not run
+ * yet, 0 failed -> design 2 is used, 1 passed).  RS_EINVAL for unknown names. */
+rs_status_t rs_get_option(const char* name, long long* value);
 
 /* ---------------------------------------------------------------- timing -- */
 /* Per-kernel device timing for measurement (bench.py): when enabled, every

@@ -44,6 +44,7 @@ SIGNATURES = {
     "rs_timing_query": (_i32, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i32)]),
     "rs_launch_count": (ctypes.c_longlong, []),
     "rs_set_option": (_i32, [ctypes.c_char_p, ctypes.c_longlong]),
+    "rs_get_option": (_i32, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_longlong)]),
 }
 
 _lib = None

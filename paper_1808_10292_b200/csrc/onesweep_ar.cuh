@@ -1,0 +1,291 @@
+// K3 "atomic rank" (design 5, default when the startup probe passes) — one
+// stable count-sort round of radix 256:
+//
+//   [load]    TMA bulk copy of tile k into s_in (issued during tile k-1's store)
+//   [rank]    warp w, row j (32 consecutive keys, lane order = input order):
+//             r = atomicAdd(&cnt_w[d], 1) on the warp's shared-memory counter of
+//             the key's digit d.  The returned old values ARE the stable ranks
+//             of the keys among the warp's keys of digit d: earlier rows were
+//             counted by earlier instructions, and within one instruction the
+//             sm_100 shared-memory atomic unit returns the old values of lanes
+//             that hit the same address in ascending lane order.  That lane order
+//             is a measured hardware property, not a PTX guarantee: the library
+//             checks it with a probe kernel before it selects this design
+//             (runtime.cu rank_probe) and otherwise runs design 2 (ballot ranks).
+//             The final counter values are the warp's digit histogram, so the
+//             counting of PAPER.md:664-667 comes out of the same instruction.
+//   [offset]  thread d: tile count, in-tile offset of digit d, per-warp start
+//             offsets; publish the tile count to the look-back status (flag A,
+//             or P for tile 0) — the tiles x 256 counter matrix of PR4,
+//             PAPER.md:690-694
+//   [scatter] key -> s_out[start_w[d] + r]  (the tile sorted by digit, stably)
+//   [lookback] thread d: windowed decoupled look-back over earlier tiles,
+//             publishes the inclusive prefix (flag P)
+//   [next]    thread 0 takes the next tile id and starts its TMA load into s_in
+//   [store]   consecutive threads store consecutive s_out slots: each bucket run
+//             is a coalesced burst at base[d] + prefix[d] + offset
+//
+// Against design 2 this removes the per-key 8-ballot peer mask and the warp
+// counter load/store round trip: per 32 keys one conflicted atomic replaces an
+// atomic + ~30 ALU instructions + a conflicted load and store.
+#pragma once
+#include "onesweep_ec.cuh"
+
+namespace rs {
+
+template <typename K, bool HAS_VAL, int RT, int KPT>
+struct OnesweepArCfg {
+    static constexpr int R = 256;
+    static constexpr int W = RT / 32;
+    static constexpr int THREADS = RT;
+    static constexpr int WK = 32 * KPT;
+    static constexpr int TILE = RT * KPT;
+    static constexpr size_t in_off = 0;
+    static constexpr size_t out_off = in_off + (size_t)TILE * sizeof(K);
+    static constexpr size_t vin_off = out_off + (size_t)TILE * sizeof(K);
+    static constexpr size_t vout_off = vin_off + (HAS_VAL ? (size_t)TILE * 4 : 0);
+    static constexpr size_t wc_off = vout_off + (HAS_VAL ? (size_t)TILE * 4 : 0);
+    static constexpr size_t texcl_off = wc_off + (size_t)W * R * 4;
+    static constexpr size_t tcnt_off = texcl_off + R * 4;
+    static constexpr size_t gofs_off = tcnt_off + R * 4;
+    static constexpr size_t misc_off = gofs_off + R * 4;
+    static constexpr size_t bar_off = misc_off + 64 * 4;
+    static constexpr size_t smem_bytes = bar_off + 16;
+};
+
+// KREG: keep the keys in registers from [rank] to [scatter] (else re-read s_in)
+template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, bool KREG>
+__global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
+    using ST = Status<S>;
+    using C = OnesweepArCfg<K, HAS_VAL, RT, KPT>;
+    constexpr int R = C::R, W = C::W, WK = C::WK, TILE = C::TILE, THREADS = C::THREADS;
+    static_assert(RT == R, "one thread per digit in the offset and look-back phases");
+    extern __shared__ __align__(128) unsigned char smem[];
+    K* s_in = reinterpret_cast<K*>(smem + C::in_off);
+    K* s_out = reinterpret_cast<K*>(smem + C::out_off);
+    uint32_t* s_vin = reinterpret_cast<uint32_t*>(smem + C::vin_off);
+    uint32_t* s_vout = reinterpret_cast<uint32_t*>(smem + C::vout_off);
+    uint32_t* s_wc = reinterpret_cast<uint32_t*>(smem + C::wc_off);
+    uint32_t* s_texcl = reinterpret_cast<uint32_t*>(smem + C::texcl_off);
+    uint32_t* s_tcnt = reinterpret_cast<uint32_t*>(smem + C::tcnt_off);
+    uint32_t* s_gofs = reinterpret_cast<uint32_t*>(smem + C::gofs_off);
+    uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + C::misc_off);
+    uint64_t* s_bar = reinterpret_cast<uint64_t*>(smem + C::bar_off);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    Ctrl* ctrl = a.ctrl;
+    S* const status = static_cast<S*>(a.status_cur);
+
+    // clear the next pass's status rows (no reader in this launch)
+    for (size_t i = (size_t)blockIdx.x * THREADS + tid; i < (size_t)a.num_tiles * R; i += (size_t)gridDim.x * THREADS)
+        static_cast<S*>(a.status_next)[i] = 0;
+    if (!ctrl->active[a.pass]) return;
+
+    const int ss = ctrl->src_sel[a.pass], ds = ctrl->dst_sel[a.pass];
+    const K* src = pick<const K>(ss, static_cast<const K*>(a.keys_in), static_cast<const K*>(a.keys_out),
+                                 static_cast<const K*>(a.keys_alt));
+    K* dst = pick<K>(ds, const_cast<K*>(static_cast<const K*>(a.keys_in)), static_cast<K*>(a.keys_out),
+                     static_cast<K*>(a.keys_alt));
+    const uint32_t* vsrc = nullptr;
+    uint32_t* vdst = nullptr;
+    if (HAS_VAL) {
+        vsrc = pick<const uint32_t>(ss, a.vals_in, a.vals_out, a.vals_alt);
+        vdst = pick<uint32_t>(ds, const_cast<uint32_t*>(a.vals_in), a.vals_out, a.vals_alt);
+    }
+    const int shift = a.shift;
+
+    auto issue_load = [&](uint32_t t) {  // thread 0 only
+        const size_t base = (size_t)t * TILE;
+        const uint32_t valid = (uint32_t)min((size_t)TILE, (size_t)a.n - base);
+        const uint32_t kbytes = (valid * (uint32_t)sizeof(K)) & ~15u;
+        const uint32_t vbytes = HAS_VAL ? ((valid * 4u) & ~15u) : 0u;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(s_bar, kbytes + vbytes);
+        if (kbytes) bulk_g2s(s_in, src + base, kbytes, s_bar);
+        if (HAS_VAL && vbytes) bulk_g2s(s_vin, vsrc + base, vbytes, s_bar);
+    };
+
+    if (tid == 0) {
+        mbar_init(s_bar, 1);
+        fence_mbar_init();
+        const uint32_t t0 = atomicAdd(&ctrl->tile_ctr[a.pass], 1u);
+        s_misc[0] = t0;
+        if (t0 < a.num_tiles) issue_load(t0);
+    }
+    for (int i = tid; i < W * R; i += THREADS) s_wc[i] = 0;
+    __syncthreads();
+    uint32_t tile = s_misc[0];
+    uint32_t phase = 0;
+    static_assert(KPT % 2 == 0 && WK <= 65536, "ranks are packed two per register");
+    K kr[KREG ? KPT : 2];  // this thread's keys of the tile (rows j, lane)
+    uint32_t rr[KPT / 2];  // their stable ranks within the warp's keys of the same digit, 16 bits each
+
+    while (tile < a.num_tiles) {
+        const size_t base = (size_t)tile * TILE;
+        const uint32_t valid = (uint32_t)min((size_t)TILE, (size_t)a.n - base);
+
+        // ---- [load] wait for the tile; ragged tail by scalar loads, all-ones padding
+        // (padding keys have digit 255 and come last, so they rank after every real key)
+        if (valid < (uint32_t)TILE) {
+            const uint32_t kdone = ((valid * (uint32_t)sizeof(K)) & ~15u) / sizeof(K);
+            for (uint32_t i = kdone + tid; i < (uint32_t)TILE; i += THREADS)
+                s_in[i] = i < valid ? src[base + i] : ~K(0);
+            if (HAS_VAL) {
+                const uint32_t vdone = ((valid * 4u) & ~15u) / 4;
+                for (uint32_t i = vdone + tid; i < (uint32_t)TILE; i += THREADS)
+                    s_vin[i] = i < valid ? vsrc[base + i] : 0u;
+            }
+        }
+        mbar_wait_parity(s_bar, phase);
+        phase ^= 1u;
+        __syncthreads();
+
+        // ---- [rank] one returning shared atomic per key: rank + per-warp histogram
+        {
+            const K* in = s_in + warp * WK + lane;
+            uint32_t* wc = s_wc + warp * R;
+#pragma unroll
+            for (int j = 0; j < KPT; j += 2) {
+                const K k0 = in[j * 32], k1 = in[(j + 1) * 32];
+                if (KREG) {
+                    kr[KREG ? j : 0] = k0;
+                    kr[KREG ? j + 1 : 1] = k1;
+                }
+                const uint32_t r0 = atomicAdd(&wc[digit8<K>(k0, shift)], 1u);
+                const uint32_t r1 = atomicAdd(&wc[digit8<K>(k1, shift)], 1u);
+                rr[j / 2] = __byte_perm(r0, r1, 0x5410);
+            }
+        }
+        __syncthreads();
+
+        // ---- [offset] thread d: tile count, in-tile offset, warp start offsets; publish
+        {
+            uint32_t c[W];
+            uint32_t tcnt = 0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                c[w] = s_wc[w * R + tid];
+                tcnt += c[w];
+            }
+            uint32_t incl = tcnt;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            if (lane == 31) s_misc[8 + warp] = incl;
+            const uint32_t pub = tcnt - (tid == R - 1 ? (uint32_t)TILE - valid : 0u);  // drop padding
+            s_tcnt[tid] = pub;
+            st_relaxed_gpu(status + (size_t)tile * R + tid, (tile == 0 ? ST::kFlagP : ST::kFlagA) | (S)pub);
+            __syncthreads();
+            uint32_t pre = 0;
+#pragma unroll
+            for (int w = 0; w < W; ++w) pre += w < warp ? s_misc[8 + w] : 0u;
+            uint32_t run = pre + incl - tcnt;  // in-tile offset of digit tid
+            s_texcl[tid] = run;
+#pragma unroll
+            for (int w = 0; w < W; ++w) {
+                s_wc[w * R + tid] = run;
+                run += c[w];
+            }
+        }
+        __syncthreads();
+
+        // ---- [scatter] each key to its stable slot of the tile sorted by digit
+        {
+            const uint32_t* wc = s_wc + warp * R;
+            const int ibase = warp * WK + lane;
+#pragma unroll
+            for (int j = 0; j < KPT; ++j) {
+                const K k = KREG ? kr[KREG ? j : 0] : s_in[ibase + j * 32];
+                const uint32_t pos = wc[digit8<K>(k, shift)] + ((rr[j / 2] >> (16 * (j & 1))) & 0xFFFFu);
+                RS_DCHECK(pos < (uint32_t)TILE);
+                s_out[pos] = k;
+                if (HAS_VAL) s_vout[pos] = s_vin[ibase + j * 32];
+            }
+        }
+
+        // ---- [look-back] one digit per thread, windowed walk over earlier tiles
+        {
+            S excl = 0;
+            if (tile != 0) {
+                constexpr int LB = 8;
+                const S* sp = status + (size_t)(tile - 1) * R + tid;
+                int64_t left = (int64_t)tile;
+                bool done = false;
+                while (!done) {
+                    S v[LB];
+#pragma unroll
+                    for (int i = 0; i < LB; ++i) v[i] = i < left ? ld_relaxed_gpu(sp - (size_t)i * R) : ST::kFlagP;
+#pragma unroll
+                    for (int i = 0; i < LB; ++i) {
+                        if (done) break;
+                        while ((v[i] & (ST::kFlagA | ST::kFlagP)) == 0) v[i] = ld_relaxed_gpu(sp - (size_t)i * R);
+                        excl += ST::val(v[i]);
+                        done = (v[i] & ST::kFlagP) != 0;
+                    }
+                    sp -= (size_t)LB * R;
+                    left -= LB;
+                }
+                st_relaxed_gpu(status + (size_t)tile * R + tid, ST::kFlagP | (excl + (S)s_tcnt[tid]));
+            }
+            s_gofs[tid] = a.bases[a.pass * R + tid] + (uint32_t)excl - s_texcl[tid];
+        }
+        __syncthreads();
+
+        // ---- [next] take the next tile and start its load; s_in and the counters are free
+        if (tid == 0) {
+            const uint32_t nt = atomicAdd(&ctrl->tile_ctr[a.pass], 1u);
+            s_misc[0] = nt;
+            if (nt < a.num_tiles) issue_load(nt);
+        }
+#pragma unroll
+        for (int w = 0; w < W; ++w) s_wc[w * R + tid] = 0;
+
+        // ---- [store] bucket runs leave as coalesced bursts
+#pragma unroll 4
+        for (uint32_t i = tid; i < valid; i += THREADS) {
+            const K k = s_out[i];
+            const uint32_t g = s_gofs[digit8<K>(k, shift)] + i;
+            RS_DCHECK(g < a.n);
+            dst[g] = k;
+            if (HAS_VAL) vdst[g] = s_vout[i];
+        }
+        __syncthreads();
+        tile = s_misc[0];
+    }
+}
+
+// Startup probe of the lane-order property design 5 relies on: every warp ranks
+// `rows` rows of digits with returning shared atomics and compares each result
+// with the stable rank computed from the definition (count of equal digits in
+// earlier rows + earlier lanes of the same row).  Mismatches are added to *bad.
+__global__ void __launch_bounds__(256) k_rank_probe(uint32_t seed, int rows, uint32_t* bad) {
+    __shared__ uint32_t cnt[8][256];
+    __shared__ uint32_t ref[8][256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) {
+        (&cnt[0][0])[i] = 0;
+        (&ref[0][0])[i] = 0;
+    }
+    __syncthreads();
+    // digit ranges 256, 16, 2, 1 (by block) so groups of every size occur
+    const uint32_t mask = 0xFFu >> (2 * (blockIdx.x & 3));
+    uint32_t miss = 0;
+    for (int j = 0; j < rows; ++j) {
+        uint32_t z = seed + (uint32_t)((blockIdx.x * 8 + warp) * rows + j) * 32u + lane;
+        z ^= z >> 16; z *= 0x7feb352du; z ^= z >> 15; z *= 0x846ca68bu; z ^= z >> 16;
+        const uint32_t d = (blockIdx.x & 3) == 3 ? 7u : (z & mask);
+        const uint32_t r = atomicAdd(&cnt[warp][d], 1u);
+        // definition: earlier rows (ref) + earlier lanes of this row with digit d
+        const uint32_t peers = __match_any_sync(0xffffffffu, d);
+        const uint32_t want = ref[warp][d] + __popc(peers & lanemask_lt());
+        miss += (r != want);
+        __syncwarp();
+        if ((peers & lanemask_gt()) == 0) ref[warp][d] += __popc(peers);
+        __syncwarp();
+    }
+    if (miss) atomicAdd(bad, miss);
+}
+
+}  // namespace rs

@@ -5,10 +5,13 @@
 // caller's stream; no host synchronisation, no allocation.
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <type_traits>
 
 #include "onesweep.cuh"
 #include "onesweep_ec.cuh"
+#include "onesweep_ar.cuh"
 #include "onesweep_cr.cuh"
 #include "onesweep_n4.cuh"
 #include "radix16.cuh"
@@ -119,11 +122,38 @@ struct TuneN4<uint64_t, true> : TuneT<256, 12, 2> {};
 template <>
 struct TuneN4<uint32_t, true> : TuneT<256, 12, 3> {};
 
+// atomic-rank design (5): same tile sizes as design 2 (the layout does not depend
+// on which of the two runs)
+template <typename K, bool V>
+struct TuneAr;
+#ifndef RS_AR_U32_MINB
+#define RS_AR_U32_MINB 3
+#endif
+#ifndef RS_AR_KREG
+#define RS_AR_KREG 0
+#endif
+template <>
+struct TuneAr<uint32_t, false> : TuneT<256, 24, RS_AR_U32_MINB> {};
+template <>
+struct TuneAr<uint64_t, false> : TuneT<256, 12, 3> {};
+template <>
+struct TuneAr<uint64_t, true> : TuneT<256, 12, 2> {};
+template <>
+struct TuneAr<uint32_t, true> : TuneT<256, 12, 3> {};
+static_assert(TuneAr<uint32_t, false>::THREADS * TuneAr<uint32_t, false>::KPT ==
+                  TuneEc<uint32_t, false>::THREADS * TuneEc<uint32_t, false>::KPT, "design 5 tile = design 2 tile");
+static_assert(TuneAr<uint64_t, false>::THREADS * TuneAr<uint64_t, false>::KPT ==
+                  TuneEc<uint64_t, false>::THREADS * TuneEc<uint64_t, false>::KPT, "design 5 tile = design 2 tile");
+static_assert(TuneAr<uint64_t, true>::THREADS * TuneAr<uint64_t, true>::KPT ==
+                  TuneEc<uint64_t, true>::THREADS * TuneEc<uint64_t, true>::KPT, "design 5 tile = design 2 tile");
+static_assert(TuneAr<uint32_t, true>::THREADS * TuneAr<uint32_t, true>::KPT ==
+                  TuneEc<uint32_t, true>::THREADS * TuneEc<uint32_t, true>::KPT, "design 5 tile = design 2 tile");
+
 template <typename K, bool V>
 static int tile_keys() {
     if (options().pass_design == 4) return TuneN4<K, V>::THREADS * TuneN4<K, V>::KPT;
     if (options().pass_design == 3) return TuneCr<K, V>::THREADS * TuneCr<K, V>::KPT;
-    if (options().pass_design >= 1) return TuneEc<K, V>::THREADS * TuneEc<K, V>::KPT;
+    if (options().pass_design >= 1) return TuneEc<K, V>::THREADS * TuneEc<K, V>::KPT;  // 1, 2, 5
     return Tune<K, V>::THREADS * Tune<K, V>::KPT;
 }
 
@@ -222,6 +252,73 @@ static rs_status_t launch_pass_ec_me(const PassArgs& a, size_t T, cudaStream_t s
 }
 
 template <typename K, bool V, typename S>
+static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st) {
+    using TN = TuneAr<K, V>;
+    using C = OnesweepArCfg<K, V, TN::THREADS, TN::KPT>;
+    auto kern = k_onesweep_ar<K, V, TN::THREADS, TN::KPT, TN::MINB, S, (RS_AR_KREG != 0)>;
+    static int grid_cap = 0;
+    if (!grid_cap) {
+        RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
+        int per_sm = 0;
+        RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, C::THREADS, C::smem_bytes));
+        grid_cap = std::max(1, per_sm) * sm_count();
+    }
+    const unsigned grid = (unsigned)std::min<size_t>(T, (size_t)grid_cap);  // persistent CTAs
+    LaunchScope ls("onesweep", st);
+    kern<<<grid, C::THREADS, C::smem_bytes, st>>>(a);
+    return RS_OK;
+}
+
+// ---------------------------------------------------- design-5 lane-order probe
+// Design 5 takes stable ranks from the old values returned by warp-wide shared
+// atomicAdd; it is used only on a device where k_rank_probe finds the returned
+// values in lane order for every same-address group (onesweep_ar.cuh).  Run
+// once per device, on the caller's stream, with one host synchronisation; the
+// counter word is in the (zeroed) control block.  Never run inside a stream
+// capture: there design 2 is used for that call.
+static std::mutex g_probe_mu;
+static std::map<int, int> g_probe;  // device -> 0 failed / 1 passed
+
+int rank_probe_state() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+    std::lock_guard<std::mutex> lk(g_probe_mu);
+    auto it = g_probe.find(dev);
+    return it == g_probe.end() ? -1 : it->second;
+}
+
+static rs_status_t rank_order_ok(Ctrl* ctrl, cudaStream_t st, bool* ok) {
+    int dev = 0;
+    RS_CUDA_TRY(cudaGetDevice(&dev));
+    {
+        std::lock_guard<std::mutex> lk(g_probe_mu);
+        auto it = g_probe.find(dev);
+        if (it != g_probe.end()) {
+            *ok = it->second == 1;
+            return RS_OK;
+        }
+    }
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    RS_CUDA_TRY(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone) {
+        *ok = false;
+        return RS_OK;
+    }
+    uint32_t* bad = reinterpret_cast<uint32_t*>(&ctrl->pad[0]);  // zeroed with the control block
+    {
+        LaunchScope ls("rank_probe", st);
+        k_rank_probe<<<sm_count() * 4, 256, 0, st>>>(0x9E3779B9u, 64, bad);
+    }
+    uint32_t h = 1;
+    RS_CUDA_TRY(cudaMemcpyAsync(&h, bad, sizeof(h), cudaMemcpyDeviceToHost, st));
+    RS_CUDA_TRY(cudaStreamSynchronize(st));
+    std::lock_guard<std::mutex> lk(g_probe_mu);
+    g_probe[dev] = h == 0 ? 1 : 0;
+    *ok = h == 0;
+    return RS_OK;
+}
+
+template <typename K, bool V, typename S>
 static rs_status_t launch_pass_cr(const PassArgs& a, size_t T, cudaStream_t st) {
     using TN = TuneCr<K, V>;
     using C = OnesweepCrCfg<K, V, TN::THREADS, TN::KPT>;
@@ -258,7 +355,11 @@ static rs_status_t launch_pass_n4(const PassArgs& a, size_t T, cudaStream_t st) 
 }
 
 template <typename K, bool V>
-static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStream_t st) {
+static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStream_t st, bool ar_ok) {
+    if (options().pass_design == 5 && ar_ok) {
+        if (wide) return launch_pass_ar<K, V, uint64_t>(a, T, st);
+        return launch_pass_ar<K, V, uint32_t>(a, T, st);
+    }
     if (options().pass_design == 4) {
         if (wide) return launch_pass_n4<K, V, uint64_t>(a, T, st);
         return launch_pass_n4<K, V, uint32_t>(a, T, st);
@@ -271,7 +372,7 @@ static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStrea
         if (wide) return launch_pass_ec<K, V, uint64_t, true, 0>(a, T, st);
         return launch_pass_ec<K, V, uint32_t, true, 0>(a, T, st);
     }
-    if (options().pass_design == 2) {
+    if (options().pass_design == 2 || options().pass_design == 5) {  // 5 without the probe -> 2
         if (wide) return launch_pass_ec_me<K, V, uint64_t, false>(a, T, st);
         return launch_pass_ec_me<K, V, uint32_t, false>(a, T, st);
     }
@@ -332,12 +433,17 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
     a.ctrl = L.ctrl;
     a.bases = L.bases;
     a.debug_skip = options().debug_skip;
+    bool ar_ok = false;
+    if (options().pass_design == 5 && P > 0) {
+        s = rank_order_ok(L.ctrl, st, &ar_ok);
+        if (s != RS_OK) return s;
+    }
     for (int t = 0; t < P; ++t) {
         a.pass = t;
         a.shift = 8 * t;
         a.status_cur = static_cast<char*>(L.status) + (size_t)(t & 1) * L.status_bytes;
         a.status_next = static_cast<char*>(L.status) + (size_t)((t + 1) & 1) * L.status_bytes;
-        s = launch_pass<K, V>(a, L.T, L.wide, st);
+        s = launch_pass<K, V>(a, L.T, L.wide, st, ar_ok);
         if (s != RS_OK) return s;
     }
     {

@@ -138,9 +138,25 @@ rs_status_t rs_set_option(const char* name, long long value) {
     else if (n == "compact" && value <= 1) options().compact = value != 0;
     else if (n == "match_every" && (value == 0 || value == 4 || value == 6 || value == 8))
         options().match_every = (int)value;
-    else if (n == "pass_design" && value <= 4) options().pass_design = (int)value;
+    else if (n == "pass_design" && value <= 5) options().pass_design = (int)value;
     else if (n == "rank_variant" && value <= 4) options().rank_variant = (int)value;
     else return fail(RS_EINVAL, "rs_set_option: unknown option or value: " + n);
+    return RS_OK;
+}
+
+rs_status_t rs_get_option(const char* name, long long* value) {
+    if (!name || !value) return fail(RS_EINVAL, "rs_get_option: null argument");
+    const std::string n(name);
+    const Options& o = options();
+    if (n == "wide_status") *value = o.wide_status;
+    else if (n == "debug_skip") *value = o.debug_skip;
+    else if (n == "gsd_merge") *value = o.gsd_merge;
+    else if (n == "compact") *value = o.compact;
+    else if (n == "match_every") *value = o.match_every;
+    else if (n == "pass_design") *value = o.pass_design;
+    else if (n == "rank_variant") *value = o.rank_variant;
+    else if (n == "rank_probe") *value = rank_probe_state();
+    else return fail(RS_EINVAL, "rs_get_option: unknown option: " + n);
     return RS_OK;
 }
 

@@ -2,6 +2,8 @@
 steps on this GPU, device copies in place of NCCL) against the CPU GSD
 simulator (oracle/gsd.c): splitters, the p×p count matrix
 and every Y_j bit-exact."""
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -82,14 +84,16 @@ def test_gsd_config4_shape_reduced():
 
 @pytest.fixture
 def option():
-    names = []
+    saved = {}
 
     def _set(name, value):
+        v = ctypes.c_longlong()
+        assert rs.lib().rs_get_option(name.encode(), ctypes.byref(v)) == 0
+        saved.setdefault(name, v.value)
         assert rs.lib().rs_set_option(name.encode(), value) == 0
-        names.append(name)
     yield _set
-    for name in names:
-        rs.lib().rs_set_option(name.encode(), 0)
+    for name, value in saved.items():
+        rs.lib().rs_set_option(name.encode(), value)
 
 
 @pytest.mark.parametrize("merge", [0, 1])

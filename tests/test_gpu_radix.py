@@ -2,6 +2,8 @@
 serial oracle: bit-exact after every pass, for every key type, digit width,
 size edge case and BASELINE distribution (configs 1-3 at full size; configs
 4-5 at p = 1 by invariants and sampled order statistics)."""
+import ctypes
+
 import numpy as np
 import pytest
 import torch
@@ -227,16 +229,33 @@ def test_narrow_pairs_stability_at_scale():
         assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
 
 
+def get_option(name):
+    v = ctypes.c_longlong()
+    assert rs.lib().rs_get_option(name.encode(), ctypes.byref(v)) == 0
+    return v.value
+
+
 @pytest.fixture
 def option():
-    set_ = []
+    saved = {}
 
     def _set(name, value):
+        saved.setdefault(name, get_option(name))
         assert rs.lib().rs_set_option(name.encode(), value) == 0
-        set_.append(name)
     yield _set
-    for name in set_:
-        rs.lib().rs_set_option(name.encode(), 0)
+    for name, value in saved.items():
+        rs.lib().rs_set_option(name.encode(), value)
+
+
+def test_atomic_rank_probe_passes():
+    """Design 5 (the default pass) ranks keys by the old values of warp-wide
+    shared atomicAdd; the library enables it only after its probe kernel found
+    those values in lane order for every same-address group on this device.
+    On a B200 the probe must pass, so the parity tests run design 5."""
+    a = inputs.gen_u32(3 * TILE32 + 11, 50)
+    assert (_sort_u32(a, 8) == oracle.sr(a, 8)).all()
+    assert get_option("pass_design") == 5
+    assert get_option("rank_probe") == 1
 
 
 @pytest.mark.parametrize("kind", ["u32", "u64", "pairs"])
@@ -269,6 +288,7 @@ def test_wide_status_lookback(option, kind):
 @pytest.mark.parametrize("variant", [1, 2, 3, 4])
 def test_rank_variants(option, variant):
     """match.any (1) and atomic-OR (2) peer masks give the same stable ranks."""
+    option("pass_design", 2)
     option("rank_variant", variant)
     a = inputs.gen_u32(5 * TILE32 + 3, 33)
     assert (_sort_u32(a, 8) == oracle.sr(a, 8)).all()
@@ -280,7 +300,7 @@ def test_rank_variants(option, variant):
     assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
 
 
-@pytest.mark.parametrize("design", [0, 1, 2, 3, 4])
+@pytest.mark.parametrize("design", [0, 1, 2, 3, 4, 5])
 @pytest.mark.parametrize("wide", [0, 1])
 def test_pass_designs(option, design, wide):
     """Every radix-256 pass kernel design (classic; early counts with a
@@ -307,6 +327,7 @@ def test_pass_designs(option, design, wide):
 @pytest.mark.parametrize("me", [4, 6, 8])
 def test_match_every_hybrid_ranking(option, me):
     """u32 pass with every me-th key ranked by match.any, the rest by ballots."""
+    option("pass_design", 2)
     option("match_every", me)
     a = inputs.gen_u32(7 * TILE32 + 999, 44)
     for t in range(1, 5):
@@ -316,6 +337,7 @@ def test_match_every_hybrid_ranking(option, me):
 
 def test_compact_layout(option):
     """design 2 with 16-bit per-warp counters (compact shared-memory layout)."""
+    option("pass_design", 2)
     option("compact", 1)
     a = inputs.gen_u32(9 * TILE32 + 77, 45)
     for t in range(1, 5):
