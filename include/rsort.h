@@ -196,9 +196,11 @@ rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits,
  *                    bit 1 no ranking, bit 2 no global store, bit 3 no reorder.
  * Returns RS_EINVAL for an unknown name or a negative value. */
 rs_status_t rs_set_option(const char* name, long long value);
-/* Current value of an rs_set_option knob, or the read-only "rank_probe": the
- * result of the design-5 lane-order probe on the current device (-1 not run
- * yet, 0 failed -> design 2 is used, 1 passed).  RS_EINVAL for unknown names. */
+/* Current value of an rs_set_option knob, or a read-only value: "rank_probe",
+ * the result of the design-5 lane-order probe on the current device (-1 not run
+ * yet, 0 failed -> design 2 is used, 1 passed); "tile_u32", "tile_u64",
+ * "tile_pairs", the radix-256 tile (keys per look-back row) of the selected
+ * pass design.  RS_EINVAL for unknown names. */
 rs_status_t rs_get_option(const char* name, long long* value);
 
 /* ---------------------------------------------------------------- timing -- */

@@ -31,6 +31,12 @@
 #pragma once
 #include "onesweep_ec.cuh"
 
+// timing ablations of design 5 (development builds only, OUTPUT INVALID):
+// 1 no look-back walk, 2 no global store, 4 no scatter
+#ifndef RS_AR_ABLATE
+#define RS_AR_ABLATE 0
+#endif
+
 namespace rs {
 
 template <typename K, bool HAS_VAL, int RT, int KPT>
@@ -59,7 +65,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
     using ST = Status<S>;
     using C = OnesweepArCfg<K, HAS_VAL, RT, KPT>;
     constexpr int R = C::R, W = C::W, WK = C::WK, TILE = C::TILE, THREADS = C::THREADS;
-    static_assert(RT == R, "one thread per digit in the offset and look-back phases");
+    static_assert(RT % R == 0, "threads 0..255: one per digit in the offset and look-back phases");
     extern __shared__ __align__(128) unsigned char smem[];
     K* s_in = reinterpret_cast<K*>(smem + C::in_off);
     K* s_out = reinterpret_cast<K*>(smem + C::out_off);
@@ -117,6 +123,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
     uint32_t tile = s_misc[0];
     uint32_t phase = 0;
     static_assert(KPT % 2 == 0 && WK <= 65536, "ranks are packed two per register");
+    constexpr int G = KPT % 8 == 0 ? 8 : (KPT % 6 == 0 ? 6 : (KPT % 4 == 0 ? 4 : 2));  // batch of keys
     K kr[KREG ? KPT : 2];  // this thread's keys of the tile (rows j, lane)
     uint32_t rr[KPT / 2];  // their stable ranks within the warp's keys of the same digit, 16 bits each
 
@@ -144,22 +151,28 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         {
             const K* in = s_in + warp * WK + lane;
             uint32_t* wc = s_wc + warp * R;
+            // groups of G keys: G loads, then G atomics, then the packing of
+            // their results, so G shared-memory round trips overlap (the compiler
+            // keeps shared loads and atomics in program order)
 #pragma unroll
-            for (int j = 0; j < KPT; j += 2) {
-                const K k0 = in[j * 32], k1 = in[(j + 1) * 32];
-                if (KREG) {
-                    kr[KREG ? j : 0] = k0;
-                    kr[KREG ? j + 1 : 1] = k1;
+            for (int g = 0; g < KPT; g += G) {
+                K kk[G];
+                uint32_t rg[G];
+#pragma unroll
+                for (int i = 0; i < G; ++i) kk[i] = in[(g + i) * 32];
+#pragma unroll
+                for (int i = 0; i < G; ++i) {
+                    if (KREG) kr[KREG ? g + i : 0] = kk[i];
+                    rg[i] = atomicAdd(&wc[digit8<K>(kk[i], shift)], 1u);
                 }
-                const uint32_t r0 = atomicAdd(&wc[digit8<K>(k0, shift)], 1u);
-                const uint32_t r1 = atomicAdd(&wc[digit8<K>(k1, shift)], 1u);
-                rr[j / 2] = __byte_perm(r0, r1, 0x5410);
+#pragma unroll
+                for (int i = 0; i < G; i += 2) rr[(g + i) / 2] = __byte_perm(rg[i], rg[i + 1], 0x5410);
             }
         }
         __syncthreads();
 
         // ---- [offset] thread d: tile count, in-tile offset, warp start offsets; publish
-        {
+        if (tid < R) {
             uint32_t c[W];
             uint32_t tcnt = 0;
 #pragma unroll
@@ -177,10 +190,10 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             const uint32_t pub = tcnt - (tid == R - 1 ? (uint32_t)TILE - valid : 0u);  // drop padding
             s_tcnt[tid] = pub;
             st_relaxed_gpu(status + (size_t)tile * R + tid, (tile == 0 ? ST::kFlagP : ST::kFlagA) | (S)pub);
-            __syncthreads();
+            named_barrier_sync(1, R);
             uint32_t pre = 0;
 #pragma unroll
-            for (int w = 0; w < W; ++w) pre += w < warp ? s_misc[8 + w] : 0u;
+            for (int w = 0; w < R / 32; ++w) pre += w < warp ? s_misc[8 + w] : 0u;
             uint32_t run = pre + incl - tcnt;  // in-tile offset of digit tid
             s_texcl[tid] = run;
 #pragma unroll
@@ -195,20 +208,34 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         {
             const uint32_t* wc = s_wc + warp * R;
             const int ibase = warp * WK + lane;
+            // groups of G keys: G key loads, G offset loads, then G stores
 #pragma unroll
-            for (int j = 0; j < KPT; ++j) {
-                const K k = KREG ? kr[KREG ? j : 0] : s_in[ibase + j * 32];
-                const uint32_t pos = wc[digit8<K>(k, shift)] + ((rr[j / 2] >> (16 * (j & 1))) & 0xFFFFu);
-                RS_DCHECK(pos < (uint32_t)TILE);
-                s_out[pos] = k;
-                if (HAS_VAL) s_vout[pos] = s_vin[ibase + j * 32];
+            for (int g = 0; g < ((RS_AR_ABLATE & 4) ? 0 : KPT); g += G) {
+                K kk[G];
+                uint32_t pos[G], vv[HAS_VAL ? G : 1];
+#pragma unroll
+                for (int i = 0; i < G; ++i) kk[i] = KREG ? kr[KREG ? g + i : 0] : s_in[ibase + (g + i) * 32];
+#pragma unroll
+                for (int i = 0; i < G; ++i) {
+                    const int j = g + i;
+                    pos[i] = wc[digit8<K>(kk[i], shift)] + ((rr[j / 2] >> (16 * (j & 1))) & 0xFFFFu);
+                    if (HAS_VAL) vv[HAS_VAL ? i : 0] = s_vin[ibase + j * 32];
+                }
+#pragma unroll
+                for (int i = 0; i < G; ++i) {
+                    RS_DCHECK(pos[i] < (uint32_t)TILE);
+                    s_out[pos[i]] = kk[i];
+                    if (HAS_VAL) s_vout[pos[i]] = vv[HAS_VAL ? i : 0];
+                }
             }
         }
 
         // ---- [look-back] one digit per thread, windowed walk over earlier tiles
-        {
+        if (tid < R) {
             S excl = 0;
-            if (tile != 0) {
+            if (tile != 0 && (RS_AR_ABLATE & 1)) {
+                st_relaxed_gpu(status + (size_t)tile * R + tid, ST::kFlagP | (S)s_tcnt[tid]);
+            } else if (tile != 0) {
                 constexpr int LB = 8;
                 const S* sp = status + (size_t)(tile - 1) * R + tid;
                 int64_t left = (int64_t)tile;
@@ -240,11 +267,12 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             if (nt < a.num_tiles) issue_load(nt);
         }
 #pragma unroll
-        for (int w = 0; w < W; ++w) s_wc[w * R + tid] = 0;
+        for (int i = 0; i < W * R / THREADS; ++i) s_wc[i * THREADS + tid] = 0;
 
         // ---- [store] bucket runs leave as coalesced bursts
 #pragma unroll 4
         for (uint32_t i = tid; i < valid; i += THREADS) {
+            if (RS_AR_ABLATE & 2) break;
             const K k = s_out[i];
             const uint32_t g = s_gofs[digit8<K>(k, shift)] + i;
             RS_DCHECK(g < a.n);

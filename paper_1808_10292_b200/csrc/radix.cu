@@ -122,44 +122,65 @@ struct TuneN4<uint64_t, true> : TuneT<256, 12, 2> {};
 template <>
 struct TuneN4<uint32_t, true> : TuneT<256, 12, 3> {};
 
-// atomic-rank design (5): same tile sizes as design 2 (the layout does not depend
-// on which of the two runs)
+// atomic-rank design (5): (threads, keys per thread, min CTAs per SM).  Large
+// tiles amortise the per-tile offsets and look-back (measured on B200, 2^27 and
+// 2^31 keys: u32 256x48 with 2 CTAs/SM beats 256x24x3, 256x30x3, 256x40x2,
+// 256x64x1, 256x96x1, 512x20x2, 512x24x1, 512x32x1; pairs 256x32x1 beats
+// 256x12x2, 256x16x2, 256x24x1; u64 keys 256x24x2 beats 256x12x3, 512x12x1)
 template <typename K, bool V>
 struct TuneAr;
 #ifndef RS_AR_U32_MINB
-#define RS_AR_U32_MINB 3
+#define RS_AR_U32_MINB 2
 #endif
 #ifndef RS_AR_KREG
-#define RS_AR_KREG 0
+#define RS_AR_KREG 2  // 0 never, 1 always, 2 with values (pairs: 2 CTAs/SM leave room)
+#endif
+#ifndef RS_AR_U32_KPT
+#define RS_AR_U32_KPT 48
+#endif
+#ifndef RS_AR_U32_T
+#define RS_AR_U32_T 256
 #endif
 template <>
-struct TuneAr<uint32_t, false> : TuneT<256, 24, RS_AR_U32_MINB> {};
+struct TuneAr<uint32_t, false> : TuneT<RS_AR_U32_T, RS_AR_U32_KPT, RS_AR_U32_MINB> {};
+#ifndef RS_AR_U64_T
+#define RS_AR_U64_T 256
+#define RS_AR_U64_KPT 24
+#define RS_AR_U64_MINB 2
+#endif
 template <>
-struct TuneAr<uint64_t, false> : TuneT<256, 12, 3> {};
+struct TuneAr<uint64_t, false> : TuneT<RS_AR_U64_T, RS_AR_U64_KPT, RS_AR_U64_MINB> {};
+#ifndef RS_AR_PAIRS_T
+#define RS_AR_PAIRS_T 256
+#define RS_AR_PAIRS_KPT 32
+#define RS_AR_PAIRS_MINB 1
+#endif
 template <>
-struct TuneAr<uint64_t, true> : TuneT<256, 12, 2> {};
+struct TuneAr<uint64_t, true> : TuneT<RS_AR_PAIRS_T, RS_AR_PAIRS_KPT, RS_AR_PAIRS_MINB> {};
 template <>
-struct TuneAr<uint32_t, true> : TuneT<256, 12, 3> {};
-static_assert(TuneAr<uint32_t, false>::THREADS * TuneAr<uint32_t, false>::KPT ==
-                  TuneEc<uint32_t, false>::THREADS * TuneEc<uint32_t, false>::KPT, "design 5 tile = design 2 tile");
-static_assert(TuneAr<uint64_t, false>::THREADS * TuneAr<uint64_t, false>::KPT ==
-                  TuneEc<uint64_t, false>::THREADS * TuneEc<uint64_t, false>::KPT, "design 5 tile = design 2 tile");
-static_assert(TuneAr<uint64_t, true>::THREADS * TuneAr<uint64_t, true>::KPT ==
-                  TuneEc<uint64_t, true>::THREADS * TuneEc<uint64_t, true>::KPT, "design 5 tile = design 2 tile");
-static_assert(TuneAr<uint32_t, true>::THREADS * TuneAr<uint32_t, true>::KPT ==
-                  TuneEc<uint32_t, true>::THREADS * TuneEc<uint32_t, true>::KPT, "design 5 tile = design 2 tile");
-
+struct TuneAr<uint32_t, true> : TuneT<256, 24, 2> {};
 template <typename K, bool V>
-static int tile_keys() {
-    if (options().pass_design == 4) return TuneN4<K, V>::THREADS * TuneN4<K, V>::KPT;
-    if (options().pass_design == 3) return TuneCr<K, V>::THREADS * TuneCr<K, V>::KPT;
-    if (options().pass_design >= 1) return TuneEc<K, V>::THREADS * TuneEc<K, V>::KPT;  // 1, 2, 5
+static int tile_keys(int design) {
+    if (design == 5) return TuneAr<K, V>::THREADS * TuneAr<K, V>::KPT;
+    if (design == 4) return TuneN4<K, V>::THREADS * TuneN4<K, V>::KPT;
+    if (design == 3) return TuneCr<K, V>::THREADS * TuneCr<K, V>::KPT;
+    if (design >= 1) return TuneEc<K, V>::THREADS * TuneEc<K, V>::KPT;  // 1, 2
     return Tune<K, V>::THREADS * Tune<K, V>::KPT;
 }
 
-static int tile_for(int key_bytes, bool has_val) {
-    if (key_bytes == 4) return has_val ? tile_keys<uint32_t, true>() : tile_keys<uint32_t, false>();
-    return has_val ? tile_keys<uint64_t, true>() : tile_keys<uint64_t, false>();
+static int tile_for(int key_bytes, bool has_val, int design) {
+    if (key_bytes == 4) return has_val ? tile_keys<uint32_t, true>(design) : tile_keys<uint32_t, false>(design);
+    return has_val ? tile_keys<uint64_t, true>(design) : tile_keys<uint64_t, false>(design);
+}
+
+int tile_keys_for(int key_bytes, bool has_val) { return tile_for(key_bytes, has_val, options().pass_design); }
+
+// the tile size the workspace is sized for: design 5 may fall back to design 2
+// after its probe, so size for the smaller of the two tiles (more status rows)
+static int ws_tile_for(int key_bytes, bool has_val) {
+    const int d = options().pass_design;
+    const int t = tile_for(key_bytes, has_val, d);
+    return d == 5 ? std::min(t, tile_for(key_bytes, has_val, 2)) : t;
 }
 
 struct Layout8 {
@@ -173,9 +194,9 @@ struct Layout8 {
     bool wide;
 };
 
-static Layout8 layout8(void* ws, int key_bytes, bool has_val, size_t n) {
+// `ctrl` is always the first carve (offset 0), whatever the tile size
+static Layout8 layout8(void* ws, int key_bytes, bool has_val, size_t n, size_t tile) {
     Layout8 L{};
-    const size_t tile = (size_t)tile_for(key_bytes, has_val);
     const int P = key_bytes * 8 / 8;
     L.T = std::max<size_t>(1, (n + tile - 1) / tile);
     L.wide = n > kNarrowStatusMaxN || options().wide_status;  // P values need > 31 bits
@@ -192,7 +213,7 @@ static Layout8 layout8(void* ws, int key_bytes, bool has_val, size_t n) {
 }
 
 size_t local_ws_bytes(int key_bytes, bool has_val, size_t n, int b) {
-    if (b == 8) return layout8(nullptr, key_bytes, has_val, n).bytes;
+    if (b == 8) return layout8(nullptr, key_bytes, has_val, n, (size_t)ws_tile_for(key_bytes, has_val)).bytes;
     return radix16_ws_bytes(key_bytes, has_val, n);
 }
 
@@ -255,7 +276,7 @@ template <typename K, bool V, typename S>
 static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st) {
     using TN = TuneAr<K, V>;
     using C = OnesweepArCfg<K, V, TN::THREADS, TN::KPT>;
-    auto kern = k_onesweep_ar<K, V, TN::THREADS, TN::KPT, TN::MINB, S, (RS_AR_KREG != 0)>;
+    auto kern = k_onesweep_ar<K, V, TN::THREADS, TN::KPT, TN::MINB, S, (RS_AR_KREG == 1 || (RS_AR_KREG == 2 && V))>;
     static int grid_cap = 0;
     if (!grid_cap) {
         RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
@@ -355,24 +376,24 @@ static rs_status_t launch_pass_n4(const PassArgs& a, size_t T, cudaStream_t st) 
 }
 
 template <typename K, bool V>
-static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStream_t st, bool ar_ok) {
-    if (options().pass_design == 5 && ar_ok) {
+static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStream_t st, int design) {
+    if (design == 5) {
         if (wide) return launch_pass_ar<K, V, uint64_t>(a, T, st);
         return launch_pass_ar<K, V, uint32_t>(a, T, st);
     }
-    if (options().pass_design == 4) {
+    if (design == 4) {
         if (wide) return launch_pass_n4<K, V, uint64_t>(a, T, st);
         return launch_pass_n4<K, V, uint32_t>(a, T, st);
     }
-    if (options().pass_design == 3) {
+    if (design == 3) {
         if (wide) return launch_pass_cr<K, V, uint64_t>(a, T, st);
         return launch_pass_cr<K, V, uint32_t>(a, T, st);
     }
-    if (options().pass_design == 1) {
+    if (design == 1) {
         if (wide) return launch_pass_ec<K, V, uint64_t, true, 0>(a, T, st);
         return launch_pass_ec<K, V, uint32_t, true, 0>(a, T, st);
     }
-    if (options().pass_design == 2 || options().pass_design == 5) {  // 5 without the probe -> 2
+    if (design == 2) {
         if (wide) return launch_pass_ec_me<K, V, uint64_t, false>(a, T, st);
         return launch_pass_ec_me<K, V, uint32_t, false>(a, T, st);
     }
@@ -408,9 +429,17 @@ static rs_status_t launch_hist(const K* keys, size_t n, int P, uint32_t* hist,
 template <typename K, bool V>
 static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, int end_bit, K* out,
                          uint32_t* vout, void* ws, cudaStream_t st) {
-    const Layout8 L = layout8(ws, sizeof(K), V, n);
     const int P = (end_bit + 7) / 8;
-    RS_CUDA_TRY(cudaMemsetAsync(L.ctrl, 0, sizeof(Ctrl), st));
+    Ctrl* ctrl = static_cast<Ctrl*>(ws);  // first carve of every layout
+    RS_CUDA_TRY(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), st));
+    int design = options().pass_design;
+    if (design == 5 && P > 0) {
+        bool ar_ok = false;
+        rs_status_t s = rank_order_ok(ctrl, st, &ar_ok);
+        if (s != RS_OK) return s;
+        if (!ar_ok) design = 2;
+    }
+    const Layout8 L = layout8(ws, sizeof(K), V, n, (size_t)tile_for(sizeof(K), V, design));
     RS_CUDA_TRY(cudaMemsetAsync(L.hist, 0, (size_t)P * 256 * 4, st));
     // K1 also zeroes the first pass's status region (as u32 words)
     rs_status_t s = launch_hist<K>(keys_in, n, P, L.hist, static_cast<uint32_t*>(L.status), L.status_bytes / 4, st);
@@ -433,17 +462,12 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
     a.ctrl = L.ctrl;
     a.bases = L.bases;
     a.debug_skip = options().debug_skip;
-    bool ar_ok = false;
-    if (options().pass_design == 5 && P > 0) {
-        s = rank_order_ok(L.ctrl, st, &ar_ok);
-        if (s != RS_OK) return s;
-    }
     for (int t = 0; t < P; ++t) {
         a.pass = t;
         a.shift = 8 * t;
         a.status_cur = static_cast<char*>(L.status) + (size_t)(t & 1) * L.status_bytes;
         a.status_next = static_cast<char*>(L.status) + (size_t)((t + 1) & 1) * L.status_bytes;
-        s = launch_pass<K, V>(a, L.T, L.wide, st, ar_ok);
+        s = launch_pass<K, V>(a, L.T, L.wide, st, design);
         if (s != RS_OK) return s;
     }
     {

@@ -156,6 +156,9 @@ rs_status_t rs_get_option(const char* name, long long* value) {
     else if (n == "pass_design") *value = o.pass_design;
     else if (n == "rank_variant") *value = o.rank_variant;
     else if (n == "rank_probe") *value = rank_probe_state();
+    else if (n == "tile_u32") *value = tile_keys_for(4, false);
+    else if (n == "tile_u64") *value = tile_keys_for(8, false);
+    else if (n == "tile_pairs") *value = tile_keys_for(8, true);
     else return fail(RS_EINVAL, "rs_get_option: unknown option: " + n);
     return RS_OK;
 }

@@ -50,6 +50,8 @@ struct Options {
 };
 // design 5 precondition (radix.cu): -1 not probed yet on this device, 0 failed, 1 passed
 int rank_probe_state();
+// radix-256 tile (keys) of the selected pass design (radix.cu)
+int tile_keys_for(int key_bytes, bool has_val);
 Options& options();
 
 inline size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }

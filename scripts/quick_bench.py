@@ -14,6 +14,7 @@ import paper_1808_10292_b200 as rs  # noqa: E402
 
 L = rs.lib()
 PEAK = 6545.6
+ONE_PASS = os.environ.get("RS_ONE_PASS") == "1"
 for _opt in ("rank_variant", "debug_skip", "wide_status", "pass_design", "match_every", "compact"):
     if os.environ.get("RS_" + _opt.upper()):
         L.rs_set_option(_opt.encode(), int(os.environ["RS_" + _opt.upper()]))
@@ -40,6 +41,8 @@ def run(log2n, kind="u32", b=8, dist="uniform", reps=5):
     work = torch.empty_like(src)
     vwork = torch.empty_like(vals0) if vb else None
     ws = torch.empty(rs.workspace_bytes(kb, vb, n, b), dtype=torch.uint8, device="cuda")
+    obuf = torch.empty_like(src) if ONE_PASS else None
+    ovbuf = torch.empty_like(vals0) if (ONE_PASS and vb) else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     times = []
     for i in range(reps + 2):
@@ -51,7 +54,10 @@ def run(log2n, kind="u32", b=8, dist="uniform", reps=5):
             L.rs_timing_reset()
             L.rs_timing_enable(1)
         e0.record()
-        if vb:
+        if ONE_PASS:  # pass 0 only (ablations: later passes would see corrupted digits)
+            rs.sort_bits(work, end_bit=b, digit_bits=b, vals=vwork if vb else None, out_keys=obuf,
+                         out_vals=ovbuf, ws=ws)
+        elif vb:
             rs.sort_pairs(work, vwork, digit_bits=b, ws=ws)
         else:
             rs.sort(work, digit_bits=b, ws=ws)

@@ -15,8 +15,18 @@ from tests.gpu_util import dev, free_dev_gb, free_host_gb, host
 
 pytestmark = pytest.mark.gpu
 
-TILE32 = 256 * 24   # u32 keys-only tile (radix.cu TuneEc; classic Tune is 512 * 12, same size)
-TILE64 = 256 * 12   # u64 keys / pairs tile (TuneEc)
+
+
+def _tile(kind):
+    v = ctypes.c_longlong()
+    assert rs.lib().rs_get_option(f"tile_{kind}".encode(), ctypes.byref(v)) == 0
+    return v.value
+
+
+# tiles (keys per look-back row) of the default pass design, for ragged sizes
+TILE32 = _tile("u32")     # u32 keys
+TILE64 = _tile("u64")     # u64 keys
+TILEP = _tile("pairs")    # (u64, u32) pairs
 
 
 def _sort_u32(a, b, inplace=True):
@@ -72,8 +82,8 @@ def test_every_pass_u64_and_pairs(b):
         assert (host(gk, np.uint64) == wk).all() and (host(gv, np.uint32) == wv).all(), f"pairs pass {t}"
 
 
-EDGE_N = [1, 2, 3, 31, 32, 33, 1000, TILE64 - 1, TILE64, TILE64 + 1, TILE32 - 1, TILE32, TILE32 + 1,
-          2 * TILE32 + 3, 7 * TILE32 + 4095]
+EDGE_N = sorted({1, 2, 3, 31, 32, 33, 1000, TILE64 - 1, TILE64, TILE64 + 1, TILEP - 1, TILEP, TILEP + 1,
+                 TILE32 - 1, TILE32, TILE32 + 1, 2 * TILE32 + 3, 7 * TILE32 + 4095})
 
 
 @pytest.mark.parametrize("b", [8, 16])
