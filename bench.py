@@ -353,7 +353,14 @@ def main():
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(f"{args.config}:p{p}")
-    roofline = {"kernel": "k_onesweep_ec (one radix-256 count-sort pass)", "bound": "hbm",
+    design, probe = ctypes.c_longlong(), ctypes.c_longlong()
+    L.rs_get_option(b"pass_design", ctypes.byref(design))
+    L.rs_get_option(b"rank_probe", ctypes.byref(probe))
+    kname = ("k_onesweep_ar (design 5: atomic ranks)" if design.value == 5 and probe.value == 1
+             else f"k_onesweep_* (design {design.value if design.value != 5 else 2})")
+    if b == 16:
+        kname = "k16_* (radix-65536 passes)"
+    roofline = {"kernel": kname + ", one count-sort pass", "bound": "hbm",
                 "achieved": round(achieved, 1) if achieved else None, "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4) if achieved else None, "traffic": traffic,
                 "algorithmic_bytes_per_launch": bpk * n_local, "launch_ms": round(pass_ms, 4),
