@@ -192,6 +192,8 @@ rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits,
  *                    1 = stable radix re-sort of the received runs (same result).
  *   "compact"        1 = default pass with 16-bit per-warp counters (smaller
  *                    shared-memory footprint; ballots only).
+ *   "hist_shared"    1 = digit-histogram kernel with one shared histogram per
+ *                    4 warps (0, default: lane-private copies, conflict-free).
  *   "debug_skip"     timing ablations, OUTPUT INVALID: bit 0 no look-back,
  *                    bit 1 no ranking, bit 2 no global store, bit 3 no reorder.
  * Returns RS_EINVAL for an unknown name or a negative value. */

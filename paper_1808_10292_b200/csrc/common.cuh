@@ -92,6 +92,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// prefetch `bytes` (multiple of 16) at 16-byte aligned `src` into L2 through the TMA engine
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // lanes of this warp whose 8-bit digit d equals mine, from 8 ballots
 __device__ __forceinline__ uint32_t peers8(uint32_t d) {
     // Lanes that disagree with me on bit b are the set bits of ballot(bit b) ^ s_b,

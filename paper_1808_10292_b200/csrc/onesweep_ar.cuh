@@ -39,7 +39,7 @@
 
 namespace rs {
 
-template <typename K, bool HAS_VAL, int RT, int KPT>
+template <typename K, bool HAS_VAL, int RT, int KPT, int KSRC = 0>
 struct OnesweepArCfg {
     static constexpr int R = 256;
     static constexpr int W = RT / 32;
@@ -47,7 +47,7 @@ struct OnesweepArCfg {
     static constexpr int WK = 32 * KPT;
     static constexpr int TILE = RT * KPT;
     static constexpr size_t in_off = 0;
-    static constexpr size_t out_off = in_off + (size_t)TILE * sizeof(K);
+    static constexpr size_t out_off = in_off + (KSRC != 0 ? 0 : (size_t)TILE * sizeof(K));
     static constexpr size_t vin_off = out_off + (size_t)TILE * sizeof(K);
     static constexpr size_t vout_off = vin_off + (HAS_VAL ? (size_t)TILE * 4 : 0);
     static constexpr size_t wc_off = vout_off + (HAS_VAL ? (size_t)TILE * 4 : 0);
@@ -59,11 +59,21 @@ struct OnesweepArCfg {
     static constexpr size_t smem_bytes = bar_off + 16;
 };
 
-// KREG: keep the keys in registers from [rank] to [scatter] (else re-read s_in)
-template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, bool KREG>
+// KREG: keep the keys in registers from [rank] to [scatter] (else re-read s_in).
+// KSRC (where the ranking warps get their keys; 1 and 2 keys-only):
+//   0  TMA bulk copy of the tile into shared memory (s_in)
+//   1  each thread loads its keys from global memory into registers and keeps
+//      them until the scatter (coalesced rows; the next tile is prefetched into
+//      L2 by the TMA engine): no s_in, no shared-memory write/read of the input
+//   2  as 1, but the keys are not kept: the scatter loads them again (from L2),
+//      which frees the registers for larger tiles
+template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, bool KREG_, int KSRC = 0>
 __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
+    static_assert(KSRC == 0 || !HAS_VAL, "register/global tiles are for keys-only sorts");
+    constexpr bool LDGK = KSRC != 0;
+    constexpr bool KREG = (KREG_ && KSRC != 2) || KSRC == 1;
     using ST = Status<S>;
-    using C = OnesweepArCfg<K, HAS_VAL, RT, KPT>;
+    using C = OnesweepArCfg<K, HAS_VAL, RT, KPT, KSRC>;
     constexpr int R = C::R, W = C::W, WK = C::WK, TILE = C::TILE, THREADS = C::THREADS;
     static_assert(RT % R == 0, "threads 0..255: one per digit in the offset and look-back phases");
     extern __shared__ __align__(128) unsigned char smem[];
@@ -104,6 +114,10 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         const size_t base = (size_t)t * TILE;
         const uint32_t valid = (uint32_t)min((size_t)TILE, (size_t)a.n - base);
         const uint32_t kbytes = (valid * (uint32_t)sizeof(K)) & ~15u;
+        if (LDGK) {  // L2 prefetch only; the threads load their keys themselves
+            if (kbytes) bulk_prefetch_l2(src + base, kbytes);
+            return;
+        }
         const uint32_t vbytes = HAS_VAL ? ((valid * 4u) & ~15u) : 0u;
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(s_bar, kbytes + vbytes);
@@ -112,8 +126,10 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
     };
 
     if (tid == 0) {
-        mbar_init(s_bar, 1);
-        fence_mbar_init();
+        if (!LDGK) {
+            mbar_init(s_bar, 1);
+            fence_mbar_init();
+        }
         const uint32_t t0 = atomicAdd(&ctrl->tile_ctr[a.pass], 1u);
         s_misc[0] = t0;
         if (t0 < a.num_tiles) issue_load(t0);
@@ -133,7 +149,18 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
 
         // ---- [load] wait for the tile; ragged tail by scalar loads, all-ones padding
         // (padding keys have digit 255 and come last, so they rank after every real key)
-        if (valid < (uint32_t)TILE) {
+        const K* gk = src + base + warp * WK + lane;  // this thread's row-0 key (KSRC 1, 2)
+        const uint32_t lim = valid - min(valid, (uint32_t)(warp * WK + lane));  // rows j*32 < lim are real
+        if (KSRC == 1) {
+            const K* g = gk;
+            if (valid == (uint32_t)TILE) {
+#pragma unroll
+                for (int j = 0; j < KPT; ++j) kr[KREG ? j : 0] = __ldcs(g + j * 32);
+            } else {
+#pragma unroll
+                for (int j = 0; j < KPT; ++j) kr[KREG ? j : 0] = (uint32_t)(j * 32) < lim ? g[j * 32] : ~K(0);
+            }
+        } else if (valid < (uint32_t)TILE) {
             const uint32_t kdone = ((valid * (uint32_t)sizeof(K)) & ~15u) / sizeof(K);
             for (uint32_t i = kdone + tid; i < (uint32_t)TILE; i += THREADS)
                 s_in[i] = i < valid ? src[base + i] : ~K(0);
@@ -143,9 +170,11 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                     s_vin[i] = i < valid ? vsrc[base + i] : 0u;
             }
         }
-        mbar_wait_parity(s_bar, phase);
-        phase ^= 1u;
-        __syncthreads();
+        if (!LDGK) {
+            mbar_wait_parity(s_bar, phase);
+            phase ^= 1u;
+            __syncthreads();
+        }
 
         // ---- [rank] one returning shared atomic per key: rank + per-warp histogram
         {
@@ -159,10 +188,13 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                 K kk[G];
                 uint32_t rg[G];
 #pragma unroll
-                for (int i = 0; i < G; ++i) kk[i] = in[(g + i) * 32];
+                for (int i = 0; i < G; ++i)
+                    kk[i] = KSRC == 1   ? kr[KREG ? g + i : 0]
+                            : KSRC == 2 ? ((uint32_t)((g + i) * 32) < lim ? gk[(g + i) * 32] : ~K(0))
+                                        : in[(g + i) * 32];
 #pragma unroll
                 for (int i = 0; i < G; ++i) {
-                    if (KREG) kr[KREG ? g + i : 0] = kk[i];
+                    if (KREG && KSRC == 0) kr[KREG ? g + i : 0] = kk[i];
                     rg[i] = atomicAdd(&wc[digit8<K>(kk[i], shift)], 1u);
                 }
 #pragma unroll
@@ -214,7 +246,10 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                 K kk[G];
                 uint32_t pos[G], vv[HAS_VAL ? G : 1];
 #pragma unroll
-                for (int i = 0; i < G; ++i) kk[i] = KREG ? kr[KREG ? g + i : 0] : s_in[ibase + (g + i) * 32];
+                for (int i = 0; i < G; ++i)
+                    kk[i] = KREG        ? kr[KREG ? g + i : 0]
+                            : KSRC == 2 ? ((uint32_t)((g + i) * 32) < lim ? __ldcs(gk + (g + i) * 32) : ~K(0))
+                                        : s_in[ibase + (g + i) * 32];
 #pragma unroll
                 for (int i = 0; i < G; ++i) {
                     const int j = g + i;

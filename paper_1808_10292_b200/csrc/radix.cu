@@ -132,6 +132,15 @@ struct TuneAr;
 #ifndef RS_AR_U32_MINB
 #define RS_AR_U32_MINB 2
 #endif
+// where keys-only passes take their keys (onesweep_ar.cuh KSRC): 0 TMA tile in
+// shared memory, 1 registers, 2 global memory twice.  Measured per 2^27 pass:
+// u64 KSRC 0 -> 1 0.576 -> 0.533 ms; u32 at 256x48 KSRC 1 no gain (register-bound)
+#ifndef RS_AR_KSRC_U32
+#define RS_AR_KSRC_U32 0
+#endif
+#ifndef RS_AR_KSRC_U64
+#define RS_AR_KSRC_U64 1
+#endif
 #ifndef RS_AR_KREG
 #define RS_AR_KREG 2  // 0 never, 1 always, 2 with values (pairs: 2 CTAs/SM leave room)
 #endif
@@ -275,8 +284,9 @@ static rs_status_t launch_pass_ec_me(const PassArgs& a, size_t T, cudaStream_t s
 template <typename K, bool V, typename S>
 static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st) {
     using TN = TuneAr<K, V>;
-    using C = OnesweepArCfg<K, V, TN::THREADS, TN::KPT>;
-    auto kern = k_onesweep_ar<K, V, TN::THREADS, TN::KPT, TN::MINB, S, (RS_AR_KREG == 1 || (RS_AR_KREG == 2 && V))>;
+    constexpr int KSRC = V ? 0 : (sizeof(K) == 8 ? RS_AR_KSRC_U64 : RS_AR_KSRC_U32);
+    using C = OnesweepArCfg<K, V, TN::THREADS, TN::KPT, KSRC>;
+    auto kern = k_onesweep_ar<K, V, TN::THREADS, TN::KPT, TN::MINB, S, (RS_AR_KREG == 1 || (RS_AR_KREG == 2 && V)), KSRC>;
     static int grid_cap = 0;
     if (!grid_cap) {
         RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
@@ -411,6 +421,32 @@ static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStrea
 template <typename K>
 static rs_status_t launch_hist(const K* keys, size_t n, int P, uint32_t* hist,
                                uint32_t* zero_ptr, size_t zero_words, cudaStream_t st) {
+    if (!options().hist_shared) {
+        // lane-private copies (default): C = 32 for <= 4 passes, 16 for <= 8
+        constexpr int T = 1024;
+        if (P <= 4) {
+            auto kern = k_digit_hist_lp<K, T, 32>;
+            const size_t smem = (size_t)4 * 256 * 32 * 4;
+            static bool attr = false;
+            if (!attr) {
+                RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                attr = true;
+            }
+            LaunchScope ls("hist", st);
+            kern<<<sm_count(), T, (size_t)P * 256 * 32 * 4, st>>>(keys, n, P, hist, zero_ptr, zero_words);
+            return RS_OK;
+        }
+        auto kern = k_digit_hist_lp<K, T, 16>;
+        const size_t smem = (size_t)8 * 256 * 16 * 4;
+        static bool attr = false;
+        if (!attr) {
+            RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+        }
+        LaunchScope ls("hist", st);
+        kern<<<sm_count(), T, (size_t)P * 256 * 16 * 4, st>>>(keys, n, P, hist, zero_ptr, zero_words);
+        return RS_OK;
+    }
     constexpr int COPIES = kHistThreads / 128;
     const size_t smem = (size_t)COPIES * P * 256 * 4;
     auto kern = k_digit_hist<K, kHistThreads>;

@@ -99,6 +99,60 @@ __global__ void __launch_bounds__(THREADS) k_digit_hist(const K* __restrict__ ke
     }
 }
 
+// K1, lane-private layout (default): the CTA keeps C copies of every pass's
+// histogram and lane l adds to copy l % C, with copy c of digit d at word
+// d*C + c, so the 32 lanes of an atomic touch 32/C words per bank at most:
+// C = 32 (u32 keys, 4 passes: 128 KB) makes every warp-wide atomic a single
+// conflict-free shared-memory wavefront (random digits in one 256-word array
+// cost ~3.15 wavefronts); C = 16 (u64 keys, 8 passes: 128 KB) ~2.  One CTA of
+// 1024 threads per SM, persistent; each thread loads 16-byte vectors.
+template <typename K, int THREADS, int C>
+__global__ void __launch_bounds__(THREADS, 1) k_digit_hist_lp(const K* __restrict__ keys, size_t n, int P,
+                                                             uint32_t* __restrict__ hist,
+                                                             uint32_t* __restrict__ zero_ptr, size_t zero_words) {
+    extern __shared__ __align__(16) uint32_t s_h[];  // [P][256][C]
+    const int tid = threadIdx.x, lane = tid & 31;
+    const size_t gtid = (size_t)blockIdx.x * THREADS + tid;
+    const size_t gstride = (size_t)gridDim.x * THREADS;
+    for (size_t i = gtid; i < zero_words; i += gstride) zero_ptr[i] = 0;
+    for (int i = tid; i < P * 256 * C; i += THREADS) s_h[i] = 0;
+    __syncthreads();
+    uint32_t* my = s_h + (lane % C);
+    constexpr int VEC = 16 / sizeof(K);
+    const size_t nvec = n / VEC;
+    const uint4* vbase = reinterpret_cast<const uint4*>(keys);
+    auto count = [&](K k) {
+        for (int t = 0; t < P; ++t)
+            atomicAdd(&my[(t * 256 + (uint32_t)((k >> (8 * t)) & 0xFFu)) * C], 1u);
+    };
+    size_t v = gtid;
+    for (; v + 3 * gstride < nvec; v += 4 * gstride) {  // four 16-byte loads in flight
+        uint4 x[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = __ldg(vbase + v + u * gstride);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const K* ks = reinterpret_cast<const K*>(&x[u]);
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) count(ks[e]);
+        }
+    }
+    for (; v < nvec; v += gstride) {
+        uint4 x = __ldg(vbase + v);
+        const K* ks = reinterpret_cast<const K*>(&x);
+#pragma unroll
+        for (int e = 0; e < VEC; ++e) count(ks[e]);
+    }
+    for (size_t i = nvec * VEC + gtid; i < n; i += gstride) count(keys[i]);
+    __syncthreads();
+    for (int i = tid; i < P * 256; i += THREADS) {
+        uint32_t s = 0;
+#pragma unroll
+        for (int c = 0; c < C; ++c) s += s_h[i * C + ((c + i) % C)];  // rotated: conflict-free
+        if (s) atomicAdd(&hist[i], s);
+    }
+}
+
 // ------------------------------------------------------------------ K2 ----
 // One CTA of 256 threads.  bases[t][d] = Σ_{d'<d} hist[t][d'].
 // Pass t is trivial (skipped: it would be the identity permutation) iff one

@@ -136,6 +136,7 @@ rs_status_t rs_set_option(const char* name, long long value) {
     else if (n == "debug_skip" && value <= 31) options().debug_skip = (unsigned)value;
     else if (n == "gsd_merge" && value <= 1) options().gsd_merge = (int)value;
     else if (n == "compact" && value <= 1) options().compact = value != 0;
+    else if (n == "hist_shared" && value <= 1) options().hist_shared = value != 0;
     else if (n == "match_every" && (value == 0 || value == 4 || value == 6 || value == 8))
         options().match_every = (int)value;
     else if (n == "pass_design" && value <= 5) options().pass_design = (int)value;
@@ -152,6 +153,7 @@ rs_status_t rs_get_option(const char* name, long long* value) {
     else if (n == "debug_skip") *value = o.debug_skip;
     else if (n == "gsd_merge") *value = o.gsd_merge;
     else if (n == "compact") *value = o.compact;
+    else if (n == "hist_shared") *value = o.hist_shared;
     else if (n == "match_every") *value = o.match_every;
     else if (n == "pass_design") *value = o.pass_design;
     else if (n == "rank_variant") *value = o.rank_variant;
