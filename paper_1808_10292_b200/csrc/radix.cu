@@ -418,34 +418,38 @@ static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStrea
     return launch_pass_v<K, V, 0, uint32_t>(a, T, st);
 }
 
+template <typename K, int C, int P>
+static rs_status_t launch_hist_lp(const K* keys, size_t n, uint32_t* hist, uint32_t* zero_ptr, size_t zero_words,
+                                  cudaStream_t st) {
+    constexpr int T = 1024;
+    constexpr size_t smem = (size_t)P * 256 * C * 4;
+    auto kern = k_digit_hist_lp<K, T, C, P>;
+    static bool attr = false;
+    if (!attr) {
+        RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    LaunchScope ls("hist", st);
+    kern<<<sm_count(), T, smem, st>>>(keys, n, hist, zero_ptr, zero_words);
+    return RS_OK;
+}
+
 template <typename K>
 static rs_status_t launch_hist(const K* keys, size_t n, int P, uint32_t* hist,
                                uint32_t* zero_ptr, size_t zero_words, cudaStream_t st) {
     if (!options().hist_shared) {
         // lane-private copies (default): C = 32 for <= 4 passes, 16 for <= 8
-        constexpr int T = 1024;
-        if (P <= 4) {
-            auto kern = k_digit_hist_lp<K, T, 32>;
-            const size_t smem = (size_t)4 * 256 * 32 * 4;
-            static bool attr = false;
-            if (!attr) {
-                RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                attr = true;
-            }
-            LaunchScope ls("hist", st);
-            kern<<<sm_count(), T, (size_t)P * 256 * 32 * 4, st>>>(keys, n, P, hist, zero_ptr, zero_words);
-            return RS_OK;
+        switch (P) {
+            case 1: return launch_hist_lp<K, 32, 1>(keys, n, hist, zero_ptr, zero_words, st);
+            case 2: return launch_hist_lp<K, 32, 2>(keys, n, hist, zero_ptr, zero_words, st);
+            case 3: return launch_hist_lp<K, 32, 3>(keys, n, hist, zero_ptr, zero_words, st);
+            case 4: return launch_hist_lp<K, 32, 4>(keys, n, hist, zero_ptr, zero_words, st);
+            case 5: return launch_hist_lp<K, 16, 5>(keys, n, hist, zero_ptr, zero_words, st);
+            case 6: return launch_hist_lp<K, 16, 6>(keys, n, hist, zero_ptr, zero_words, st);
+            case 7: return launch_hist_lp<K, 16, 7>(keys, n, hist, zero_ptr, zero_words, st);
+            case 8: return launch_hist_lp<K, 16, 8>(keys, n, hist, zero_ptr, zero_words, st);
+            default: return fail(RS_EINVAL, "digit histogram: bad pass count");
         }
-        auto kern = k_digit_hist_lp<K, T, 16>;
-        const size_t smem = (size_t)8 * 256 * 16 * 4;
-        static bool attr = false;
-        if (!attr) {
-            RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
-        }
-        LaunchScope ls("hist", st);
-        kern<<<sm_count(), T, (size_t)P * 256 * 16 * 4, st>>>(keys, n, P, hist, zero_ptr, zero_words);
-        return RS_OK;
     }
     constexpr int COPIES = kHistThreads / 128;
     const size_t smem = (size_t)COPIES * P * 256 * 4;

@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(THREADS) k_digit_hist(const K* __restrict__ ke
 // conflict-free shared-memory wavefront (random digits in one 256-word array
 // cost ~3.15 wavefronts); C = 16 (u64 keys, 8 passes: 128 KB) ~2.  One CTA of
 // 1024 threads per SM, persistent; each thread loads 16-byte vectors.
-template <typename K, int THREADS, int C>
-__global__ void __launch_bounds__(THREADS, 1) k_digit_hist_lp(const K* __restrict__ keys, size_t n, int P,
+template <typename K, int THREADS, int C, int P>
+__global__ void __launch_bounds__(THREADS, 1) k_digit_hist_lp(const K* __restrict__ keys, size_t n,
                                                              uint32_t* __restrict__ hist,
                                                              uint32_t* __restrict__ zero_ptr, size_t zero_words) {
     extern __shared__ __align__(16) uint32_t s_h[];  // [P][256][C]
@@ -122,8 +122,8 @@ __global__ void __launch_bounds__(THREADS, 1) k_digit_hist_lp(const K* __restric
     const size_t nvec = n / VEC;
     const uint4* vbase = reinterpret_cast<const uint4*>(keys);
     auto count = [&](K k) {
-        for (int t = 0; t < P; ++t)
-            atomicAdd(&my[(t * 256 + (uint32_t)((k >> (8 * t)) & 0xFFu)) * C], 1u);
+#pragma unroll
+        for (int t = 0; t < P; ++t) atomicAdd(&my[(t * 256 + digit_of<K>(k, 8 * t, 0xFFu)) * C], 1u);
     };
     size_t v = gtid;
     for (; v + 3 * gstride < nvec; v += 4 * gstride) {  // four 16-byte loads in flight
