@@ -36,6 +36,11 @@
 #ifndef RS_AR_ABLATE
 #define RS_AR_ABLATE 0
 #endif
+// per-warp digit counters as 16-bit halves of shared words (digits 2w, 2w+1
+// share word w): 128 words per warp instead of 256, so fewer bank conflicts
+#ifndef RS_AR_CT16
+#define RS_AR_CT16 1
+#endif
 
 namespace rs {
 
@@ -51,7 +56,7 @@ struct OnesweepArCfg {
     static constexpr size_t vin_off = out_off + (size_t)TILE * sizeof(K);
     static constexpr size_t vout_off = vin_off + (HAS_VAL ? (size_t)TILE * 4 : 0);
     static constexpr size_t wc_off = vout_off + (HAS_VAL ? (size_t)TILE * 4 : 0);
-    static constexpr size_t texcl_off = wc_off + (size_t)W * R * 4;
+    static constexpr size_t texcl_off = wc_off + (size_t)W * R * (RS_AR_CT16 ? 2 : 4);
     static constexpr size_t tcnt_off = texcl_off + R * 4;
     static constexpr size_t gofs_off = tcnt_off + R * 4;
     static constexpr size_t misc_off = gofs_off + R * 4;
@@ -134,7 +139,9 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         s_misc[0] = t0;
         if (t0 < a.num_tiles) issue_load(t0);
     }
-    for (int i = tid; i < W * R; i += THREADS) s_wc[i] = 0;
+    constexpr int WCW = W * R / (RS_AR_CT16 ? 2 : 1);  // counter words
+    uint16_t* s_wc16 = reinterpret_cast<uint16_t*>(smem + C::wc_off);
+    for (int i = tid; i < WCW; i += THREADS) s_wc[i] = 0;
     __syncthreads();
     uint32_t tile = s_misc[0];
     uint32_t phase = 0;
@@ -179,7 +186,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         // ---- [rank] one returning shared atomic per key: rank + per-warp histogram
         {
             const K* in = s_in + warp * WK + lane;
-            uint32_t* wc = s_wc + warp * R;
+            uint32_t* wc = s_wc + warp * (WCW / W);
             // groups of G keys: G loads, then G atomics, then the packing of
             // their results, so G shared-memory round trips overlap (the compiler
             // keeps shared loads and atomics in program order)
@@ -195,7 +202,13 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
 #pragma unroll
                 for (int i = 0; i < G; ++i) {
                     if (KREG && KSRC == 0) kr[KREG ? g + i : 0] = kk[i];
-                    rg[i] = atomicAdd(&wc[digit8<K>(kk[i], shift)], 1u);
+                    const uint32_t d = digit8<K>(kk[i], shift);
+                    if (RS_AR_CT16) {
+                        const uint32_t sh = (d & 1u) << 4;
+                        rg[i] = atomicAdd(&wc[d >> 1], 1u << sh) >> sh;  // high bits cleared at packing
+                    } else {
+                        rg[i] = atomicAdd(&wc[d], 1u);
+                    }
                 }
 #pragma unroll
                 for (int i = 0; i < G; i += 2) rr[(g + i) / 2] = __byte_perm(rg[i], rg[i + 1], 0x5410);
@@ -209,7 +222,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             uint32_t tcnt = 0;
 #pragma unroll
             for (int w = 0; w < W; ++w) {
-                c[w] = s_wc[w * R + tid];
+                c[w] = RS_AR_CT16 ? (uint32_t)s_wc16[w * R + tid] : s_wc[w * R + tid];
                 tcnt += c[w];
             }
             uint32_t incl = tcnt;
@@ -230,7 +243,8 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             s_texcl[tid] = run;
 #pragma unroll
             for (int w = 0; w < W; ++w) {
-                s_wc[w * R + tid] = run;
+                if (RS_AR_CT16) s_wc16[w * R + tid] = (uint16_t)run;
+                else s_wc[w * R + tid] = run;
                 run += c[w];
             }
         }
@@ -239,6 +253,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         // ---- [scatter] each key to its stable slot of the tile sorted by digit
         {
             const uint32_t* wc = s_wc + warp * R;
+            const uint16_t* wc16 = s_wc16 + warp * R;
             const int ibase = warp * WK + lane;
             // groups of G keys: G key loads, G offset loads, then G stores
 #pragma unroll
@@ -253,7 +268,8 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
 #pragma unroll
                 for (int i = 0; i < G; ++i) {
                     const int j = g + i;
-                    pos[i] = wc[digit8<K>(kk[i], shift)] + ((rr[j / 2] >> (16 * (j & 1))) & 0xFFFFu);
+                    const uint32_t d = digit8<K>(kk[i], shift);
+                    pos[i] = (RS_AR_CT16 ? (uint32_t)wc16[d] : wc[d]) + ((rr[j / 2] >> (16 * (j & 1))) & 0xFFFFu);
                     if (HAS_VAL) vv[HAS_VAL ? i : 0] = s_vin[ibase + j * 32];
                 }
 #pragma unroll
@@ -302,7 +318,8 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             if (nt < a.num_tiles) issue_load(nt);
         }
 #pragma unroll
-        for (int i = 0; i < W * R / THREADS; ++i) s_wc[i * THREADS + tid] = 0;
+        for (int i = 0; i < (WCW + THREADS - 1) / THREADS; ++i)
+            if (WCW % THREADS == 0 || i * THREADS + tid < WCW) s_wc[i * THREADS + tid] = 0;
 
         // ---- [store] bucket runs leave as coalesced bursts
 #pragma unroll 4
@@ -320,17 +337,21 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
 }
 
 // Startup probe of the lane-order property design 5 relies on: every warp ranks
-// `rows` rows of digits with returning shared atomics and compares each result
-// with the stable rank computed from the definition (count of equal digits in
-// earlier rows + earlier lanes of the same row).  Mismatches are added to *bad.
+// `rows` rows of digits with returning shared atomics — on plain 32-bit counters
+// and on 16-bit halves of shared words (digits 2w, 2w+1 in word w), the two
+// forms the pass uses — and compares each result with the stable rank from the
+// definition (count of equal digits in earlier rows + earlier lanes of the same
+// row, via match.any).  Mismatches are added to *bad.
 __global__ void __launch_bounds__(256) k_rank_probe(uint32_t seed, int rows, uint32_t* bad) {
     __shared__ uint32_t cnt[8][256];
+    __shared__ uint32_t cnt2[8][128];
     __shared__ uint32_t ref[8][256];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) {
         (&cnt[0][0])[i] = 0;
         (&ref[0][0])[i] = 0;
     }
+    for (int i = threadIdx.x; i < 8 * 128; i += blockDim.x) (&cnt2[0][0])[i] = 0;
     __syncthreads();
     // digit ranges 256, 16, 2, 1 (by block) so groups of every size occur
     const uint32_t mask = 0xFFu >> (2 * (blockIdx.x & 3));
@@ -340,10 +361,12 @@ __global__ void __launch_bounds__(256) k_rank_probe(uint32_t seed, int rows, uin
         z ^= z >> 16; z *= 0x7feb352du; z ^= z >> 15; z *= 0x846ca68bu; z ^= z >> 16;
         const uint32_t d = (blockIdx.x & 3) == 3 ? 7u : (z & mask);
         const uint32_t r = atomicAdd(&cnt[warp][d], 1u);
+        const uint32_t sh = (d & 1u) << 4;
+        const uint32_t r2 = (atomicAdd(&cnt2[warp][d >> 1], 1u << sh) >> sh) & 0xFFFFu;
         // definition: earlier rows (ref) + earlier lanes of this row with digit d
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
         const uint32_t want = ref[warp][d] + __popc(peers & lanemask_lt());
-        miss += (r != want);
+        miss += (r != want) + (r2 != want);
         __syncwarp();
         if ((peers & lanemask_gt()) == 0) ref[warp][d] += __popc(peers);
         __syncwarp();
