@@ -321,15 +321,38 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         for (int i = 0; i < (WCW + THREADS - 1) / THREADS; ++i)
             if (WCW % THREADS == 0 || i * THREADS + tid < WCW) s_wc[i * THREADS + tid] = 0;
 
-        // ---- [store] bucket runs leave as coalesced bursts
+        // ---- [store] bucket runs leave as coalesced bursts (full tiles in batches
+        // of SG loads, SG offset lookups, SG stores)
+        if (valid == (uint32_t)TILE && !(RS_AR_ABLATE & 2)) {
+            constexpr int SG = KPT % 8 == 0 ? 8 : (KPT % 4 == 0 ? 4 : 2);
+#pragma unroll 1
+            for (int b = 0; b < KPT; b += SG) {
+                K k[SG];
+                uint32_t g[SG], vv[HAS_VAL ? SG : 1];
+#pragma unroll
+                for (int i = 0; i < SG; ++i) k[i] = s_out[(b + i) * THREADS + tid];
+#pragma unroll
+                for (int i = 0; i < SG; ++i) {
+                    g[i] = s_gofs[digit8<K>(k[i], shift)] + (uint32_t)((b + i) * THREADS + tid);
+                    if (HAS_VAL) vv[HAS_VAL ? i : 0] = s_vout[(b + i) * THREADS + tid];
+                }
+#pragma unroll
+                for (int i = 0; i < SG; ++i) {
+                    RS_DCHECK(g[i] < a.n);
+                    dst[g[i]] = k[i];
+                    if (HAS_VAL) vdst[g[i]] = vv[HAS_VAL ? i : 0];
+                }
+            }
+        } else {
 #pragma unroll 4
-        for (uint32_t i = tid; i < valid; i += THREADS) {
-            if (RS_AR_ABLATE & 2) break;
-            const K k = s_out[i];
-            const uint32_t g = s_gofs[digit8<K>(k, shift)] + i;
-            RS_DCHECK(g < a.n);
-            dst[g] = k;
-            if (HAS_VAL) vdst[g] = s_vout[i];
+            for (uint32_t i = tid; i < valid; i += THREADS) {
+                if (RS_AR_ABLATE & 2) break;
+                const K k = s_out[i];
+                const uint32_t g = s_gofs[digit8<K>(k, shift)] + i;
+                RS_DCHECK(g < a.n);
+                dst[g] = k;
+                if (HAS_VAL) vdst[g] = s_vout[i];
+            }
         }
         __syncthreads();
         tile = s_misc[0];
