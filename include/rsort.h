@@ -126,6 +126,22 @@ rs_status_t rs_comm_destroy(void* comm);
 /* GSD oversampling factor r (s = r·p samples per rank; default 8, BASELINE
  * config 4 "oversampling factor 8·p").  Must match on every rank. */
 rs_status_t rs_comm_set_oversampling(void* comm, int r);
+/* Sample selection of the sample sort (§3.3): mode 0 = GSD's regular
+ * oversampling (default; r from rs_comm_set_oversampling); mode 1 = GER
+ * (Algorithm GER): s·p − 1 keys drawn uniformly at random,
+ * with replacement, from the concatenation of the locally sorted blocks, by
+ * SplitMix64(seed) in counter form — draw i at global position
+ * ⌊z_i·n/2^64⌋, z_i = mix(seed + (i+1)·0x9E3779B97F4A7C15); S_i = (i·s)-th
+ * smallest composite (key, rank, position).  s = 0 selects the paper's
+ * s = 2⌈ω⌉²⌈lg n⌉, ω = lg lg n (n = keys on all ranks).  Everything after the
+ * splitters is GSD's.  Mode, s and seed must match on every rank (checked).
+ * The output capacity (rs_output_capacity) then follows Lemma Sampling1 with
+ * ρ = 1: exceeding it has probability ≤ 1/n and returns RS_ECAPACITY. */
+rs_status_t rs_comm_set_sampling(void* comm, int mode, size_t s, uint64_t seed);
+/* GER's default s for n keys in all, and the Lemma-Sampling1 capacity for a
+ * largest block of n_local_max keys over p ranks (s = 0: the default s). */
+size_t rs_ger_default_s(uint64_t n_total);
+size_t rs_ger_capacity(size_t n_local_max, int p, size_t s);
 int rs_comm_rank(void* comm);
 int rs_comm_size(void* comm);
 
@@ -166,6 +182,19 @@ rs_status_t rs_gsd_exchange_plan(int p, int rank, const uint64_t* counts, const 
 size_t rs_gsd_emulate_ws_bytes(int key_bytes, int val_bytes, int p, int r, int digit_bits, size_t n_max,
                                size_t out_cap);
 rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits,
+                           void* const* keys, uint32_t* const* vals, const size_t* n,
+                           void* const* out_keys, uint32_t* const* out_vals, size_t out_cap,
+                           size_t* n_out, uint64_t* splitters, uint64_t* counts,
+                           void* ws, size_t ws_bytes, void* stream);
+
+/* rs_ger_emulate: GER (see rs_comm_set_sampling) over p ranks on this GPU, with
+ * the same arguments as rs_gsd_emulate except s and seed in place of r
+ * (the draws of every rank go into one array, standing in for the all-reduce).
+ *   ws: rs_ger_emulate_ws_bytes(key_bytes, val_bytes, p, s, digit_bits,
+ *       max_k n[k], out_cap) bytes (s = 0: sized for n = p·max_k n[k]). */
+size_t rs_ger_emulate_ws_bytes(int key_bytes, int val_bytes, int p, size_t s, int digit_bits, size_t n_max,
+                               size_t out_cap);
+rs_status_t rs_ger_emulate(int key_bytes, int p, size_t s, uint64_t seed, int digit_bits,
                            void* const* keys, uint32_t* const* vals, const size_t* n,
                            void* const* out_keys, uint32_t* const* out_vals, size_t out_cap,
                            size_t* n_out, uint64_t* splitters, uint64_t* counts,

@@ -55,6 +55,13 @@ def lib():
         L.or_gsd_u64.restype = i32
         L.or_gsd_u32.argtypes = [i32, i32, i32, vp, vp, vp, sz, vp, vp, vp]
         L.or_gsd_u32.restype = i32
+        u64 = ctypes.c_uint64
+        L.or_ger_u64.argtypes = [i32, sz, u64, i32, vp, vp, vp, vp, vp, sz, vp, vp, vp]
+        L.or_ger_u64.restype = i32
+        L.or_ger_u32.argtypes = [i32, sz, u64, i32, vp, vp, vp, sz, vp, vp, vp]
+        L.or_ger_u32.restype = i32
+        L.or_splitmix64_at.argtypes = [u64, u64]
+        L.or_splitmix64_at.restype = u64
         for name in ("or_is_nondecreasing_u32", "or_is_nondecreasing_u64"):
             getattr(L, name).argtypes = [vp, sz]
             getattr(L, name).restype = i32
@@ -120,6 +127,20 @@ def gsd(shards, r: int, b: int = 8, vals=None, cap: int | None = None):
     """Simulate GSD over p = len(shards) blocks.
 
     Returns dict(Y=[...], Yv=[...] or None, splitters=(p-1,3) array, counts=(p,p))."""
+    return _sample_sort(shards, 0, r, 0, b, vals, cap)
+
+
+def ger(shards, s: int, seed: int, b: int = 8, vals=None, cap: int | None = None):
+    """Simulate GER over p = len(shards) blocks: s·p − 1 random
+    samples drawn with SplitMix64(seed) (readings R28-R30); same result dict as gsd()."""
+    return _sample_sort(shards, 1, s, seed, b, vals, cap)
+
+
+def splitmix64_at(seed: int, i: int) -> int:
+    return int(lib().or_splitmix64_at(seed, i))
+
+
+def _sample_sort(shards, mode, r_or_s, seed, b, vals, cap):
     p = len(shards)
     is32 = shards[0].dtype == np.uint32
     dt = np.uint32 if is32 else np.uint64
@@ -137,8 +158,12 @@ def gsd(shards, r: int, b: int = 8, vals=None, cap: int | None = None):
     Yv = None
     if is32:
         assert vals is None
-        rc = L.or_gsd_u32(p, r, b, kp, N.ctypes.data, yp, cap, ylen.ctypes.data,
-                          spl.ctypes.data, counts.ctypes.data)
+        if mode == 0:
+            rc = L.or_gsd_u32(p, r_or_s, b, kp, N.ctypes.data, yp, cap, ylen.ctypes.data,
+                              spl.ctypes.data, counts.ctypes.data)
+        else:
+            rc = L.or_ger_u32(p, r_or_s, seed, b, kp, N.ctypes.data, yp, cap, ylen.ctypes.data,
+                              spl.ctypes.data, counts.ctypes.data)
     else:
         vp_ = None
         if vals is not None:
@@ -146,9 +171,11 @@ def gsd(shards, r: int, b: int = 8, vals=None, cap: int | None = None):
             Yv = [np.empty(max(cap, 1), dtype=np.uint32) for _ in range(p)]
             vp_ = (ctypes.c_void_p * p)(*[v.ctypes.data for v in vs])
             yvp = (ctypes.c_void_p * p)(*[y.ctypes.data for y in Yv])
-        rc = L.or_gsd_u64(p, r, b, kp, vp_, N.ctypes.data, yp,
-                          yvp if vals is not None else None, cap, ylen.ctypes.data,
-                          spl.ctypes.data, counts.ctypes.data)
+        fn = L.or_gsd_u64 if mode == 0 else L.or_ger_u64
+        args = (p, r_or_s) if mode == 0 else (p, r_or_s, seed)
+        rc = fn(*args, b, kp, vp_, N.ctypes.data, yp,
+                yvp if vals is not None else None, cap, ylen.ctypes.data,
+                spl.ctypes.data, counts.ctypes.data)
     if rc == -2:
         raise OverflowError("GSD output exceeds capacity")
     if rc:

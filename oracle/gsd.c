@@ -33,6 +33,19 @@
  * are ≤_c S_j by a linear scan (the paper's binary search returns the same
  * number because X_k is sorted).  Step 5 repeatedly takes the smallest head,
  * lowest source rank on ties.
+ *
+ * GER(X, n, p) (Algorithm "GER") is the same skeleton with
+ * step 2 replaced by random oversampling: "the sample consists of sp−1 keys
+ * selected uniformly at random from the keys of all X_k".
+ * Readings (R28-R30):
+ *   R28 draw i = 0..sp−2: z_i = SplitMix64 in counter form (this file's own
+ *       copy: z = seed + (i+1)·0x9E3779B97F4A7C15, then the standard finaliser),
+ *       global position q_i = ⌊z_i · n / 2^64⌋ of the concatenation X_0‖…‖X_{p−1}
+ *       of the sorted blocks (with replacement: equal draws give equal composites);
+ *   R29 the key drawn at q_i is the composite (X_k[q_i − off_k], k, q_i − off_k),
+ *       off_k = N_0 + … + N_{k−1} — so splitting, duplicates and stability are
+ *       exactly GSD's (R14-R16); n = 0 gives +∞ composites;
+ *   R30 s = 2⌈ω⌉²⌈lg n⌉ with ω = lg lg n unless the caller fixes s.
  */
 #include <stdlib.h>
 #include <string.h>
@@ -52,16 +65,28 @@ static int comp_qsort(const void* a, const void* b) {
     return comp_cmp((const composite_t*)a, (const composite_t*)b);
 }
 
-int or_gsd_u64(int p, int r, int b,
-               const uint64_t* const* keys, const uint32_t* const* vals, const size_t* N,
-               uint64_t* const* Y_keys, uint32_t* const* Y_vals, size_t Ycap, size_t* Ylen,
-               uint64_t* splitters, uint64_t* counts) {
-    if (p < 1 || r < 1 || (b != 8 && b != 16)) return -1;
-    const size_t s = (size_t)r * (size_t)p;
+/* SplitMix64 (this file's copy; pinned by tests/test_oracle_gsd.py against the
+ * published vector): the i-th output of the sequential generator seeded `seed`. */
+static uint64_t splitmix64_at(uint64_t seed, uint64_t i) {
+    uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+uint64_t or_splitmix64_at(uint64_t seed, uint64_t i) { return splitmix64_at(seed, i); }
+
+/* mode 0: GSD, s = r·p samples per block (regular);  mode 1: GER, s·p − 1 random
+ * samples of the whole input (R28-R29).  Everything else is shared. */
+static int sample_sort_u64(int p, int mode, size_t s, uint64_t seed, int b,
+                           const uint64_t* const* keys, const uint32_t* const* vals, const size_t* N,
+                           uint64_t* const* Y_keys, uint32_t* const* Y_vals, size_t Ycap, size_t* Ylen,
+                           uint64_t* splitters, uint64_t* counts) {
+    if (p < 1 || s < 1 || (b != 8 && b != 16)) return -1;
     int rc = 0;
+    const size_t M = mode == 0 ? s * (size_t)p : s * (size_t)p - 1;  /* sample size */
     uint64_t** X = (uint64_t**)calloc((size_t)p, sizeof(uint64_t*));
     uint32_t** V = (uint32_t**)calloc((size_t)p, sizeof(uint32_t*));
-    composite_t* T = (composite_t*)malloc(s * (size_t)p * sizeof(composite_t));
+    composite_t* T = (composite_t*)malloc((M ? M : 1) * sizeof(composite_t));
     composite_t* S = (composite_t*)malloc((size_t)p * sizeof(composite_t));
     size_t* cut = (size_t*)malloc((size_t)p * ((size_t)p + 1) * sizeof(size_t));
     size_t* head = (size_t*)malloc((size_t)p * sizeof(size_t));
@@ -80,8 +105,25 @@ int or_gsd_u64(int p, int r, int b,
         } else if (or_sr_u64(X[k], N[k], b, -1)) { rc = -1; goto done; }
     }
 
-    /* Step 2: Sample selection — T_k (R10), then T = sort(∪ T_k) (R11). */
-    for (int k = 0; k < p; ++k) {
+    /* Step 2 (GER): sp−1 keys drawn uniformly at random from all X_k (R28, R29). */
+    if (mode == 1) {
+        size_t n = 0;
+        for (int k = 0; k < p; ++k) n += N[k];
+        for (size_t i = 0; i < M; ++i) {
+            composite_t c = { UINT64_MAX, 0, POS_INF };
+            if (n) {
+                const uint64_t q = (uint64_t)(((unsigned __int128)splitmix64_at(seed, i) * n) >> 64);
+                uint64_t off = 0;
+                for (int k = 0; k < p; ++k) {   /* owner: off_k <= q < off_k + N_k */
+                    if (q < off + N[k]) { c.key = X[k][q - off]; c.rank = (uint64_t)k; c.pos = q - off; break; }
+                    off += N[k];
+                }
+            }
+            T[i] = c;
+        }
+    }
+    /* Step 2 (GSD): Sample selection — T_k (R10), then T = sort(∪ T_k) (R11). */
+    for (int k = 0; k < p && mode == 0; ++k) {
         composite_t* Tk = T + (size_t)k * s;
         for (size_t i = 1; i <= s; ++i) {
             composite_t c;
@@ -94,7 +136,7 @@ int or_gsd_u64(int p, int r, int b,
             Tk[i - 1] = c;
         }
     }
-    qsort(T, s * (size_t)p, sizeof(composite_t), comp_qsort);
+    qsort(T, M, sizeof(composite_t), comp_qsort);
 
     /* Step 3: Splitter selection — S_i = T[i·s − 1], 1 ≤ i ≤ p−1 (R12). */
     for (int i = 1; i < p; ++i) {
@@ -152,12 +194,28 @@ done:
     return rc;
 }
 
+int or_gsd_u64(int p, int r, int b,
+               const uint64_t* const* keys, const uint32_t* const* vals, const size_t* N,
+               uint64_t* const* Y_keys, uint32_t* const* Y_vals, size_t Ycap, size_t* Ylen,
+               uint64_t* splitters, uint64_t* counts) {
+    if (p < 1 || r < 1) return -1;
+    return sample_sort_u64(p, 0, (size_t)r * (size_t)p, 0, b, keys, vals, N, Y_keys, Y_vals, Ycap, Ylen,
+                           splitters, counts);
+}
+
+int or_ger_u64(int p, size_t s, uint64_t seed, int b,
+               const uint64_t* const* keys, const uint32_t* const* vals, const size_t* N,
+               uint64_t* const* Y_keys, uint32_t* const* Y_vals, size_t Ycap, size_t* Ylen,
+               uint64_t* splitters, uint64_t* counts) {
+    return sample_sort_u64(p, 1, s, seed, b, keys, vals, N, Y_keys, Y_vals, Ycap, Ylen, splitters, counts);
+}
+
 /* u32 keys: the same algorithm on zero-extended keys (b-bit digits of a u32 key
  * and of its zero extension agree; the extra high rounds see one digit). */
-int or_gsd_u32(int p, int r, int b,
-               const uint32_t* const* keys, const size_t* N,
-               uint32_t* const* Y_keys, size_t Ycap, size_t* Ylen,
-               uint64_t* splitters, uint64_t* counts) {
+static int sample_sort_u32(int p, int mode, size_t s, uint64_t seed, int b,
+                           const uint32_t* const* keys, const size_t* N,
+                           uint32_t* const* Y_keys, size_t Ycap, size_t* Ylen,
+                           uint64_t* splitters, uint64_t* counts) {
     if (p < 1) return -1;
     int rc = 0;
     uint64_t** K = (uint64_t**)calloc((size_t)p, sizeof(uint64_t*));
@@ -169,12 +227,27 @@ int or_gsd_u32(int p, int r, int b,
         if (!K[k] || !Y[k]) rc = -1;
         else for (size_t i = 0; i < N[k]; ++i) K[k][i] = keys[k][i];
     }
-    if (!rc) rc = or_gsd_u64(p, r, b, (const uint64_t* const*)K, NULL, N, Y, NULL, Ycap, Ylen,
-                             splitters, counts);
+    if (!rc) rc = sample_sort_u64(p, mode, s, seed, b, (const uint64_t* const*)K, NULL, N, Y, NULL, Ycap, Ylen,
+                                  splitters, counts);
     if (rc == 0)
         for (int j = 0; j < p; ++j)
             for (size_t i = 0; i < Ylen[j]; ++i) Y_keys[j][i] = (uint32_t)Y[j][i];
     for (int k = 0; k < p; ++k) { free(K[k]); free(Y[k]); }
     free(K); free(Y);
     return rc;
+}
+
+int or_gsd_u32(int p, int r, int b,
+               const uint32_t* const* keys, const size_t* N,
+               uint32_t* const* Y_keys, size_t Ycap, size_t* Ylen,
+               uint64_t* splitters, uint64_t* counts) {
+    if (p < 1 || r < 1) return -1;
+    return sample_sort_u32(p, 0, (size_t)r * (size_t)p, 0, b, keys, N, Y_keys, Ycap, Ylen, splitters, counts);
+}
+
+int or_ger_u32(int p, size_t s, uint64_t seed, int b,
+               const uint32_t* const* keys, const size_t* N,
+               uint32_t* const* Y_keys, size_t Ycap, size_t* Ylen,
+               uint64_t* splitters, uint64_t* counts) {
+    return sample_sort_u32(p, 1, s, seed, b, keys, N, Y_keys, Ycap, Ylen, splitters, counts);
 }

@@ -11,7 +11,8 @@
  *   sr.c      SR-b: serial LSD radix sort by count-sort rounds
  *             (§3.2 "Serial radix-r radix-sort: SR4").
  *   gsd.c     GSD: deterministic regular oversampling sort, simulated for p
- *             processors in one process (Algorithm 1).
+ *             processors in one process (Algorithm 1), and
+ *             GER, its random-oversampling variant.
  *   verify.c  invariants: nondecreasing order, multiset hash, pair stability.
  *
  * Pins (tests/test_oracle.py, tests/test_oracle_gsd.py): library sort
@@ -55,6 +56,20 @@ int or_gsd_u32(int p, int r, int b,
                const uint32_t* const* keys, const size_t* N,
                uint32_t* const* Y_keys, size_t Ycap, size_t* Ylen,
                uint64_t* splitters, uint64_t* counts);
+
+/* GER(X, n, p): as GSD but the sample is s·p − 1 keys drawn
+ * uniformly at random (with replacement, SplitMix64 `seed`, readings R28-R30)
+ * from the concatenation of the sorted blocks; S_i = T[i·s − 1]. */
+int or_ger_u64(int p, size_t s, uint64_t seed, int b,
+               const uint64_t* const* keys, const uint32_t* const* vals, const size_t* N,
+               uint64_t* const* Y_keys, uint32_t* const* Y_vals, size_t Ycap, size_t* Ylen,
+               uint64_t* splitters, uint64_t* counts);
+int or_ger_u32(int p, size_t s, uint64_t seed, int b,
+               const uint32_t* const* keys, const size_t* N,
+               uint32_t* const* Y_keys, size_t Ycap, size_t* Ylen,
+               uint64_t* splitters, uint64_t* counts);
+/* the i-th output of SplitMix64 seeded `seed` (the generator GER draws with) */
+uint64_t or_splitmix64_at(uint64_t seed, uint64_t i);
 
 /* ---- verify.c ------------------------------------------------------------ */
 int or_is_nondecreasing_u32(const uint32_t* a, size_t n);

@@ -203,6 +203,13 @@ class Comm:
         check(lib().rs_comm_set_oversampling(self.handle, r), "rs_comm_set_oversampling")
         self.r = r
 
+    def set_sampling(self, mode: str = "gsd", s: int = 0, seed: int = 0):
+        """"gsd" (regular oversampling, default) or "ger" (random oversampling
+        with s samples per rank, s = 0 the paper's choice, SplitMix64 seed)."""
+        m = {"gsd": 0, "ger": 1}[mode]
+        check(lib().rs_comm_set_sampling(self.handle, m, s, seed), "rs_comm_set_sampling")
+        self.sampling = mode
+
     def capacity(self, n_local: int) -> int:
         return lib().rs_output_capacity(self.ws_n(n_local), self.handle)
 
@@ -225,29 +232,49 @@ def gsd_emulate(blocks: list[torch.Tensor], r: int = 8, digit_bits: int = 8, val
                 out_cap: int | None = None, stream=None):
     """GSD over p = len(blocks) ranks held on this GPU (see include/rsort.h):
     returns dict(Y, Yv, n_out, splitters (p-1,3) uint64, counts (p,p) uint64)."""
+    return _emulate(0, blocks, r, 0, 0, digit_bits, vals, out_cap, stream)
+
+
+def ger_emulate(blocks: list[torch.Tensor], s: int = 0, seed: int = 0, digit_bits: int = 8,
+                vals: list[torch.Tensor] | None = None, out_cap: int | None = None, stream=None):
+    """GER (random oversampling) over p = len(blocks) ranks on
+    this GPU; s = 0 selects the paper's s.  Same result dict as gsd_emulate."""
+    return _emulate(1, blocks, 1, s, seed, digit_bits, vals, out_cap, stream)
+
+
+def _emulate(mode, blocks, r, s, seed, digit_bits, vals, out_cap, stream):
     import numpy as np
     p = len(blocks)
     kb = _KEY_BYTES[blocks[0].dtype]
     n = [b.numel() for b in blocks]
     nmax = max(n) if n else 0
-    cap = out_cap if out_cap is not None else nmax + nmax // r + p
+    if out_cap is not None:
+        cap = out_cap
+    elif mode == 0:
+        cap = nmax + nmax // r + p
+    else:
+        cap = lib().rs_ger_capacity(nmax, p, s)
     dev = blocks[0].device
     outs = [torch.empty(max(cap, 1), dtype=blocks[0].dtype, device=dev) for _ in range(p)]
     vouts = [torch.empty(max(cap, 1), dtype=torch.int32, device=dev) for _ in range(p)] if vals is not None else None
-    wsb = lib().rs_gsd_emulate_ws_bytes(kb, 4 if vals is not None else 0, p, r, digit_bits, nmax, cap)
+    vb = 4 if vals is not None else 0
+    wsb = (lib().rs_gsd_emulate_ws_bytes(kb, vb, p, r, digit_bits, nmax, cap) if mode == 0
+           else lib().rs_ger_emulate_ws_bytes(kb, vb, p, s, digit_bits, nmax, cap))
     ws = _workspace(wsb, dev)
     arr = ctypes.c_void_p * p
     n_arr = (ctypes.c_size_t * p)(*n)
     n_out = (ctypes.c_size_t * p)()
     spl = np.zeros((max(p - 1, 1), 3), dtype=np.uint64)
     counts = np.zeros((p, p), dtype=np.uint64)
-    check(lib().rs_gsd_emulate(kb, p, r, digit_bits, arr(*[b.data_ptr() for b in blocks]),
-                               arr(*[v.data_ptr() for v in vals]) if vals is not None else None, n_arr,
-                               arr(*[o.data_ptr() for o in outs]),
-                               arr(*[o.data_ptr() for o in vouts]) if vals is not None else None, cap, n_out,
-                               spl.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
-                               counts.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ws.data_ptr(), ws.numel(),
-                               _stream(stream)), "rs_gsd_emulate")
+    head = (kb, p, r) if mode == 0 else (kb, p, s, seed)
+    fn = lib().rs_gsd_emulate if mode == 0 else lib().rs_ger_emulate
+    check(fn(*head, digit_bits, arr(*[b.data_ptr() for b in blocks]),
+             arr(*[v.data_ptr() for v in vals]) if vals is not None else None, n_arr,
+             arr(*[o.data_ptr() for o in outs]),
+             arr(*[o.data_ptr() for o in vouts]) if vals is not None else None, cap, n_out,
+             spl.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
+             counts.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ws.data_ptr(), ws.numel(),
+             _stream(stream)), "rs_gsd_emulate" if mode == 0 else "rs_ger_emulate")
     return dict(Y=[outs[j][: n_out[j]] for j in range(p)],
                 Yv=[vouts[j][: n_out[j]] for j in range(p)] if vals is not None else None,
                 n_out=list(n_out), splitters=spl[: p - 1], counts=counts)

@@ -16,7 +16,16 @@
 //                          (R16): a tree of stable 2-way merge-path merges (merge.cu),
 //                          or optionally a stable radix re-sort of the concatenation,
 //                          which gives the identical result (R17).
+//
+// GER replaces step 2-3 (Comm::sampling = 1): s·p − 1 keys drawn
+// uniformly at random from the concatenation of the sorted blocks (readings R28-R30:
+// SplitMix64 counter draws, position ⌊z·n/2^64⌋, with replacement).  Each rank fills
+// the draws that fall in its block (k_ger_draw), ncclAllReduce(max) assembles the
+// sample everywhere, and two stable radix sorts of the (position, draw) and then
+// (key, draw) pairs order it by composite (key, rank, pos) — too large for the
+// one-CTA bitonic sort; S_i is the (i·s)-th smallest (k_ger_pick).
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -112,6 +121,59 @@ __global__ void k_gsd_split(const K* __restrict__ X, size_t N, uint32_t rank, in
     counts[j] = (uint64_t)(cut(j + 1) - cut(j));
 }
 
+// ------------------------------------------------------------------ GER ---
+__device__ __forceinline__ uint64_t splitmix64_at(uint64_t seed, uint64_t i) {
+    uint64_t z = seed + (i + 1) * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+// draws i < M that land in this rank's block [off, off + N): key and position
+// (the other entries are left as they are: zero, for the max all-reduce)
+template <typename K>
+__global__ void k_ger_draw(const K* __restrict__ X, uint64_t off, size_t N, uint64_t n_total, uint64_t seed, size_t M,
+                           uint64_t* __restrict__ key, uint64_t* __restrict__ q) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (size_t)gridDim.x * blockDim.x) {
+        const uint64_t qi = __umul64hi(splitmix64_at(seed, i), n_total);
+        if (qi >= off && qi - off < N) {
+            key[i] = static_cast<uint64_t>(X[qi - off]);
+            q[i] = qi;
+        }
+    }
+}
+
+__global__ void k_iota_u32(uint32_t* __restrict__ a, size_t M) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (size_t)gridDim.x * blockDim.x)
+        a[i] = (uint32_t)i;
+}
+
+__global__ void k_ger_gather(const uint64_t* __restrict__ key, const uint32_t* __restrict__ idx, size_t M,
+                             uint64_t* __restrict__ out) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < M; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = key[idx[i]];
+}
+
+// S_j = composite of the (j·s)-th smallest draw: rank = owner of its position
+__global__ void k_ger_pick(const uint64_t* __restrict__ key, const uint64_t* __restrict__ q,
+                           const uint32_t* __restrict__ order, size_t s, int p, const uint64_t* __restrict__ off,
+                           Comp* __restrict__ S) {
+    const int j = 1 + threadIdx.x;
+    if (j >= p) return;
+    const uint32_t e = order[(size_t)j * s - 1];
+    const uint64_t qe = q[e];
+    int k = 0;
+    while (k + 1 < p && off[k + 1] <= qe) ++k;  // last block starting at or before qe: non-empty, owns qe
+    S[j - 1] = Comp{key[e], (uint32_t)k, (uint32_t)(qe - off[k])};
+}
+
+size_t ger_default_s(uint64_t n_total) {
+    // s = 2⌈ω⌉²⌈lg n⌉, ω = lg lg n  (reading R30)
+    const double lg = n_total > 1 ? std::log2((double)n_total) : 1.0;
+    const double w = std::max(1.0, std::ceil(lg > 1.0 ? std::log2(lg) : 1.0));
+    return (size_t)(2.0 * w * w * std::ceil(lg));
+}
+
 // ------------------------------------------------------------------ host --
 struct GsdLayout {
     void* local_ws;
@@ -125,6 +187,17 @@ struct GsdLayout {
     Comp* splitters;      // p-1
     uint64_t* counts_local;  // p
     uint64_t* counts_all;    // p*p (or p slots of p for the emulation)
+    // GER: M = s·p − 1 draws
+    uint64_t* ger_key;   // M
+    uint64_t* ger_q;     // M
+    uint64_t* ger_k2;    // M (positions in order, then gathered keys)
+    uint64_t* ger_k3;    // M (keys in composite order)
+    uint32_t* ger_idx;   // M
+    uint32_t* ger_ia;    // M
+    uint32_t* ger_ib;    // M
+    uint64_t* ger_off;   // p + 1 block offsets
+    void* ger_ws;        // radix workspace for M (u64, u32) pairs
+    size_t ger_ws_bytes, ger_M;
     void* merge_keys;        // merge-tree scratch: cap keys (+ values)
     uint32_t* merge_vals;
     size_t* merge_split;
@@ -132,7 +205,7 @@ struct GsdLayout {
 };
 
 static GsdLayout gsd_layout(void* ws, int key_bytes, bool has_val, size_t n, size_t cap, int b, int p, int r,
-                            size_t recv_slots) {
+                            size_t recv_slots, size_t ger_M = 0) {
     GsdLayout L{};
     Carver c(ws);
     const size_t s = (size_t)r * p;
@@ -150,20 +223,92 @@ static GsdLayout gsd_layout(void* ws, int key_bytes, bool has_val, size_t n, siz
     L.merge_keys = c.take(cap * key_bytes);
     L.merge_vals = static_cast<uint32_t*>(has_val ? c.take(cap * 4) : nullptr);
     L.merge_split = static_cast<size_t*>(c.take(merge_scratch_bytes(cap)));
+    L.ger_M = ger_M;
+    if (ger_M) {
+        L.ger_key = static_cast<uint64_t*>(c.take(ger_M * 8));
+        L.ger_q = static_cast<uint64_t*>(c.take(ger_M * 8));
+        L.ger_k2 = static_cast<uint64_t*>(c.take(ger_M * 8));
+        L.ger_k3 = static_cast<uint64_t*>(c.take(ger_M * 8));
+        L.ger_idx = static_cast<uint32_t*>(c.take(ger_M * 4));
+        L.ger_ia = static_cast<uint32_t*>(c.take(ger_M * 4));
+        L.ger_ib = static_cast<uint32_t*>(c.take(ger_M * 4));
+        L.ger_off = static_cast<uint64_t*>(c.take(((size_t)p + 1) * 8));
+        L.ger_ws_bytes = local_ws_bytes(8, true, ger_M, 8);
+        L.ger_ws = c.take(L.ger_ws_bytes);
+    }
     L.bytes = c.used();
     return L;
 }
+
+// GER draws for n_total keys over p ranks (0 for GSD)
+static size_t ger_draws(size_t s, int p) { return p > 1 ? s * (size_t)p - 1 : 0; }
 
 static size_t capacity_for(size_t n_local_max, int r, int p) {
     // ⌊(1 + 1/r)·N_max⌋ + p   (reading R18)
     return n_local_max + n_local_max / (size_t)r + (size_t)p;
 }
 
-size_t gsd_capacity(Comm* c, size_t n_local_max) { return capacity_for(n_local_max, c->r, c->nranks); }
+// GER: Lemma `Sampling1` with ρ = 1 bounds every bucket of the
+// non-sample keys by ⌈(1+ε)(n−p+1)/p⌉ with probability ≥ 1 − 1/n, for the smallest
+// ε with s ≥ (1+ε)/ε²·(2 ln n + ln(2π p²(ps−1) e^{1/(3(ps−1))})); a bucket also
+// holds at most s sample keys.  Capacity = ⌈(1+ε)·N_max⌉ + s + p (n ≤ p·N_max).
+static size_t ger_capacity_for(size_t n_local_max, int p, size_t s) {
+    const double n = std::max(2.0, (double)n_local_max * p), ps1 = std::max(1.0, (double)s * p - 1);
+    const double A = 2.0 * std::log(n) + std::log(2.0 * 3.141592653589793 * p * p * ps1) + 1.0 / (3.0 * ps1);
+    const double eps = (A + std::sqrt(A * A + 4.0 * (double)s * A)) / (2.0 * (double)s);  // s·ε² − A·ε − A = 0
+    return (size_t)std::ceil((1.0 + eps) * (double)n_local_max) + s + (size_t)p;
+}
+
+static size_t ger_s_for(Comm* c, uint64_t n_total) { return c->ger_s ? c->ger_s : ger_default_s(n_total); }
+
+size_t gsd_capacity(Comm* c, size_t n_local_max) {
+    if (c->sampling == 1) return ger_capacity_for(n_local_max, c->nranks, ger_s_for(c, (uint64_t)n_local_max * c->nranks));
+    return capacity_for(n_local_max, c->r, c->nranks);
+}
 
 size_t gsd_ws_bytes(Comm* c, int key_bytes, bool has_val, size_t n_local_max, int b) {
     const size_t cap = gsd_capacity(c, n_local_max);
-    return gsd_layout(nullptr, key_bytes, has_val, n_local_max, cap, b, c->nranks, c->r, 1).bytes;
+    const size_t M = c->sampling == 1 ? ger_draws(ger_s_for(c, (uint64_t)n_local_max * c->nranks), c->nranks) : 0;
+    return gsd_layout(nullptr, key_bytes, has_val, n_local_max, cap, b, c->nranks, c->r, 1, M).bytes;
+}
+
+// GER steps 2b-3 on the assembled draws (L.ger_key, L.ger_q, M entries; offsets in
+// L.ger_off): order the draws by composite with two stable radix sorts, pick S_j
+static rs_status_t ger_splitters(const GsdLayout& L, size_t M, size_t s, int p, uint64_t n_total, Comp* S,
+                                 cudaStream_t st) {
+    const int threads = 256;
+    const int grid = (int)std::min<size_t>((M + threads - 1) / threads, 1024);
+    {
+        LaunchScope ls("ger_sample", st);
+        k_iota_u32<<<grid, threads, 0, st>>>(L.ger_idx, M);
+    }
+    // (position, draw) -> draws in position order; positions need ⌈log2 n⌉ bits
+    int qbits = 8;
+    while (qbits < 64 && (n_total >> qbits) != 0) qbits += 8;
+    rs_status_t sst = local_sort(8, L.ger_q, L.ger_idx, M, 8, qbits, L.ger_k2, L.ger_ia, L.ger_ws, L.ger_ws_bytes, st);
+    if (sst != RS_OK) return sst;
+    {
+        LaunchScope ls("ger_sample", st);
+        k_ger_gather<<<grid, threads, 0, st>>>(L.ger_key, L.ger_ia, M, L.ger_k2);
+    }
+    // stable by key: ties keep position order, i.e. (key, rank, pos) order
+    sst = local_sort(8, L.ger_k2, L.ger_ia, M, 8, 64, L.ger_k3, L.ger_ib, L.ger_ws, L.ger_ws_bytes, st);
+    if (sst != RS_OK) return sst;
+    LaunchScope ls("ger_sample", st);
+    k_ger_pick<<<1, ((p + 31) / 32) * 32, 0, st>>>(L.ger_key, L.ger_q, L.ger_ib, s, p, L.ger_off, S);
+    return RS_OK;
+}
+
+static rs_status_t launch_ger_draw(int key_bytes, const void* X, uint64_t off, size_t N, uint64_t n_total,
+                                   uint64_t seed, size_t M, uint64_t* key, uint64_t* q, cudaStream_t st) {
+    if (!N || !M) return RS_OK;
+    LaunchScope ls("ger_sample", st);
+    const int grid = (int)std::min<size_t>((M + 255) / 256, 1024);
+    if (key_bytes == 4)
+        k_ger_draw<uint32_t><<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(X), off, N, n_total, seed, M, key, q);
+    else
+        k_ger_draw<uint64_t><<<grid, 256, 0, st>>>(static_cast<const uint64_t*>(X), off, N, n_total, seed, M, key, q);
+    return RS_OK;
 }
 
 static rs_status_t launch_sample(int key_bytes, const void* X, size_t N, int rank, int s, Comp* out,
@@ -228,23 +373,26 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
     const int p = c->nranks, rank = c->rank, r = c->r;
     const size_t s = (size_t)r * p;
     const bool hv = vals != nullptr;
-    if ((size_t)p * s > (size_t)kMaxSample)
+    const bool ger = c->sampling == 1;
+    if (!ger && (size_t)p * s > (size_t)kMaxSample)
         return fail(RS_EINVAL, "r*p^2 exceeds the one-CTA sample sort limit of 8192");
-    const GsdLayout L = gsd_layout(ws, key_bytes, hv, n, out_cap, b, p, r, 1);
+    GsdLayout L = gsd_layout(ws, key_bytes, hv, n, out_cap, b, p, r, 1);  // GER region carved once n is known
     if (!ws || ws_bytes < L.bytes || !aligned16(ws))
         return fail(RS_EINVAL, "GSD workspace too small / misaligned: need " + std::to_string(L.bytes));
     if (out_cap && (!out || (hv && !vout))) return fail(RS_EINVAL, "NULL output with out_cap > 0");
 
     // header all-gather: a mismatch is an error on every rank, not a hang
     uint64_t* h = c->h_pinned;
-    uint64_t hdr[8] = {0x52534F5254ull, (uint64_t)key_bytes, (uint64_t)hv, (uint64_t)b, (uint64_t)r, (uint64_t)p,
+    const uint64_t samp_id = ger ? (0x4745520000000000ull ^ (uint64_t)c->ger_s ^ (c->ger_seed * 0x9E3779B97F4A7C15ull))
+                                 : (uint64_t)r;
+    uint64_t hdr[8] = {0x52534F5254ull, (uint64_t)key_bytes, (uint64_t)hv, (uint64_t)b, samp_id, (uint64_t)p,
                        (uint64_t)out_cap, (uint64_t)n};
     std::memcpy(h, hdr, sizeof(hdr));
     RS_CUDA_TRY(cudaMemcpyAsync(L.hdr_local, h, sizeof(hdr), cudaMemcpyHostToDevice, st));
     RS_NCCL_TRY(ncclAllGather(L.hdr_local, L.hdr_all, 8, ncclUint64, c->nccl, st));
     RS_CUDA_TRY(cudaMemcpyAsync(h, L.hdr_all, (size_t)p * 64, cudaMemcpyDeviceToHost, st));
     RS_CUDA_TRY(cudaStreamSynchronize(st));
-    std::vector<uint64_t> caps(p);
+    std::vector<uint64_t> caps(p), noff(p + 1, 0);
     for (int k = 0; k < p; ++k) {
         for (int f = 0; f < 6; ++f)
             if (h[k * 8 + f] != hdr[f])
@@ -252,6 +400,17 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
                                            std::to_string(f) + ")");
         caps[k] = h[k * 8 + 6];
         if (h[k * 8 + 7] >= (1ull << 32)) return fail(RS_EINVAL, "n >= 2^32 on rank " + std::to_string(k));
+        noff[k + 1] = noff[k] + h[k * 8 + 7];
+    }
+    const uint64_t n_total = noff[p];
+    size_t ger_s = 0, M = 0;
+    if (ger) {
+        ger_s = ger_s_for(c, n_total);
+        M = ger_draws(ger_s, p);
+        L = gsd_layout(ws, key_bytes, hv, n, out_cap, b, p, r, 1, M);
+        if (ws_bytes < L.bytes)
+            return fail(RS_EINVAL, "GER workspace too small: need " + std::to_string(L.bytes) +
+                                       " (size it with the largest local n)");
     }
 
     // step 1: local sort in place -> X_k
@@ -259,11 +418,26 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
                                      L.local_ws_bytes, st)
                         : RS_OK;
     if (sst != RS_OK) return sst;
-    // step 2: regular sample + all-gather
-    if ((sst = launch_sample(key_bytes, keys, n, rank, (int)s, L.samp_local, st)) != RS_OK) return sst;
-    RS_NCCL_TRY(ncclAllGather(L.samp_local, L.samp_all, s * sizeof(Comp), ncclUint8, c->nccl, st));
-    // step 3: splitters, identical on every rank
-    if ((sst = launch_splitters(L.samp_all, (int)(p * s), (int)s, p, L.splitters, st)) != RS_OK) return sst;
+    if (ger && M) {
+        // GER step 2: random sample assembled on every rank by a max all-reduce
+        std::memcpy(h, noff.data(), (p + 1) * 8);
+        RS_CUDA_TRY(cudaMemcpyAsync(L.ger_off, h, (p + 1) * 8, cudaMemcpyHostToDevice, st));
+        RS_CUDA_TRY(cudaMemsetAsync(L.ger_key, 0, M * 8, st));
+        RS_CUDA_TRY(cudaMemsetAsync(L.ger_q, 0, M * 8, st));
+        if ((sst = launch_ger_draw(key_bytes, keys, noff[rank], n, n_total, c->ger_seed, M, L.ger_key, L.ger_q,
+                                   st)) != RS_OK)
+            return sst;
+        RS_NCCL_TRY(ncclAllReduce(L.ger_key, L.ger_key, M, ncclUint64, ncclMax, c->nccl, st));
+        RS_NCCL_TRY(ncclAllReduce(L.ger_q, L.ger_q, M, ncclUint64, ncclMax, c->nccl, st));
+        // GER step 3: S_i = (i·s)-th smallest, identical on every rank
+        if ((sst = ger_splitters(L, M, ger_s, p, n_total, L.splitters, st)) != RS_OK) return sst;
+    } else if (!ger) {
+        // step 2: regular sample + all-gather
+        if ((sst = launch_sample(key_bytes, keys, n, rank, (int)s, L.samp_local, st)) != RS_OK) return sst;
+        RS_NCCL_TRY(ncclAllGather(L.samp_local, L.samp_all, s * sizeof(Comp), ncclUint8, c->nccl, st));
+        // step 3: splitters, identical on every rank
+        if ((sst = launch_splitters(L.samp_all, (int)(p * s), (int)s, p, L.splitters, st)) != RS_OK) return sst;
+    }
     // step 4: split + count exchange
     if ((sst = launch_split(key_bytes, keys, n, rank, p, L.splitters, L.counts_local, st)) != RS_OK) return sst;
     RS_NCCL_TRY(ncclAllGather(L.counts_local, L.counts_all, p, ncclUint64, c->nccl, st));
@@ -393,41 +567,57 @@ int rs_comm_rank(void* comm) { return comm ? static_cast<Comm*>(comm)->rank : 0;
 int rs_comm_size(void* comm) { return comm ? static_cast<Comm*>(comm)->nranks : 1; }
 
 // ---------------------------------------------------------- emulation ----
-size_t rs_gsd_emulate_ws_bytes(int key_bytes, int val_bytes, int p, int r, int digit_bits, size_t n_max,
-                               size_t out_cap) {
-    if (p < 1 || r < 1) return 0;
-    return gsd_layout(nullptr, key_bytes, val_bytes != 0, n_max, out_cap, digit_bits, p, r, 1).bytes;
-}
+}  // extern "C"
 
-rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits, void* const* keys, uint32_t* const* vals,
-                           const size_t* n, void* const* out_keys, uint32_t* const* out_vals, size_t out_cap,
-                           size_t* n_out, uint64_t* splitters, uint64_t* counts, void* ws, size_t ws_bytes,
-                           void* stream) {
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
+namespace rs {
+// GSD (mode 0, oversampling r) or GER (mode 1, s draws per rank, seed) over p
+// ranks held on this GPU: every rank's steps, device copies in place of NCCL
+static rs_status_t emulate(int mode, int key_bytes, int p, int r, size_t ger_s, uint64_t seed, int digit_bits,
+                           void* const* keys, uint32_t* const* vals, const size_t* n, void* const* out_keys,
+                           uint32_t* const* out_vals, size_t out_cap, size_t* n_out, uint64_t* splitters,
+                           uint64_t* counts, void* ws, size_t ws_bytes, cudaStream_t st) {
     if (p < 1 || r < 1 || !keys || !n || !out_keys || !n_out) return fail(RS_EINVAL, "bad emulate arguments");
     if (digit_bits != 8 && digit_bits != 16) return fail(RS_EINVAL, "digit_bits must be 8 or 16");
     if (key_bytes != 4 && key_bytes != 8) return fail(RS_EINVAL, "key_bytes must be 4 or 8");
     const bool hv = vals != nullptr;
     const size_t s = (size_t)r * p;
-    if ((size_t)p * s > (size_t)kMaxSample) return fail(RS_EINVAL, "r*p^2 exceeds 8192");
+    if (mode == 0 && (size_t)p * s > (size_t)kMaxSample) return fail(RS_EINVAL, "r*p^2 exceeds 8192");
     size_t n_max = 0;
+    std::vector<uint64_t> noff(p + 1, 0);
     for (int k = 0; k < p; ++k) {
         if (n[k] >= (1ull << 32)) return fail(RS_EINVAL, "n >= 2^32");
         if (n[k] && (!keys[k] || !aligned16(keys[k]) || (hv && (!vals[k] || !aligned16(vals[k])))))
             return fail(RS_EINVAL, "NULL / misaligned block");
         n_max = std::max(n_max, n[k]);
+        noff[k + 1] = noff[k] + n[k];
     }
-    const GsdLayout L = gsd_layout(ws, key_bytes, hv, n_max, out_cap, digit_bits, p, r, 1);
+    const uint64_t n_total = noff[p];
+    const size_t gs = mode == 1 ? (ger_s ? ger_s : ger_default_s(n_total)) : 0;
+    const size_t M = mode == 1 ? ger_draws(gs, p) : 0;
+    const GsdLayout L = gsd_layout(ws, key_bytes, hv, n_max, out_cap, digit_bits, p, r, 1, M);
     if (!ws || ws_bytes < L.bytes) return fail(RS_EINVAL, "emulate workspace too small: need " + std::to_string(L.bytes));
     rs_status_t sst;
     for (int k = 0; k < p; ++k)  // step 1
         if (n[k] && (sst = local_sort(key_bytes, keys[k], hv ? vals[k] : nullptr, n[k], digit_bits, key_bytes * 8,
                                       keys[k], hv ? vals[k] : nullptr, L.local_ws, L.local_ws_bytes, st)) != RS_OK)
             return sst;
+    if (mode == 1) {  // GER steps 2-3: the draws of every rank into one array (= the all-reduce)
+        if (M) {
+            RS_CUDA_TRY(cudaMemcpyAsync(L.ger_off, noff.data(), (p + 1) * 8, cudaMemcpyHostToDevice, st));
+            RS_CUDA_TRY(cudaMemsetAsync(L.ger_key, 0, M * 8, st));
+            RS_CUDA_TRY(cudaMemsetAsync(L.ger_q, 0, M * 8, st));
+            for (int k = 0; k < p; ++k)
+                if ((sst = launch_ger_draw(key_bytes, keys[k], noff[k], n[k], n_total, seed, M, L.ger_key, L.ger_q,
+                                           st)) != RS_OK)
+                    return sst;
+            if ((sst = ger_splitters(L, M, gs, p, n_total, L.splitters, st)) != RS_OK) return sst;
+        }
+    } else {
     for (int k = 0; k < p; ++k)  // step 2 (the all-gather is the slot layout)
         if ((sst = launch_sample(key_bytes, keys[k], n[k], k, (int)s, L.samp_all + (size_t)k * s, st)) != RS_OK)
             return sst;
     if ((sst = launch_splitters(L.samp_all, (int)(p * s), (int)s, p, L.splitters, st)) != RS_OK) return sst;
+    }
     for (int k = 0; k < p; ++k)  // step 4
         if ((sst = launch_split(key_bytes, keys[k], n[k], k, p, L.splitters, L.counts_all + (size_t)k * p, st)) !=
             RS_OK)
@@ -484,6 +674,54 @@ rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits, void* co
             return sst;
     }
     RS_CUDA_TRY(cudaGetLastError());
+    return RS_OK;
+}
+}  // namespace rs
+
+extern "C" {
+
+size_t rs_gsd_emulate_ws_bytes(int key_bytes, int val_bytes, int p, int r, int digit_bits, size_t n_max,
+                               size_t out_cap) {
+    if (p < 1 || r < 1) return 0;
+    return gsd_layout(nullptr, key_bytes, val_bytes != 0, n_max, out_cap, digit_bits, p, r, 1).bytes;
+}
+
+rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits, void* const* keys, uint32_t* const* vals,
+                           const size_t* n, void* const* out_keys, uint32_t* const* out_vals, size_t out_cap,
+                           size_t* n_out, uint64_t* splitters, uint64_t* counts, void* ws, size_t ws_bytes,
+                           void* stream) {
+    return emulate(0, key_bytes, p, r, 0, 0, digit_bits, keys, vals, n, out_keys, out_vals, out_cap, n_out,
+                   splitters, counts, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+size_t rs_ger_emulate_ws_bytes(int key_bytes, int val_bytes, int p, size_t s, int digit_bits, size_t n_max,
+                               size_t out_cap) {
+    if (p < 1) return 0;
+    const size_t gs = s ? s : ger_default_s((uint64_t)n_max * p);
+    return gsd_layout(nullptr, key_bytes, val_bytes != 0, n_max, out_cap, digit_bits, p, 1, 1, ger_draws(gs, p)).bytes;
+}
+
+rs_status_t rs_ger_emulate(int key_bytes, int p, size_t s, uint64_t seed, int digit_bits, void* const* keys,
+                           uint32_t* const* vals, const size_t* n, void* const* out_keys, uint32_t* const* out_vals,
+                           size_t out_cap, size_t* n_out, uint64_t* splitters, uint64_t* counts, void* ws,
+                           size_t ws_bytes, void* stream) {
+    return emulate(1, key_bytes, p, 1, s, seed, digit_bits, keys, vals, n, out_keys, out_vals, out_cap, n_out,
+                   splitters, counts, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
+size_t rs_ger_capacity(size_t n_local_max, int p, size_t s) {
+    if (p < 1) return 0;
+    return ger_capacity_for(n_local_max, p, s ? s : ger_default_s((uint64_t)n_local_max * p));
+}
+
+size_t rs_ger_default_s(uint64_t n_total) { return ger_default_s(n_total); }
+
+rs_status_t rs_comm_set_sampling(void* comm, int mode, size_t s, uint64_t seed) {
+    if (!comm || (mode != 0 && mode != 1)) return fail(RS_EINVAL, "bad comm / sampling mode");
+    Comm* c = static_cast<Comm*>(comm);
+    c->sampling = mode;
+    c->ger_s = s;
+    c->ger_seed = seed;
     return RS_OK;
 }
 

@@ -14,6 +14,9 @@ struct Comm {
     ncclComm_t nccl = nullptr;
     int rank = 0, nranks = 1, device = 0;
     int r = 8;                     // oversampling factor, s = r·p
+    int sampling = 0;              // 0 GSD (regular), 1 GER (random)
+    size_t ger_s = 0;              // GER: samples per rank (s·p − 1 in all); 0 = 2⌈ω⌉²⌈lg n⌉, ω = lg lg n
+    uint64_t ger_seed = 0;         // GER: SplitMix64 seed of the sample draws
     uint64_t* h_pinned = nullptr;  // p*p counts + headers (pinned host)
     size_t h_pinned_words = 0;
 };
@@ -27,6 +30,9 @@ struct Comp {
 };
 constexpr uint32_t kPosInf = 0xFFFFFFFFu;
 constexpr int kMaxSample = 8192;  // r·p² composites sorted in one CTA
+
+// GER's s for n keys in all when the caller did not fix it (reading R30)
+size_t ger_default_s(uint64_t n_total);
 
 size_t gsd_capacity(Comm* c, size_t n_local_max);
 size_t gsd_ws_bytes(Comm* c, int key_bytes, bool has_val, size_t n_local_max, int b);

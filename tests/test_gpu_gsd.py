@@ -119,3 +119,56 @@ def test_merge_tree_large_runs(option):
     blocks = [inputs.gen_u32(n, 90 + i, "sorted" if i % 2 else "uniform") for i, n in
               enumerate((300000, 17, 250001, 0, 123457))]
     _check(blocks, r=8, b=8)
+
+
+# ---------------------------------------------------------------- GER ----
+def _check_ger(blocks_np, s, seed, b=8, vals_np=None):
+    p = len(blocks_np)
+    dt = blocks_np[0].dtype
+    want = oracle.ger(blocks_np, s=s if s else _default_s(sum(x.size for x in blocks_np)), seed=seed, b=b,
+                      vals=vals_np)
+    got = rs.ger_emulate([dev(x) for x in blocks_np], s=s, seed=seed, digit_bits=b,
+                         vals=[dev(v) for v in vals_np] if vals_np is not None else None)
+    assert got["counts"].tolist() == want["counts"].tolist()
+    assert got["splitters"].tolist() == want["splitters"].tolist()
+    for j in range(p):
+        assert (host(got["Y"][j], dt) == want["Y"][j]).all(), j
+        if vals_np is not None:
+            assert (host(got["Yv"][j], np.uint32) == want["Yv"][j]).all(), j
+    return got
+
+
+def _default_s(n):
+    return int(rs.lib().rs_ger_default_s(n))
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 8])
+@pytest.mark.parametrize("dist", ["uniform", "mod16", "equal", "reversed"])
+def test_ger_u32_matches_simulator(p, dist):
+    """GER: random sample drawn on the GPU (SplitMix64 counter
+    draws), ordered by two stable radix sorts, S_i = (i·s)-th: splitters, count
+    matrix and every Y_j bit-exact against the CPU simulator."""
+    total = 50000 + 3 * p
+    a = inputs.gen_u32(total, 80 + p, dist)
+    cuts = np.linspace(0, total, p + 1).astype(int)
+    _check_ger([a[cuts[k]:cuts[k + 1]] for k in range(p)], s=0, seed=11 + p)   # the paper's s
+    _check_ger([a[cuts[k]:cuts[k + 1]] for k in range(p)], s=13, seed=7)
+
+
+@pytest.mark.parametrize("b", [8, 16])
+def test_ger_pairs_global_stability(b):
+    p, N = 4, 20000
+    k = inputs.gen_u64(p * N, 6, "mod1024")
+    v = inputs.iota_u32(p * N)
+    got = _check_ger([k[i * N:(i + 1) * N] for i in range(p)], s=0, seed=2, b=b,
+                     vals_np=[v[i * N:(i + 1) * N] for i in range(p)])
+    K = np.concatenate([host(y, np.uint64) for y in got["Y"]])
+    V = np.concatenate([host(y, np.uint32) for y in got["Yv"]])
+    assert oracle.pairs_stable(K, V)
+
+
+def test_ger_uneven_empty_blocks_and_u64():
+    a = inputs.gen_u32(9000, 91)
+    _check_ger([a[:0], a[:5000], a[5000:5003], a[5003:]], s=6, seed=4)
+    k = inputs.gen_u64(30001, 92)
+    _check_ger([k[:12000], k[12000:12001], k[12001:]], s=0, seed=5)

@@ -64,3 +64,15 @@ def test_gsd_capacity_error(comm):
     with pytest.raises(rs.RSortError) as e:
         rs.sort(dev(a), comm=comm, out_cap=999)
     assert e.value.status == 5
+
+
+def test_ger_p1_through_nccl(comm):
+    """GER sampling selected on the communicator (header-checked); at p = 1 there
+    are no splitters, so the call is the local sort through the NCCL path."""
+    comm.set_sampling("ger", s=0, seed=3)
+    try:
+        a = inputs.gen_u32(70001, 62)
+        y = rs.sort(dev(a), comm=comm)
+        assert (host(y, np.uint32) == oracle.sr(a, 8)).all()
+    finally:
+        comm.set_sampling("gsd")
