@@ -134,7 +134,11 @@ rs_status_t rs_comm_set_oversampling(void* comm, int r);
  * ⌊z_i·n/2^64⌋, z_i = mix(seed + (i+1)·0x9E3779B97F4A7C15); S_i = (i·s)-th
  * smallest composite (key, rank, position).  s = 0 selects the paper's
  * s = 2⌈ω⌉²⌈lg n⌉, ω = lg lg n (n = keys on all ranks).  Everything after the
- * splitters is GSD's.  Mode, s and seed must match on every rank (checked).
+ * splitters is GSD's.  mode 2 = GVR (Algorithm GVR): the
+ * same draws taken from the UNSORTED blocks (positions in the unsorted block),
+ * each key sent to the rank of its splitter interval (binary search, then a
+ * stable count-sort by destination), and Y_j sorted locally after the exchange
+ * (same result, no merge).  Mode, s and seed must match on every rank (checked).
  * The output capacity (rs_output_capacity) then follows Lemma Sampling1 with
  * ρ = 1: exceeding it has probability ≤ 1/n and returns RS_ECAPACITY. */
 rs_status_t rs_comm_set_sampling(void* comm, int mode, size_t s, uint64_t seed);
@@ -195,6 +199,16 @@ rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits,
 size_t rs_ger_emulate_ws_bytes(int key_bytes, int val_bytes, int p, size_t s, int digit_bits, size_t n_max,
                                size_t out_cap);
 rs_status_t rs_ger_emulate(int key_bytes, int p, size_t s, uint64_t seed, int digit_bits,
+                           void* const* keys, uint32_t* const* vals, const size_t* n,
+                           void* const* out_keys, uint32_t* const* out_vals, size_t out_cap,
+                           size_t* n_out, uint64_t* splitters, uint64_t* counts,
+                           void* ws, size_t ws_bytes, void* stream);
+
+/* rs_gvr_emulate: GVR over p ranks on this GPU, arguments as rs_ger_emulate
+ * (the blocks are partitioned by destination in place). */
+size_t rs_gvr_emulate_ws_bytes(int key_bytes, int val_bytes, int p, size_t s, int digit_bits, size_t n_max,
+                               size_t out_cap);
+rs_status_t rs_gvr_emulate(int key_bytes, int p, size_t s, uint64_t seed, int digit_bits,
                            void* const* keys, uint32_t* const* vals, const size_t* n,
                            void* const* out_keys, uint32_t* const* out_vals, size_t out_cap,
                            size_t* n_out, uint64_t* splitters, uint64_t* counts,

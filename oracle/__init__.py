@@ -60,6 +60,10 @@ def lib():
         L.or_ger_u64.restype = i32
         L.or_ger_u32.argtypes = [i32, sz, u64, i32, vp, vp, vp, sz, vp, vp, vp]
         L.or_ger_u32.restype = i32
+        L.or_gvr_u64.argtypes = [i32, sz, u64, i32, vp, vp, vp, vp, vp, sz, vp, vp, vp]
+        L.or_gvr_u64.restype = i32
+        L.or_gvr_u32.argtypes = [i32, sz, u64, i32, vp, vp, vp, sz, vp, vp, vp]
+        L.or_gvr_u32.restype = i32
         L.or_splitmix64_at.argtypes = [u64, u64]
         L.or_splitmix64_at.restype = u64
         for name in ("or_is_nondecreasing_u32", "or_is_nondecreasing_u64"):
@@ -136,6 +140,12 @@ def ger(shards, s: int, seed: int, b: int = 8, vals=None, cap: int | None = None
     return _sample_sort(shards, 1, s, seed, b, vals, cap)
 
 
+def gvr(shards, s: int, seed: int, b: int = 8, vals=None, cap: int | None = None):
+    """Simulate GVR over p = len(shards) blocks: random sample
+    of the unsorted blocks, split by destination, local sort of each Y_j."""
+    return _sample_sort(shards, 2, s, seed, b, vals, cap)
+
+
 def splitmix64_at(seed: int, i: int) -> int:
     return int(lib().or_splitmix64_at(seed, i))
 
@@ -162,8 +172,9 @@ def _sample_sort(shards, mode, r_or_s, seed, b, vals, cap):
             rc = L.or_gsd_u32(p, r_or_s, b, kp, N.ctypes.data, yp, cap, ylen.ctypes.data,
                               spl.ctypes.data, counts.ctypes.data)
         else:
-            rc = L.or_ger_u32(p, r_or_s, seed, b, kp, N.ctypes.data, yp, cap, ylen.ctypes.data,
-                              spl.ctypes.data, counts.ctypes.data)
+            fn = L.or_ger_u32 if mode == 1 else L.or_gvr_u32
+            rc = fn(p, r_or_s, seed, b, kp, N.ctypes.data, yp, cap, ylen.ctypes.data,
+                    spl.ctypes.data, counts.ctypes.data)
     else:
         vp_ = None
         if vals is not None:
@@ -171,7 +182,7 @@ def _sample_sort(shards, mode, r_or_s, seed, b, vals, cap):
             Yv = [np.empty(max(cap, 1), dtype=np.uint32) for _ in range(p)]
             vp_ = (ctypes.c_void_p * p)(*[v.ctypes.data for v in vs])
             yvp = (ctypes.c_void_p * p)(*[y.ctypes.data for y in Yv])
-        fn = L.or_gsd_u64 if mode == 0 else L.or_ger_u64
+        fn = [L.or_gsd_u64, L.or_ger_u64, L.or_gvr_u64][mode]
         args = (p, r_or_s) if mode == 0 else (p, r_or_s, seed)
         rc = fn(*args, b, kp, vp_, N.ctypes.data, yp,
                 yvp if vals is not None else None, cap, ylen.ctypes.data,

@@ -194,6 +194,87 @@ done:
     return rc;
 }
 
+/*
+ * GVR(X, n, p): PAPER.md:988-1016 (Algorithm GVR), in its order:
+ *   1 SampleSelection  s·p − 1 keys drawn uniformly at random from the (unsorted)
+ *                      blocks X_k — the GER draws (R28) with positions in the
+ *                      unsorted X_k, composites (key, k, position) (R29); T = sort
+ *   2 SplitterSelect   S_i = T[i·s − 1], 1 ≤ i ≤ p−1
+ *   3 Split            each key's destination j = #{i : S_i <_c (x, k, q)} ("binary
+ *                      search of X_k into S"), then a count-sort of X_k by destination
+ *                      (stable) gives the unordered X_{k,j}; processor k sends X_{k,j}
+ *   4 LocalSorting     Y_j = X_{0,j} ‖ … ‖ X_{p−1,j} sorted by SR-b (stable), so equal
+ *                      keys keep (source rank, position) order (R16)
+ */
+static int gvr_u64(int p, size_t s, uint64_t seed, int b,
+                   const uint64_t* const* keys, const uint32_t* const* vals, const size_t* N,
+                   uint64_t* const* Y_keys, uint32_t* const* Y_vals, size_t Ycap, size_t* Ylen,
+                   uint64_t* splitters, uint64_t* counts) {
+    if (p < 1 || s < 1 || (b != 8 && b != 16)) return -1;
+    const size_t M = s * (size_t)p - 1;
+    composite_t* T = (composite_t*)malloc((M ? M : 1) * sizeof(composite_t));
+    composite_t* S = (composite_t*)malloc((size_t)p * sizeof(composite_t));
+    if (!T || !S) { free(T); free(S); return -1; }
+    size_t n = 0;
+    for (int k = 0; k < p; ++k) n += N[k];
+
+    /* Step 1: sample of the unsorted blocks (R28, R29), sorted as composites. */
+    for (size_t i = 0; i < M; ++i) {
+        composite_t c = { UINT64_MAX, 0, POS_INF };
+        if (n) {
+            const uint64_t q = (uint64_t)(((unsigned __int128)splitmix64_at(seed, i) * n) >> 64);
+            uint64_t off = 0;
+            for (int k = 0; k < p; ++k) {
+                if (q < off + N[k]) { c.key = keys[k][q - off]; c.rank = (uint64_t)k; c.pos = q - off; break; }
+                off += N[k];
+            }
+        }
+        T[i] = c;
+    }
+    qsort(T, M, sizeof(composite_t), comp_qsort);
+
+    /* Step 2: splitters. */
+    for (int i = 1; i < p; ++i) {
+        S[i] = T[(size_t)i * s - 1];
+        if (splitters) {
+            splitters[3 * (i - 1) + 0] = S[i].key;
+            splitters[3 * (i - 1) + 1] = S[i].rank;
+            splitters[3 * (i - 1) + 2] = S[i].pos;
+        }
+    }
+
+    /* Steps 3-4: destinations, X_{k,j} in source order, Y_j = concatenation sorted. */
+    int rc = 0;
+    for (int j = 0; j < p; ++j) Ylen[j] = 0;
+    for (int k = 0; k < p; ++k) {
+        for (int j = 0; j < p; ++j) if (counts) counts[(size_t)k * p + j] = 0;
+        for (size_t q = 0; q < N[k]; ++q) {
+            composite_t e = { keys[k][q], (uint64_t)k, q };
+            int j = 0;
+            for (int i = 1; i < p; ++i) if (comp_cmp(&S[i], &e) < 0) j = i;  /* S_i <_c e */
+            if (counts) counts[(size_t)k * p + j]++;
+            if (Ylen[j] < Ycap) {
+                Y_keys[j][Ylen[j]] = keys[k][q];
+                if (vals) Y_vals[j][Ylen[j]] = vals[k][q];
+            } else rc = -2;
+            Ylen[j]++;
+        }
+    }
+    for (int j = 0; j < p && rc == 0; ++j) {
+        if (vals) { if (or_sr_pairs_u64_u32(Y_keys[j], Y_vals[j], Ylen[j], b, -1)) rc = -1; }
+        else if (or_sr_u64(Y_keys[j], Ylen[j], b, -1)) rc = -1;
+    }
+    free(T); free(S);
+    return rc;
+}
+
+int or_gvr_u64(int p, size_t s, uint64_t seed, int b,
+               const uint64_t* const* keys, const uint32_t* const* vals, const size_t* N,
+               uint64_t* const* Y_keys, uint32_t* const* Y_vals, size_t Ycap, size_t* Ylen,
+               uint64_t* splitters, uint64_t* counts) {
+    return gvr_u64(p, s, seed, b, keys, vals, N, Y_keys, Y_vals, Ycap, Ylen, splitters, counts);
+}
+
 int or_gsd_u64(int p, int r, int b,
                const uint64_t* const* keys, const uint32_t* const* vals, const size_t* N,
                uint64_t* const* Y_keys, uint32_t* const* Y_vals, size_t Ycap, size_t* Ylen,
@@ -227,8 +308,10 @@ static int sample_sort_u32(int p, int mode, size_t s, uint64_t seed, int b,
         if (!K[k] || !Y[k]) rc = -1;
         else for (size_t i = 0; i < N[k]; ++i) K[k][i] = keys[k][i];
     }
-    if (!rc) rc = sample_sort_u64(p, mode, s, seed, b, (const uint64_t* const*)K, NULL, N, Y, NULL, Ycap, Ylen,
-                                  splitters, counts);
+    if (!rc) rc = mode == 2 ? gvr_u64(p, s, seed, b, (const uint64_t* const*)K, NULL, N, Y, NULL, Ycap, Ylen,
+                                      splitters, counts)
+                            : sample_sort_u64(p, mode, s, seed, b, (const uint64_t* const*)K, NULL, N, Y, NULL, Ycap,
+                                              Ylen, splitters, counts);
     if (rc == 0)
         for (int j = 0; j < p; ++j)
             for (size_t i = 0; i < Ylen[j]; ++i) Y_keys[j][i] = (uint32_t)Y[j][i];
@@ -250,4 +333,11 @@ int or_ger_u32(int p, size_t s, uint64_t seed, int b,
                uint32_t* const* Y_keys, size_t Ycap, size_t* Ylen,
                uint64_t* splitters, uint64_t* counts) {
     return sample_sort_u32(p, 1, s, seed, b, keys, N, Y_keys, Ycap, Ylen, splitters, counts);
+}
+
+int or_gvr_u32(int p, size_t s, uint64_t seed, int b,
+               const uint32_t* const* keys, const size_t* N,
+               uint32_t* const* Y_keys, size_t Ycap, size_t* Ylen,
+               uint64_t* splitters, uint64_t* counts) {
+    return sample_sort_u32(p, 2, s, seed, b, keys, N, Y_keys, Ycap, Ylen, splitters, counts);
 }

@@ -68,6 +68,16 @@ int or_ger_u32(int p, size_t s, uint64_t seed, int b,
                const uint32_t* const* keys, const size_t* N,
                uint32_t* const* Y_keys, size_t Ycap, size_t* Ylen,
                uint64_t* splitters, uint64_t* counts);
+/* GVR(X, n, p): random sample of the unsorted blocks (the GER
+ * draws), split by destination, exchange, then SR-b of each Y_j. */
+int or_gvr_u64(int p, size_t s, uint64_t seed, int b,
+               const uint64_t* const* keys, const uint32_t* const* vals, const size_t* N,
+               uint64_t* const* Y_keys, uint32_t* const* Y_vals, size_t Ycap, size_t* Ylen,
+               uint64_t* splitters, uint64_t* counts);
+int or_gvr_u32(int p, size_t s, uint64_t seed, int b,
+               const uint32_t* const* keys, const size_t* N,
+               uint32_t* const* Y_keys, size_t Ycap, size_t* Ylen,
+               uint64_t* splitters, uint64_t* counts);
 /* the i-th output of SplitMix64 seeded `seed` (the generator GER draws with) */
 uint64_t or_splitmix64_at(uint64_t seed, uint64_t i);
 

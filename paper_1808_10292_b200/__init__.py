@@ -204,9 +204,10 @@ class Comm:
         self.r = r
 
     def set_sampling(self, mode: str = "gsd", s: int = 0, seed: int = 0):
-        """"gsd" (regular oversampling, default) or "ger" (random oversampling
-        with s samples per rank, s = 0 the paper's choice, SplitMix64 seed)."""
-        m = {"gsd": 0, "ger": 1}[mode]
+        """"gsd" (regular oversampling, default), "ger" (random oversampling
+        with s samples per rank, s = 0 the paper's choice, SplitMix64 seed) or
+        "gvr" (the same sample, split before sorting)."""
+        m = {"gsd": 0, "ger": 1, "gvr": 2}[mode]
         check(lib().rs_comm_set_sampling(self.handle, m, s, seed), "rs_comm_set_sampling")
         self.sampling = mode
 
@@ -242,6 +243,13 @@ def ger_emulate(blocks: list[torch.Tensor], s: int = 0, seed: int = 0, digit_bit
     return _emulate(1, blocks, 1, s, seed, digit_bits, vals, out_cap, stream)
 
 
+def gvr_emulate(blocks: list[torch.Tensor], s: int = 0, seed: int = 0, digit_bits: int = 8,
+                vals: list[torch.Tensor] | None = None, out_cap: int | None = None, stream=None):
+    """GVR (split, exchange, then sort) over p = len(blocks)
+    ranks on this GPU; the blocks are used as scratch.  Same result dict."""
+    return _emulate(2, blocks, 1, s, seed, digit_bits, vals, out_cap, stream)
+
+
 def _emulate(mode, blocks, r, s, seed, digit_bits, vals, out_cap, stream):
     import numpy as np
     p = len(blocks)
@@ -259,7 +267,8 @@ def _emulate(mode, blocks, r, s, seed, digit_bits, vals, out_cap, stream):
     vouts = [torch.empty(max(cap, 1), dtype=torch.int32, device=dev) for _ in range(p)] if vals is not None else None
     vb = 4 if vals is not None else 0
     wsb = (lib().rs_gsd_emulate_ws_bytes(kb, vb, p, r, digit_bits, nmax, cap) if mode == 0
-           else lib().rs_ger_emulate_ws_bytes(kb, vb, p, s, digit_bits, nmax, cap))
+           else (lib().rs_ger_emulate_ws_bytes if mode == 1 else lib().rs_gvr_emulate_ws_bytes)(
+               kb, vb, p, s, digit_bits, nmax, cap))
     ws = _workspace(wsb, dev)
     arr = ctypes.c_void_p * p
     n_arr = (ctypes.c_size_t * p)(*n)
@@ -267,14 +276,14 @@ def _emulate(mode, blocks, r, s, seed, digit_bits, vals, out_cap, stream):
     spl = np.zeros((max(p - 1, 1), 3), dtype=np.uint64)
     counts = np.zeros((p, p), dtype=np.uint64)
     head = (kb, p, r) if mode == 0 else (kb, p, s, seed)
-    fn = lib().rs_gsd_emulate if mode == 0 else lib().rs_ger_emulate
+    fn = [lib().rs_gsd_emulate, lib().rs_ger_emulate, lib().rs_gvr_emulate][mode]
     check(fn(*head, digit_bits, arr(*[b.data_ptr() for b in blocks]),
              arr(*[v.data_ptr() for v in vals]) if vals is not None else None, n_arr,
              arr(*[o.data_ptr() for o in outs]),
              arr(*[o.data_ptr() for o in vouts]) if vals is not None else None, cap, n_out,
              spl.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
              counts.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ws.data_ptr(), ws.numel(),
-             _stream(stream)), "rs_gsd_emulate" if mode == 0 else "rs_ger_emulate")
+             _stream(stream)), ["rs_gsd_emulate", "rs_ger_emulate", "rs_gvr_emulate"][mode])
     return dict(Y=[outs[j][: n_out[j]] for j in range(p)],
                 Yv=[vouts[j][: n_out[j]] for j in range(p)] if vals is not None else None,
                 n_out=list(n_out), splitters=spl[: p - 1], counts=counts)

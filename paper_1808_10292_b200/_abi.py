@@ -37,6 +37,7 @@ SIGNATURES = {
     "rs_ger_default_s": (_sz, [ctypes.c_uint64]),
     "rs_ger_capacity": (_sz, [_sz, _i32, _sz]),
     "rs_ger_emulate_ws_bytes": (_sz, [_i32, _i32, _i32, _sz, _i32, _sz, _sz]),
+    "rs_gvr_emulate_ws_bytes": (_sz, [_i32, _i32, _i32, _sz, _i32, _sz, _sz]),
     "rs_comm_rank": (_i32, [_vp]),
     "rs_comm_size": (_i32, [_vp]),
     "rs_gsd_exchange_plan": (_i32, [_i32, _i32, _u64p, _u64p, _u64p, _u64p, _u64p]),
@@ -44,6 +45,8 @@ SIGNATURES = {
     "rs_gsd_emulate": (_i32, [_i32, _i32, _i32, _i32, _vpp, _vpp, _szp, _vpp, _vpp, _sz, _szp, _u64p, _u64p,
                               _vp, _sz, _vp]),
     "rs_ger_emulate": (_i32, [_i32, _i32, _sz, ctypes.c_uint64, _i32, _vpp, _vpp, _szp, _vpp, _vpp, _sz, _szp,
+                              _u64p, _u64p, _vp, _sz, _vp]),
+    "rs_gvr_emulate": (_i32, [_i32, _i32, _sz, ctypes.c_uint64, _i32, _vpp, _vpp, _szp, _vpp, _vpp, _sz, _szp,
                               _u64p, _u64p, _vp, _sz, _vp]),
     "rs_timing_enable": (None, [_i32]),
     "rs_timing_reset": (None, []),

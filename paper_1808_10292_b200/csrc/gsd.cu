@@ -24,6 +24,12 @@
 // sample everywhere, and two stable radix sorts of the (position, draw) and then
 // (key, draw) pairs order it by composite (key, rank, pos) — too large for the
 // one-CTA bitonic sort; S_i is the (i·s)-th smallest (k_ger_pick).
+//
+// GVR (Comm::sampling = 2) splits before it sorts: the same
+// random sample, drawn from the unsorted blocks; each key's destination by a
+// binary search of the composite splitters (k_gvr_dest); a stable count-sort by
+// destination (one radix-256 pass of (destination, index) pairs + a gather) gives
+// the X_{k,j}; after the exchange, Y_j is sorted by the local radix sort (SR4).
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -167,6 +173,43 @@ __global__ void k_ger_pick(const uint64_t* __restrict__ key, const uint64_t* __r
     S[j - 1] = Comp{key[e], (uint32_t)k, (uint32_t)(qe - off[k])};
 }
 
+// GVR step 3: destination of every key of the unsorted block, j = #{i : S_i <_c (x, rank, q)}
+template <typename K>
+__global__ void __launch_bounds__(256) k_gvr_dest(const K* __restrict__ X, size_t N, uint32_t rank,
+                                                  const Comp* __restrict__ S, int p, uint32_t* __restrict__ dest,
+                                                  uint32_t* __restrict__ idx, uint64_t* __restrict__ counts) {
+    __shared__ Comp sS[256];
+    __shared__ uint32_t sc[257];
+    for (int i = threadIdx.x; i < p - 1; i += blockDim.x) sS[i] = S[i];
+    for (int i = threadIdx.x; i < p; i += blockDim.x) sc[i] = 0;
+    __syncthreads();
+    for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < N; q += (size_t)gridDim.x * blockDim.x) {
+        const Comp e{static_cast<uint64_t>(X[q]), rank, (uint32_t)q};
+        int lo = 0, hi = p - 1;  // count of splitters <_c e (they are sorted)
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (comp_less(sS[mid], e)) lo = mid + 1;
+            else hi = mid;
+        }
+        dest[q] = (uint32_t)lo;
+        idx[q] = (uint32_t)q;
+        atomicAdd(&sc[lo], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < p; i += blockDim.x)
+        if (sc[i]) atomicAdd(reinterpret_cast<unsigned long long*>(&counts[i]), (unsigned long long)sc[i]);
+}
+
+template <typename K>
+__global__ void k_gvr_gather(const K* __restrict__ X, const uint32_t* __restrict__ V, const uint32_t* __restrict__ idx,
+                             size_t N, K* __restrict__ outK, uint32_t* __restrict__ outV) {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (size_t)gridDim.x * blockDim.x) {
+        const uint32_t j = idx[i];
+        outK[i] = X[j];
+        if (V) outV[i] = V[j];
+    }
+}
+
 size_t ger_default_s(uint64_t n_total) {
     // s = 2⌈ω⌉²⌈lg n⌉, ω = lg lg n  (reading R30)
     const double lg = n_total > 1 ? std::log2((double)n_total) : 1.0;
@@ -198,6 +241,12 @@ struct GsdLayout {
     uint64_t* ger_off;   // p + 1 block offsets
     void* ger_ws;        // radix workspace for M (u64, u32) pairs
     size_t ger_ws_bytes, ger_M;
+    // GVR: N = local keys
+    uint32_t *gv_dest, *gv_idx, *gv_sdest, *gv_sidx;  // N each
+    void* gv_keys;                                     // N keys partitioned by destination
+    uint32_t* gv_vals;                                 // N
+    void* gv_ws;                                       // radix workspace for N (u32, u32) pairs
+    size_t gv_ws_bytes;
     void* merge_keys;        // merge-tree scratch: cap keys (+ values)
     uint32_t* merge_vals;
     size_t* merge_split;
@@ -205,7 +254,7 @@ struct GsdLayout {
 };
 
 static GsdLayout gsd_layout(void* ws, int key_bytes, bool has_val, size_t n, size_t cap, int b, int p, int r,
-                            size_t recv_slots, size_t ger_M = 0) {
+                            size_t recv_slots, size_t ger_M = 0, bool gvr = false) {
     GsdLayout L{};
     Carver c(ws);
     const size_t s = (size_t)r * p;
@@ -236,6 +285,16 @@ static GsdLayout gsd_layout(void* ws, int key_bytes, bool has_val, size_t n, siz
         L.ger_ws_bytes = local_ws_bytes(8, true, ger_M, 8);
         L.ger_ws = c.take(L.ger_ws_bytes);
     }
+    if (gvr) {
+        L.gv_dest = static_cast<uint32_t*>(c.take(std::max<size_t>(n, 1) * 4));
+        L.gv_idx = static_cast<uint32_t*>(c.take(std::max<size_t>(n, 1) * 4));
+        L.gv_sdest = static_cast<uint32_t*>(c.take(std::max<size_t>(n, 1) * 4));
+        L.gv_sidx = static_cast<uint32_t*>(c.take(std::max<size_t>(n, 1) * 4));
+        L.gv_keys = c.take(std::max<size_t>(n, 1) * key_bytes);
+        L.gv_vals = static_cast<uint32_t*>(has_val ? c.take(std::max<size_t>(n, 1) * 4) : nullptr);
+        L.gv_ws_bytes = local_ws_bytes(4, true, n, 8);
+        L.gv_ws = c.take(L.gv_ws_bytes);
+    }
     L.bytes = c.used();
     return L;
 }
@@ -262,14 +321,14 @@ static size_t ger_capacity_for(size_t n_local_max, int p, size_t s) {
 static size_t ger_s_for(Comm* c, uint64_t n_total) { return c->ger_s ? c->ger_s : ger_default_s(n_total); }
 
 size_t gsd_capacity(Comm* c, size_t n_local_max) {
-    if (c->sampling == 1) return ger_capacity_for(n_local_max, c->nranks, ger_s_for(c, (uint64_t)n_local_max * c->nranks));
+    if (c->sampling >= 1) return ger_capacity_for(n_local_max, c->nranks, ger_s_for(c, (uint64_t)n_local_max * c->nranks));
     return capacity_for(n_local_max, c->r, c->nranks);
 }
 
 size_t gsd_ws_bytes(Comm* c, int key_bytes, bool has_val, size_t n_local_max, int b) {
     const size_t cap = gsd_capacity(c, n_local_max);
-    const size_t M = c->sampling == 1 ? ger_draws(ger_s_for(c, (uint64_t)n_local_max * c->nranks), c->nranks) : 0;
-    return gsd_layout(nullptr, key_bytes, has_val, n_local_max, cap, b, c->nranks, c->r, 1, M).bytes;
+    const size_t M = c->sampling >= 1 ? ger_draws(ger_s_for(c, (uint64_t)n_local_max * c->nranks), c->nranks) : 0;
+    return gsd_layout(nullptr, key_bytes, has_val, n_local_max, cap, b, c->nranks, c->r, 1, M, c->sampling == 2).bytes;
 }
 
 // GER steps 2b-3 on the assembled draws (L.ger_key, L.ger_q, M entries; offsets in
@@ -296,6 +355,35 @@ static rs_status_t ger_splitters(const GsdLayout& L, size_t M, size_t s, int p, 
     if (sst != RS_OK) return sst;
     LaunchScope ls("ger_sample", st);
     k_ger_pick<<<1, ((p + 31) / 32) * 32, 0, st>>>(L.ger_key, L.ger_q, L.ger_ib, s, p, L.ger_off, S);
+    return RS_OK;
+}
+
+// GVR step 3 on one rank's unsorted block: destinations, counts (added to
+// counts[0..p)), and the block partitioned by destination into L.gv_keys/gv_vals
+static rs_status_t gvr_partition(const GsdLayout& L, int key_bytes, const void* X, const uint32_t* V, size_t N,
+                                 int rank, int p, const Comp* S, uint64_t* counts, cudaStream_t st) {
+    if (!N) return RS_OK;
+    const int grid = (int)std::min<size_t>((N + 255) / 256, (size_t)sm_count() * 8);
+    {
+        LaunchScope ls("gvr_split", st);
+        if (key_bytes == 4)
+            k_gvr_dest<uint32_t><<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(X), N, (uint32_t)rank, S, p,
+                                                       L.gv_dest, L.gv_idx, counts);
+        else
+            k_gvr_dest<uint64_t><<<grid, 256, 0, st>>>(static_cast<const uint64_t*>(X), N, (uint32_t)rank, S, p,
+                                                       L.gv_dest, L.gv_idx, counts);
+    }
+    // stable count-sort by destination: one radix-256 pass (two for p > 256)
+    rs_status_t sst = local_sort(4, L.gv_dest, L.gv_idx, N, 8, p <= 256 ? 8 : 16, L.gv_sdest, L.gv_sidx, L.gv_ws,
+                                 L.gv_ws_bytes, st);
+    if (sst != RS_OK) return sst;
+    LaunchScope ls("gvr_split", st);
+    if (key_bytes == 4)
+        k_gvr_gather<uint32_t><<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(X), V, L.gv_sidx, N,
+                                                     static_cast<uint32_t*>(L.gv_keys), L.gv_vals);
+    else
+        k_gvr_gather<uint64_t><<<grid, 256, 0, st>>>(static_cast<const uint64_t*>(X), V, L.gv_sidx, N,
+                                                     static_cast<uint64_t*>(L.gv_keys), L.gv_vals);
     return RS_OK;
 }
 
@@ -373,7 +461,8 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
     const int p = c->nranks, rank = c->rank, r = c->r;
     const size_t s = (size_t)r * p;
     const bool hv = vals != nullptr;
-    const bool ger = c->sampling == 1;
+    const bool ger = c->sampling >= 1;          // random sample (GER or GVR)
+    const bool gvr = c->sampling == 2;          // split before sorting
     if (!ger && (size_t)p * s > (size_t)kMaxSample)
         return fail(RS_EINVAL, "r*p^2 exceeds the one-CTA sample sort limit of 8192");
     GsdLayout L = gsd_layout(ws, key_bytes, hv, n, out_cap, b, p, r, 1);  // GER region carved once n is known
@@ -383,8 +472,9 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
 
     // header all-gather: a mismatch is an error on every rank, not a hang
     uint64_t* h = c->h_pinned;
-    const uint64_t samp_id = ger ? (0x4745520000000000ull ^ (uint64_t)c->ger_s ^ (c->ger_seed * 0x9E3779B97F4A7C15ull))
-                                 : (uint64_t)r;
+    const uint64_t samp_id =
+        ger ? ((0x4745520000000000ull + (uint64_t)c->sampling) ^ (uint64_t)c->ger_s ^ (c->ger_seed * 0x9E3779B97F4A7C15ull))
+            : (uint64_t)r;
     uint64_t hdr[8] = {0x52534F5254ull, (uint64_t)key_bytes, (uint64_t)hv, (uint64_t)b, samp_id, (uint64_t)p,
                        (uint64_t)out_cap, (uint64_t)n};
     std::memcpy(h, hdr, sizeof(hdr));
@@ -407,16 +497,16 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
     if (ger) {
         ger_s = ger_s_for(c, n_total);
         M = ger_draws(ger_s, p);
-        L = gsd_layout(ws, key_bytes, hv, n, out_cap, b, p, r, 1, M);
+        L = gsd_layout(ws, key_bytes, hv, n, out_cap, b, p, r, 1, M, gvr);
         if (ws_bytes < L.bytes)
             return fail(RS_EINVAL, "GER workspace too small: need " + std::to_string(L.bytes) +
                                        " (size it with the largest local n)");
     }
 
-    // step 1: local sort in place -> X_k
-    rs_status_t sst = n ? local_sort(key_bytes, keys, vals, n, b, key_bytes * 8, keys, vals, L.local_ws,
-                                     L.local_ws_bytes, st)
-                        : RS_OK;
+    // step 1: local sort in place -> X_k  (GVR sorts last)
+    rs_status_t sst = (n && !gvr) ? local_sort(key_bytes, keys, vals, n, b, key_bytes * 8, keys, vals, L.local_ws,
+                                               L.local_ws_bytes, st)
+                                  : RS_OK;
     if (sst != RS_OK) return sst;
     if (ger && M) {
         // GER step 2: random sample assembled on every rank by a max all-reduce
@@ -439,7 +529,18 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
         if ((sst = launch_splitters(L.samp_all, (int)(p * s), (int)s, p, L.splitters, st)) != RS_OK) return sst;
     }
     // step 4: split + count exchange
-    if ((sst = launch_split(key_bytes, keys, n, rank, p, L.splitters, L.counts_local, st)) != RS_OK) return sst;
+    if (gvr) {
+        RS_CUDA_TRY(cudaMemsetAsync(L.counts_local, 0, (size_t)p * 8, st));
+        if (p > 1) {
+            if ((sst = gvr_partition(L, key_bytes, keys, vals, n, rank, p, L.splitters, L.counts_local, st)) != RS_OK)
+                return sst;
+        } else {
+            h[0] = n;
+            RS_CUDA_TRY(cudaMemcpyAsync(L.counts_local, h, 8, cudaMemcpyHostToDevice, st));
+        }
+    } else if ((sst = launch_split(key_bytes, keys, n, rank, p, L.splitters, L.counts_local, st)) != RS_OK) {
+        return sst;
+    }
     RS_NCCL_TRY(ncclAllGather(L.counts_local, L.counts_all, p, ncclUint64, c->nccl, st));
     RS_CUDA_TRY(cudaMemcpyAsync(h, L.counts_all, (size_t)p * p * 8, cudaMemcpyDeviceToHost, st));
     RS_CUDA_TRY(cudaStreamSynchronize(st));
@@ -449,7 +550,8 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
     if ((sst = rs_gsd_exchange_plan(p, rank, cnt.data(), caps.data(), soff.data(), roff.data(), &total)) != RS_OK)
         return sst;
     // exchange X_{k,j}: grouped send/recv; the self slice is a device copy
-    char* kx = static_cast<char*>(keys);
+    char* kx = static_cast<char*>(gvr && p > 1 ? L.gv_keys : keys);
+    if (gvr && p > 1) vals = L.gv_vals;
     char* rk = static_cast<char*>(L.recv_keys);
     {
         LaunchScope ls("gsd_exchange", st, false);
@@ -476,8 +578,14 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
                                             cudaMemcpyDeviceToDevice, st));
         }
     }
-    // step 5: merge
-    if ((sst = merge_runs(key_bytes, L.recv_keys, L.recv_vals, roff, b, out, vout, L, st)) != RS_OK) return sst;
+    // step 5: merge (GVR: local sort of the received concatenation)
+    if (gvr) {
+        if (total && (sst = local_sort(key_bytes, L.recv_keys, L.recv_vals, total, b, key_bytes * 8, out, vout,
+                                       L.local_ws, L.local_ws_bytes, st)) != RS_OK)
+            return sst;
+    } else if ((sst = merge_runs(key_bytes, L.recv_keys, L.recv_vals, roff, b, out, vout, L, st)) != RS_OK) {
+        return sst;
+    }
     if (n_out) *n_out = total;
     RS_CUDA_TRY(cudaGetLastError());
     return RS_OK;
@@ -592,16 +700,16 @@ static rs_status_t emulate(int mode, int key_bytes, int p, int r, size_t ger_s, 
         noff[k + 1] = noff[k] + n[k];
     }
     const uint64_t n_total = noff[p];
-    const size_t gs = mode == 1 ? (ger_s ? ger_s : ger_default_s(n_total)) : 0;
-    const size_t M = mode == 1 ? ger_draws(gs, p) : 0;
-    const GsdLayout L = gsd_layout(ws, key_bytes, hv, n_max, out_cap, digit_bits, p, r, 1, M);
+    const size_t gs = mode >= 1 ? (ger_s ? ger_s : ger_default_s(n_total)) : 0;
+    const size_t M = mode >= 1 ? ger_draws(gs, p) : 0;
+    const GsdLayout L = gsd_layout(ws, key_bytes, hv, n_max, out_cap, digit_bits, p, r, 1, M, mode == 2);
     if (!ws || ws_bytes < L.bytes) return fail(RS_EINVAL, "emulate workspace too small: need " + std::to_string(L.bytes));
     rs_status_t sst;
-    for (int k = 0; k < p; ++k)  // step 1
+    for (int k = 0; k < p && mode != 2; ++k)  // step 1 (GVR sorts last)
         if (n[k] && (sst = local_sort(key_bytes, keys[k], hv ? vals[k] : nullptr, n[k], digit_bits, key_bytes * 8,
                                       keys[k], hv ? vals[k] : nullptr, L.local_ws, L.local_ws_bytes, st)) != RS_OK)
             return sst;
-    if (mode == 1) {  // GER steps 2-3: the draws of every rank into one array (= the all-reduce)
+    if (mode >= 1) {  // GER/GVR steps 2-3: the draws of every rank into one array (= the all-reduce)
         if (M) {
             RS_CUDA_TRY(cudaMemcpyAsync(L.ger_off, noff.data(), (p + 1) * 8, cudaMemcpyHostToDevice, st));
             RS_CUDA_TRY(cudaMemsetAsync(L.ger_key, 0, M * 8, st));
@@ -618,10 +726,29 @@ static rs_status_t emulate(int mode, int key_bytes, int p, int r, size_t ger_s, 
             return sst;
     if ((sst = launch_splitters(L.samp_all, (int)(p * s), (int)s, p, L.splitters, st)) != RS_OK) return sst;
     }
-    for (int k = 0; k < p; ++k)  // step 4
-        if ((sst = launch_split(key_bytes, keys[k], n[k], k, p, L.splitters, L.counts_all + (size_t)k * p, st)) !=
-            RS_OK)
-            return sst;
+    if (mode == 2) {  // GVR step 3: partition each block by destination (in place: the blocks are scratch)
+        RS_CUDA_TRY(cudaMemsetAsync(L.counts_all, 0, (size_t)p * p * 8, st));
+        for (int k = 0; k < p; ++k) {
+            if (p == 1) {
+                std::vector<uint64_t> one(1, n[k]);
+                RS_CUDA_TRY(cudaMemcpyAsync(L.counts_all, one.data(), 8, cudaMemcpyHostToDevice, st));
+                RS_CUDA_TRY(cudaStreamSynchronize(st));
+                break;
+            }
+            if ((sst = gvr_partition(L, key_bytes, keys[k], hv ? vals[k] : nullptr, n[k], k, p, L.splitters,
+                                     L.counts_all + (size_t)k * p, st)) != RS_OK)
+                return sst;
+            if (n[k]) {
+                RS_CUDA_TRY(cudaMemcpyAsync(keys[k], L.gv_keys, n[k] * key_bytes, cudaMemcpyDeviceToDevice, st));
+                if (hv) RS_CUDA_TRY(cudaMemcpyAsync(vals[k], L.gv_vals, n[k] * 4, cudaMemcpyDeviceToDevice, st));
+            }
+        }
+    } else {
+        for (int k = 0; k < p; ++k)  // step 4
+            if ((sst = launch_split(key_bytes, keys[k], n[k], k, p, L.splitters, L.counts_all + (size_t)k * p,
+                                    st)) != RS_OK)
+                return sst;
+    }
     std::vector<uint64_t> cnt((size_t)p * p);
     std::vector<Comp> spl(std::max(1, p - 1));
     RS_CUDA_TRY(cudaMemcpyAsync(cnt.data(), L.counts_all, cnt.size() * 8, cudaMemcpyDeviceToHost, st));
@@ -669,9 +796,15 @@ static rs_status_t emulate(int mode, int key_bytes, int p, int r, size_t ger_s, 
                 roff.push_back(off);
             }
         }
-        if ((sst = merge_runs(key_bytes, L.recv_keys, L.recv_vals, roff, digit_bits, out_keys[j],
-                              hv ? out_vals[j] : nullptr, L, st)) != RS_OK)
+        if (mode == 2) {  // GVR step 4: local sort of the received concatenation
+            if (off && (sst = local_sort(key_bytes, L.recv_keys, L.recv_vals, off, digit_bits, key_bytes * 8,
+                                         out_keys[j], hv ? out_vals[j] : nullptr, L.local_ws, L.local_ws_bytes,
+                                         st)) != RS_OK)
+                return sst;
+        } else if ((sst = merge_runs(key_bytes, L.recv_keys, L.recv_vals, roff, digit_bits, out_keys[j],
+                                     hv ? out_vals[j] : nullptr, L, st)) != RS_OK) {
             return sst;
+        }
     }
     RS_CUDA_TRY(cudaGetLastError());
     return RS_OK;
@@ -709,6 +842,22 @@ rs_status_t rs_ger_emulate(int key_bytes, int p, size_t s, uint64_t seed, int di
                    splitters, counts, ws, ws_bytes, static_cast<cudaStream_t>(stream));
 }
 
+size_t rs_gvr_emulate_ws_bytes(int key_bytes, int val_bytes, int p, size_t s, int digit_bits, size_t n_max,
+                               size_t out_cap) {
+    if (p < 1) return 0;
+    const size_t gs = s ? s : ger_default_s((uint64_t)n_max * p);
+    return gsd_layout(nullptr, key_bytes, val_bytes != 0, n_max, out_cap, digit_bits, p, 1, 1, ger_draws(gs, p), true)
+        .bytes;
+}
+
+rs_status_t rs_gvr_emulate(int key_bytes, int p, size_t s, uint64_t seed, int digit_bits, void* const* keys,
+                           uint32_t* const* vals, const size_t* n, void* const* out_keys, uint32_t* const* out_vals,
+                           size_t out_cap, size_t* n_out, uint64_t* splitters, uint64_t* counts, void* ws,
+                           size_t ws_bytes, void* stream) {
+    return emulate(2, key_bytes, p, 1, s, seed, digit_bits, keys, vals, n, out_keys, out_vals, out_cap, n_out,
+                   splitters, counts, ws, ws_bytes, static_cast<cudaStream_t>(stream));
+}
+
 size_t rs_ger_capacity(size_t n_local_max, int p, size_t s) {
     if (p < 1) return 0;
     return ger_capacity_for(n_local_max, p, s ? s : ger_default_s((uint64_t)n_local_max * p));
@@ -717,7 +866,7 @@ size_t rs_ger_capacity(size_t n_local_max, int p, size_t s) {
 size_t rs_ger_default_s(uint64_t n_total) { return ger_default_s(n_total); }
 
 rs_status_t rs_comm_set_sampling(void* comm, int mode, size_t s, uint64_t seed) {
-    if (!comm || (mode != 0 && mode != 1)) return fail(RS_EINVAL, "bad comm / sampling mode");
+    if (!comm || mode < 0 || mode > 2) return fail(RS_EINVAL, "bad comm / sampling mode");
     Comm* c = static_cast<Comm*>(comm);
     c->sampling = mode;
     c->ger_s = s;

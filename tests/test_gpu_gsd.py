@@ -172,3 +172,52 @@ def test_ger_uneven_empty_blocks_and_u64():
     _check_ger([a[:0], a[:5000], a[5000:5003], a[5003:]], s=6, seed=4)
     k = inputs.gen_u64(30001, 92)
     _check_ger([k[:12000], k[12000:12001], k[12001:]], s=0, seed=5)
+
+
+# ---------------------------------------------------------------- GVR ----
+def _check_gvr(blocks_np, s, seed, b=8, vals_np=None):
+    p = len(blocks_np)
+    dt = blocks_np[0].dtype
+    want = oracle.gvr(blocks_np, s=s if s else _default_s(sum(x.size for x in blocks_np)), seed=seed, b=b,
+                      vals=vals_np)
+    got = rs.gvr_emulate([dev(x) for x in blocks_np], s=s, seed=seed, digit_bits=b,
+                         vals=[dev(v) for v in vals_np] if vals_np is not None else None)
+    assert got["counts"].tolist() == want["counts"].tolist()
+    assert got["splitters"].tolist() == want["splitters"].tolist()
+    for j in range(p):
+        assert (host(got["Y"][j], dt) == want["Y"][j]).all(), j
+        if vals_np is not None:
+            assert (host(got["Yv"][j], np.uint32) == want["Yv"][j]).all(), j
+    return got
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 5, 8])
+@pytest.mark.parametrize("dist", ["uniform", "mod16", "equal", "sorted"])
+def test_gvr_u32_matches_simulator(p, dist):
+    """GVR: sample of the unsorted blocks, destinations by
+    binary search of the composite splitters, stable count-sort by destination,
+    exchange, local radix sort: bit-exact against the CPU simulator."""
+    total = 50000 + 5 * p
+    a = inputs.gen_u32(total, 100 + p, dist)
+    cuts = np.linspace(0, total, p + 1).astype(int)
+    _check_gvr([a[cuts[k]:cuts[k + 1]] for k in range(p)], s=0, seed=21 + p)
+    _check_gvr([a[cuts[k]:cuts[k + 1]] for k in range(p)], s=9, seed=8)
+
+
+@pytest.mark.parametrize("b", [8, 16])
+def test_gvr_pairs_global_stability_and_u64(b):
+    p, N = 4, 20000
+    k = inputs.gen_u64(p * N, 7, "mod1024")
+    v = inputs.iota_u32(p * N)
+    got = _check_gvr([k[i * N:(i + 1) * N] for i in range(p)], s=0, seed=3, b=b,
+                     vals_np=[v[i * N:(i + 1) * N] for i in range(p)])
+    K = np.concatenate([host(y, np.uint64) for y in got["Y"]])
+    V = np.concatenate([host(y, np.uint32) for y in got["Yv"]])
+    assert oracle.pairs_stable(K, V)
+    u = inputs.gen_u64(30001, 93)
+    _check_gvr([u[:12000], u[12000:12001], u[12001:]], s=0, seed=6, b=b)
+
+
+def test_gvr_uneven_and_empty_blocks():
+    a = inputs.gen_u32(9000, 94)
+    _check_gvr([a[:0], a[:5000], a[5000:5003], a[5003:]], s=6, seed=4)

@@ -76,3 +76,15 @@ def test_ger_p1_through_nccl(comm):
         assert (host(y, np.uint32) == oracle.sr(a, 8)).all()
     finally:
         comm.set_sampling("gsd")
+
+
+def test_gvr_p1_through_nccl(comm):
+    comm.set_sampling("gvr", s=0, seed=4)
+    try:
+        k = inputs.gen_u64(40001, 63, "mod1024")
+        v = inputs.iota_u32(k.size)
+        yk, yv = rs.sort_pairs(dev(k), dev(v), comm=comm)
+        wk, wv = oracle.sr(k, 8, vals=v)
+        assert (host(yk, np.uint64) == wk).all() and (host(yv, np.uint32) == wv).all()
+    finally:
+        comm.set_sampling("gsd")

@@ -131,3 +131,61 @@ def oracle_default_s(n):
     lg = math.log2(n)
     w = max(1, math.ceil(math.log2(lg)))
     return int(2 * w * w * math.ceil(lg))
+
+
+# ---------------------------------------------------------------- GVR ----
+def _gvr_definition(blocks, s, seed):
+    """Steps 1-2 of Algorithm GVR from the definition: draws over the UNSORTED blocks."""
+    off = np.concatenate([[0], np.cumsum([b.size for b in blocks])]).astype(object)
+    n = int(off[-1])
+    p = len(blocks)
+    T = []
+    for i in range(s * p - 1):
+        q = (_splitmix_py(seed, i) * n) >> 64
+        k = max(kk for kk in range(p) if blocks[kk].size > 0 and off[kk] <= q < off[kk] + blocks[kk].size)
+        T.append((int(blocks[k][q - off[k]]), k, int(q - off[k])))
+    T.sort()
+    return [T[i * s - 1] for i in range(1, p)]
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 8])
+@pytest.mark.parametrize("dist", ["uniform", "mod16", "equal", "sorted"])
+def test_gvr_splitters_destinations_and_result(p, dist):
+    """GVR: splitters from the definition over the unsorted
+    blocks; X_{k,j} = keys of X_k whose composite (x, k, q) lies in (S_{j-1}, S_j],
+    counted element by element; Y = sorted input."""
+    rng = np.random.default_rng(p)
+    sizes = [int(x) for x in rng.integers(40, 300, p)]
+    s, seed = 6, 500 + p
+    a, blocks = _blocks(sizes, 90 + p, dist)
+    res = oracle.gvr(blocks, s=s, seed=seed)
+    S = _gvr_definition(blocks, s, seed)
+    assert [tuple(int(v) for v in row) for row in res["splitters"]] == S
+    for k in range(p):
+        dest = [sum(1 for sp in S if sp < (int(x), k, q)) for q, x in enumerate(blocks[k])]
+        assert [dest.count(j) for j in range(p)] == res["counts"][k].tolist(), k
+    assert (np.concatenate(res["Y"]) == np.sort(a)).all()
+
+
+def test_gvr_pairs_globally_stable_and_same_result_as_gsd():
+    p, N = 4, 1000
+    k = inputs.gen_u64(p * N, 12, "mod1024") & np.uint64(7)
+    v = inputs.iota_u32(p * N)
+    sh = [k[i * N:(i + 1) * N] for i in range(p)]
+    vs = [v[i * N:(i + 1) * N] for i in range(p)]
+    r1 = oracle.gvr(sh, s=11, seed=2, vals=vs)
+    r0 = oracle.gsd(sh, r=8, vals=vs)
+    order = np.lexsort((v, k))
+    assert (np.concatenate(r1["Y"]) == k[order]).all() and (np.concatenate(r1["Yv"]) == v[order]).all()
+    assert (np.concatenate(r1["Yv"]) == np.concatenate(r0["Yv"])).all()   # the sort is unique
+
+
+def test_gvr_sampling_lemma_bound_over_seeds():
+    p, n = 8, 40000
+    s = oracle_default_s(n)
+    eps = _lemma_eps(n, p, s)
+    bound = math.ceil((1 + eps) * (n - p + 1) / p)
+    a = np.random.default_rng(1).permutation(n).astype(np.uint32)
+    blocks = [a[k * n // p:(k + 1) * n // p] for k in range(p)]
+    worst = max(int(oracle.gvr(blocks, s=s, seed=seed)["Ylen"].max()) - s for seed in range(40))
+    assert worst <= bound, (worst, bound)
