@@ -41,6 +41,13 @@
 #ifndef RS_AR_CT16
 #define RS_AR_CT16 1
 #endif
+// RANK2: [rank] only counts (atomics without return); after [offset] has turned
+// the counters into warp start offsets, [scatter] takes each key's slot from a
+// second returning atomic (start + stable rank, lane-ordered as in [rank]) — no
+// rank registers and no counter load in the scatter
+#ifndef RS_AR_RANK2
+#define RS_AR_RANK2 0
+#endif
 
 namespace rs {
 
@@ -148,7 +155,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
     static_assert(KPT % 2 == 0 && WK <= 65536, "ranks are packed two per register");
     constexpr int G = KPT % 8 == 0 ? 8 : (KPT % 6 == 0 ? 6 : (KPT % 4 == 0 ? 4 : 2));  // batch of keys
     K kr[KREG ? KPT : 2];  // this thread's keys of the tile (rows j, lane)
-    uint32_t rr[KPT / 2];  // their stable ranks within the warp's keys of the same digit, 16 bits each
+    uint32_t rr[RS_AR_RANK2 ? 1 : KPT / 2];  // stable ranks within the warp's keys of their digit, 16 bits each
 
     while (tile < a.num_tiles) {
         const size_t base = (size_t)tile * TILE;
@@ -203,15 +210,21 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                 for (int i = 0; i < G; ++i) {
                     if (KREG && KSRC == 0) kr[KREG ? g + i : 0] = kk[i];
                     const uint32_t d = digit8<K>(kk[i], shift);
-                    if (RS_AR_CT16) {
+                    if (RS_AR_RANK2) {
+                        atomicAdd(&wc[RS_AR_CT16 ? d >> 1 : d], RS_AR_CT16 ? 1u << ((d & 1u) << 4) : 1u);
+                        rg[i] = 0;
+                    } else if (RS_AR_CT16) {
                         const uint32_t sh = (d & 1u) << 4;
                         rg[i] = atomicAdd(&wc[d >> 1], 1u << sh) >> sh;  // high bits cleared at packing
                     } else {
                         rg[i] = atomicAdd(&wc[d], 1u);
                     }
                 }
+                if (!RS_AR_RANK2) {
 #pragma unroll
-                for (int i = 0; i < G; i += 2) rr[(g + i) / 2] = __byte_perm(rg[i], rg[i + 1], 0x5410);
+                    for (int i = 0; i < G; i += 2)
+                        rr[RS_AR_RANK2 ? 0 : (g + i) / 2] = __byte_perm(rg[i], rg[i + 1], 0x5410);
+                }
             }
         }
         __syncthreads();
@@ -252,7 +265,8 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
 
         // ---- [scatter] each key to its stable slot of the tile sorted by digit
         {
-            const uint32_t* wc = s_wc + warp * R;
+            uint32_t* wc = s_wc + warp * R;
+            uint32_t* wcp = s_wc + warp * (WCW / W);  // packed counters (RANK2 with CT16)
             const uint16_t* wc16 = s_wc16 + warp * R;
             const int ibase = warp * WK + lane;
             // groups of G keys: G key loads, G offset loads, then G stores
@@ -269,7 +283,17 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                 for (int i = 0; i < G; ++i) {
                     const int j = g + i;
                     const uint32_t d = digit8<K>(kk[i], shift);
-                    pos[i] = (RS_AR_CT16 ? (uint32_t)wc16[d] : wc[d]) + ((rr[j / 2] >> (16 * (j & 1))) & 0xFFFFu);
+                    if (RS_AR_RANK2) {
+                        if (RS_AR_CT16) {
+                            const uint32_t sh = (d & 1u) << 4;
+                            pos[i] = (atomicAdd(&wcp[d >> 1], 1u << sh) >> sh) & 0xFFFFu;
+                        } else {
+                            pos[i] = atomicAdd(&wc[d], 1u);
+                        }
+                    } else {
+                        pos[i] = (RS_AR_CT16 ? (uint32_t)wc16[d] : wc[d]) +
+                                 ((rr[RS_AR_RANK2 ? 0 : j / 2] >> (16 * (j & 1))) & 0xFFFFu);
+                    }
                     if (HAS_VAL) vv[HAS_VAL ? i : 0] = s_vin[ibase + j * 32];
                 }
 #pragma unroll
