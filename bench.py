@@ -181,6 +181,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sampling", default="gsd", choices=["gsd", "ger", "gvr"],
+                    help="N > 1: sample sort of the paper's §3.3 (GSD regular oversampling r=8, default; "
+                         "GER / GVR random oversampling with the paper's s)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -222,6 +225,7 @@ def main():
     comm = rs.Comm() if p > 1 else None
     if comm is not None:
         comm.set_oversampling(8)
+        comm.set_sampling(args.sampling, s=0, seed=seed)
         cap = comm.capacity(n)
         out = torch.empty(cap, dtype=work.dtype, device=dev)
         vout = torch.empty(cap, dtype=torch.int32, device=dev) if kind == "pairs" else None
@@ -377,7 +381,8 @@ def main():
         "dtype": "u32" if kind == "u32" else "u64+u32", "data": "synthetic",
         "config": {"workload": args.config, "description": desc, "n": n_total, "keys_per_gpu": n,
                    "digit_bits": b, "seed": seed, "dist": dist_name,
-                   "parallelism": f"gsd-p{p} (r=8)" if p > 1 else "single GPU",
+                   "parallelism": (f"gsd-p{p} (r=8)" if args.sampling == "gsd" else f"{args.sampling}-p{p} (paper's s)")
+                   if p > 1 else "single GPU",
                    "l2": "inputs larger than L2 (no flush)", "inputs": "resident in HBM, reset outside timed region"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clocks, "kernel_ms_per_step": round(all_kernels_ms / args.steps, 4),
