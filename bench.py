@@ -115,6 +115,29 @@ def host_info():
     return info
 
 
+def bind_gpu_local_cpus(device_index: int):
+    """Run on the host CPUs of the GPU's NUMA node (sysfs local_cpulist of its PCI
+    device), so pinned host buffers are first-touched on that node and the e2e
+    copies do not cross the socket interconnect.  Best effort; returns the CPU list."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        bus = pynvml.nvmlDeviceGetPciInfo(pynvml.nvmlDeviceGetHandleByIndex(device_index)).busId
+        bus = (bus.decode() if isinstance(bus, bytes) else bus).lower()
+        dom, rest = bus.split(":", 1)
+        path = f"/sys/bus/pci/devices/{dom[-4:]}:{rest}/local_cpulist"
+        cpus = set()
+        for part in open(path).read().strip().split(","):
+            lo, _, hi = part.partition("-")
+            cpus.update(range(int(lo), int(hi or lo) + 1))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return sorted(cpus)
+    except Exception:
+        pass
+    return None
+
+
 def oracle_baseline(kind, seed, dist, b, target_s=10.0):
     """The serial C oracle (SR-b) as it stands, on a bounded
     sample of the workload's stream, one host core, until >= target_s elapsed."""
@@ -200,6 +223,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    local_cpus = bind_gpu_local_cpus(torch.cuda.current_device())
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     kind, n_total, seed, dist_name, b, desc = CONFIGS[args.config]
@@ -286,6 +310,26 @@ def main():
     pass_ms = ms_q.value / max(cnt_q.value, 1)
     L.rs_timing_query(b"", ctypes.byref(ms_q), ctypes.byref(cnt_q))
     all_kernels_ms = ms_q.value
+    # GSD all-to-all (N > 1): bytes that cross NVLink from the count matrix, time of
+    # the grouped send/recv from events on the sort stream (max over ranks below)
+    xchg = None
+    if p > 1:
+        L.rs_timing_query(b"gsd_exchange", ctypes.byref(ms_q), ctypes.byref(cnt_q))
+        x_ms = ms_q.value / max(cnt_q.value, 1)
+        cm = comm.last_counts().astype(np.float64)
+        w = KEY_BYTES[kind] + (4 if kind == "pairs" else 0)
+        sent = (cm[rank].sum() - cm[rank, rank]) * w
+        recv = (cm[:, rank].sum() - cm[rank, rank]) * w
+        t = torch.tensor([x_ms, max(sent, recv)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        x_ms, x_bytes = float(t[0]), float(t[1])
+        nvl_peak = 770.0
+        ach = x_bytes / (x_ms / 1e3) / 1e9 if x_ms > 0 else None
+        xchg = {"kernel": "grouped ncclSend/ncclRecv all-to-all (GSD step 4)", "bound": "nvlink",
+                "bytes_max_rank": int(x_bytes), "ms": round(x_ms, 4),
+                "achieved": round(ach, 1) if ach else None, "peak": nvl_peak, "unit": "GB/s",
+                "frac": round(ach / nvl_peak, 4) if ach else None,
+                "peak_source": "measured peer copy per direction (B200_PROFILING.md; 900 GB/s nominal)"}
     total_ms = sum(step_ms)
     if p > 1:
         t = torch.tensor([total_ms, pass_ms], dtype=torch.float64, device=dev)
@@ -340,6 +384,7 @@ def main():
         e2e = {"value": round(n_total / (e_ms / 1e3) / 1e9, 4), "unit": "Gkeys/s",
                "h2d_bytes_per_step": n * (kb + (4 if kind == "pairs" else 0)), "d2h_bytes_per_step": n * kb,
                "ms_per_step": round(e_ms, 3), "steps": args.e2e_steps, "slots": nslot,
+               "host_cpus": f"{len(local_cpus)} GPU-local CPUs" if local_cpus else "unbound",
                "note": "host clock over the steps: pinned H2D of the inputs + sort + D2H of the sorted keys "
                        "every step; steps pipelined over two streams on one GPU (max over ranks)"}
 
@@ -385,6 +430,7 @@ def main():
                    if p > 1 else "single GPU",
                    "l2": "inputs larger than L2 (no flush)", "inputs": "resident in HBM, reset outside timed region"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        **({"nvlink_roofline": xchg} if xchg else {}),
         "clocks": clocks, "kernel_ms_per_step": round(all_kernels_ms / args.steps, 4),
     }
     print(json.dumps(line))

@@ -146,6 +146,10 @@ rs_status_t rs_comm_set_sampling(void* comm, int mode, size_t s, uint64_t seed);
  * largest block of n_local_max keys over p ranks (s = 0: the default s). */
 size_t rs_ger_default_s(uint64_t n_total);
 size_t rs_ger_capacity(size_t n_local_max, int p, size_t s);
+/* The p×p count matrix |X_{k,j}| (row k = sender) of the last sample sort on
+ * this communicator, into host u64[p*p]; RS_EINVAL before the first sort.
+ * (bench.py derives the all-to-all bytes from it.) */
+rs_status_t rs_comm_last_counts(void* comm, uint64_t* counts);
 int rs_comm_rank(void* comm);
 int rs_comm_size(void* comm);
 

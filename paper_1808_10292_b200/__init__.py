@@ -211,6 +211,14 @@ class Comm:
         check(lib().rs_comm_set_sampling(self.handle, m, s, seed), "rs_comm_set_sampling")
         self.sampling = mode
 
+    def last_counts(self):
+        """(p, p) uint64 count matrix |X_{k,j}| of the last sort on this communicator."""
+        import numpy as np
+        c = np.zeros((self.size, self.size), dtype=np.uint64)
+        check(lib().rs_comm_last_counts(self.handle, c.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))),
+              "rs_comm_last_counts")
+        return c
+
     def capacity(self, n_local: int) -> int:
         return lib().rs_output_capacity(self.ws_n(n_local), self.handle)
 

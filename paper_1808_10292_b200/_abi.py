@@ -34,6 +34,7 @@ SIGNATURES = {
     "rs_comm_destroy": (_i32, [_vp]),
     "rs_comm_set_oversampling": (_i32, [_vp, _i32]),
     "rs_comm_set_sampling": (_i32, [_vp, _i32, _sz, ctypes.c_uint64]),
+    "rs_comm_last_counts": (_i32, [_vp, _u64p]),
     "rs_ger_default_s": (_sz, [ctypes.c_uint64]),
     "rs_ger_capacity": (_sz, [_sz, _i32, _sz]),
     "rs_ger_emulate_ws_bytes": (_sz, [_i32, _i32, _i32, _sz, _i32, _sz, _sz]),

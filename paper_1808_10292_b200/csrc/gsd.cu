@@ -545,6 +545,7 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
     RS_CUDA_TRY(cudaMemcpyAsync(h, L.counts_all, (size_t)p * p * 8, cudaMemcpyDeviceToHost, st));
     RS_CUDA_TRY(cudaStreamSynchronize(st));
     std::vector<uint64_t> cnt(h, h + (size_t)p * p);
+    c->last_counts = cnt;
     std::vector<uint64_t> soff(p + 1, 0), roff(p + 1, 0);
     uint64_t total = 0;
     if ((sst = rs_gsd_exchange_plan(p, rank, cnt.data(), caps.data(), soff.data(), roff.data(), &total)) != RS_OK)
@@ -668,6 +669,14 @@ rs_status_t rs_comm_destroy(void* comm) {
 rs_status_t rs_comm_set_oversampling(void* comm, int r) {
     if (!comm || r < 1) return fail(RS_EINVAL, "bad comm / r");
     static_cast<Comm*>(comm)->r = r;
+    return RS_OK;
+}
+
+rs_status_t rs_comm_last_counts(void* comm, uint64_t* counts) {
+    if (!comm || !counts) return fail(RS_EINVAL, "NULL comm / counts");
+    const Comm* c = static_cast<Comm*>(comm);
+    if (c->last_counts.empty()) return fail(RS_EINVAL, "no sample sort has run on this communicator");
+    std::memcpy(counts, c->last_counts.data(), c->last_counts.size() * 8);
     return RS_OK;
 }
 

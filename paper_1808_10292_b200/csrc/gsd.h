@@ -5,6 +5,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 
 #include "runtime.h"
 
@@ -19,6 +20,7 @@ struct Comm {
     uint64_t ger_seed = 0;         // GER: SplitMix64 seed of the sample draws
     uint64_t* h_pinned = nullptr;  // p*p counts + headers (pinned host)
     size_t h_pinned_words = 0;
+    std::vector<uint64_t> last_counts;  // p×p count matrix of the last sort (rs_comm_last_counts)
 };
 
 // composite key (key, rank, pos): the unique total order used for sampling

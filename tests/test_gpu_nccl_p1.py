@@ -88,3 +88,9 @@ def test_gvr_p1_through_nccl(comm):
         assert (host(yk, np.uint64) == wk).all() and (host(yv, np.uint32) == wv).all()
     finally:
         comm.set_sampling("gsd")
+
+
+def test_last_counts_after_a_sort(comm):
+    a = inputs.gen_u32(12345, 64)
+    rs.sort(dev(a), comm=comm)
+    assert comm.last_counts().tolist() == [[12345]]
