@@ -18,8 +18,11 @@
 
 namespace rs {
 
-constexpr int kMT = 256;     // threads per merge CTA
-constexpr int kMItems = 16;  // outputs per thread
+#ifndef RS_MERGE_ITEMS
+#define RS_MERGE_ITEMS 32  // measured at 2^31, p = 8: 8 -> 2.62, 16 -> 2.10, 24 -> 2.12, 32 -> 1.85, 48 -> 2.28, 64 -> 2.10 ms per rank
+#endif
+constexpr int kMT = 256;                 // threads per merge CTA
+constexpr int kMItems = RS_MERGE_ITEMS;  // outputs per thread
 constexpr int kMTile = kMT * kMItems;
 
 // first i in [lo, hi] such that taking i elements of A and diag-i of B is a valid
@@ -63,13 +66,26 @@ __global__ void __launch_bounds__(kMT) k_merge_tile(const K* __restrict__ A, con
     const size_t a0 = split[t], a1 = split[t + 1];
     const size_t b0 = d0 - a0, b1 = d1 - a1;
     const int la = (int)(a1 - a0), lb = (int)(b1 - b0), len = la + lb;
-    for (int i = threadIdx.x; i < la; i += kMT) {
-        s_k[mpad(i)] = A[a0 + i];
-        if (V) s_v[mpad(i)] = VA[a0 + i];
-    }
-    for (int i = threadIdx.x; i < lb; i += kMT) {
-        s_k[mpad(la + i)] = B[b0 + i];
-        if (V) s_v[mpad(la + i)] = VB[b0 + i];
+    // stage a segment: scalar head up to 16-byte alignment, 16-byte vector body, scalar tail
+    auto stage = [&](const K* src, size_t s0, int l, int at) {
+        constexpr int VE = 16 / sizeof(K);
+        const int head = min(l, (int)((VE - (reinterpret_cast<uintptr_t>(src + s0) / sizeof(K)) % VE) % VE));
+        const int nvec = (l - head) / VE;
+        for (int i = threadIdx.x; i < head; i += kMT) s_k[mpad(at + i)] = src[s0 + i];
+        const uint4* vb = reinterpret_cast<const uint4*>(src + s0 + head);
+        for (int v = threadIdx.x; v < nvec; v += kMT) {
+            const uint4 x = __ldcs(vb + v);
+            const K* xs = reinterpret_cast<const K*>(&x);
+#pragma unroll
+            for (int e = 0; e < VE; ++e) s_k[mpad(at + head + v * VE + e)] = xs[e];
+        }
+        for (int i = head + nvec * VE + threadIdx.x; i < l; i += kMT) s_k[mpad(at + i)] = src[s0 + i];
+    };
+    stage(A, a0, la, 0);
+    stage(B, b0, lb, la);
+    if (V) {
+        for (int i = threadIdx.x; i < la; i += kMT) s_v[mpad(i)] = VA[a0 + i];
+        for (int i = threadIdx.x; i < lb; i += kMT) s_v[mpad(la + i)] = VB[b0 + i];
     }
     __syncthreads();
     auto KA = [&](int i) { return s_k[mpad(i)]; };
@@ -111,11 +127,27 @@ __global__ void __launch_bounds__(kMT) k_merge_tile(const K* __restrict__ A, con
             if (V) s_v[mpad(diag + o)] = ov[o];
         }
     __syncthreads();
-    for (int i = threadIdx.x; i < len; i += kMT) {
-        RS_DCHECK(d0 + i < na + nb);
-        out[d0 + i] = s_k[mpad(i)];
-        if (V) vout[d0 + i] = s_v[mpad(i)];
+    // store: scalar head up to 16-byte alignment of the destination, vector body, scalar tail
+    constexpr int VE = 16 / sizeof(K);
+    const int mis = (int)((reinterpret_cast<uintptr_t>(out + d0) / sizeof(K)) % VE);
+    const int head = min(len, (VE - mis) % VE);
+    const int nvec = (len - head) / VE;
+    for (int i = threadIdx.x; i < head; i += kMT) out[d0 + i] = s_k[mpad(i)];
+    uint4* vo = reinterpret_cast<uint4*>(out + d0 + head);
+    for (int v = threadIdx.x; v < nvec; v += kMT) {
+        uint4 x;
+        K* xs = reinterpret_cast<K*>(&x);
+#pragma unroll
+        for (int e = 0; e < VE; ++e) xs[e] = s_k[mpad(head + v * VE + e)];
+        RS_DCHECK(d0 + head + (size_t)v * VE + VE <= na + nb);
+        vo[v] = x;
     }
+    for (int i = head + nvec * VE + threadIdx.x; i < len; i += kMT) out[d0 + i] = s_k[mpad(i)];
+    if (V)
+        for (int i = threadIdx.x; i < len; i += kMT) {
+            RS_DCHECK(d0 + i < na + nb);
+            vout[d0 + i] = s_v[mpad(i)];
+        }
 }
 
 template <typename K, bool V>
