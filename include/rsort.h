@@ -27,7 +27,10 @@
  *   - The caller owns all buffers.  The library never allocates device memory
  *     on a sort call: scratch comes from `ws` (size from rs_workspace_bytes).
  *   - Calls are asynchronous on `stream` unless stated; they never abort or
- *     throw.  Arguments are validated before anything is enqueued, so on
+ *     throw.  Exception: the first radix-256 sort on a device runs the
+ *     design-5 lane-order probe (about 60 us) on `stream` and waits for it once
+ *     (rs_get_option "rank_probe"); inside a stream capture the probe is skipped
+ *     and that call uses the ballot design instead.  Arguments are validated before anything is enqueued, so on
  *     RS_EINVAL the inputs are untouched (single GPU: also on RS_ECAPACITY; the
  *     GSD collective detects RS_ECAPACITY after its local sort, so `keys` then
  *     holds the rank's sorted block).  On RS_ECUDA / RS_ENCCL buffer contents
