@@ -12,6 +12,7 @@
 #include "onesweep.cuh"
 #include "onesweep_ec.cuh"
 #include "onesweep_ar.cuh"
+#include "onesweep_ts.cuh"
 #include "onesweep_cr.cuh"
 #include "onesweep_n4.cuh"
 #include "radix16.cuh"
@@ -170,7 +171,7 @@ template <>
 struct TuneAr<uint32_t, true> : TuneT<256, 24, 2> {};
 template <typename K, bool V>
 static int tile_keys(int design) {
-    if (design == 5) return TuneAr<K, V>::THREADS * TuneAr<K, V>::KPT;
+    if (design == 5 || design == 6) return TuneAr<K, V>::THREADS * TuneAr<K, V>::KPT;
     if (design == 4) return TuneN4<K, V>::THREADS * TuneN4<K, V>::KPT;
     if (design == 3) return TuneCr<K, V>::THREADS * TuneCr<K, V>::KPT;
     if (design >= 1) return TuneEc<K, V>::THREADS * TuneEc<K, V>::KPT;  // 1, 2
@@ -189,7 +190,7 @@ int tile_keys_for(int key_bytes, bool has_val) { return tile_for(key_bytes, has_
 static int ws_tile_for(int key_bytes, bool has_val) {
     const int d = options().pass_design;
     const int t = tile_for(key_bytes, has_val, d);
-    return d == 5 ? std::min(t, tile_for(key_bytes, has_val, 2)) : t;
+    return (d == 5 || d == 6) ? std::min(t, tile_for(key_bytes, has_val, 2)) : t;
 }
 
 struct Layout8 {
@@ -279,6 +280,24 @@ static rs_status_t launch_pass_ec_me(const PassArgs& a, size_t T, cudaStream_t s
         }
     }
     return launch_pass_ec<K, V, S, LBW, 0>(a, T, st);
+}
+
+template <typename K, typename S>
+static rs_status_t launch_pass_ts(const PassArgs& a, size_t T, cudaStream_t st) {
+    using TN = TuneAr<K, false>;
+    using C = OnesweepTsCfg<K, TN::THREADS, TN::KPT>;
+    auto kern = k_onesweep_ts<K, TN::THREADS, TN::KPT, TN::MINB, S>;
+    static int grid_cap = 0;
+    if (!grid_cap) {
+        RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
+        int per_sm = 0;
+        RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TN::THREADS, C::smem_bytes));
+        grid_cap = std::max(1, per_sm) * sm_count();
+    }
+    const unsigned grid = (unsigned)std::min<size_t>(T, (size_t)grid_cap);  // persistent CTAs
+    LaunchScope ls("onesweep", st);
+    kern<<<grid, TN::THREADS, C::smem_bytes, st>>>(a);
+    return RS_OK;
 }
 
 template <typename K, bool V, typename S>
@@ -387,7 +406,11 @@ static rs_status_t launch_pass_n4(const PassArgs& a, size_t T, cudaStream_t st) 
 
 template <typename K, bool V>
 static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStream_t st, int design) {
-    if (design == 5) {
+    if (design == 6 && !V) {
+        if (wide) return launch_pass_ts<K, uint64_t>(a, T, st);
+        return launch_pass_ts<K, uint32_t>(a, T, st);
+    }
+    if (design == 5 || design == 6) {
         if (wide) return launch_pass_ar<K, V, uint64_t>(a, T, st);
         return launch_pass_ar<K, V, uint32_t>(a, T, st);
     }
@@ -473,7 +496,7 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
     Ctrl* ctrl = static_cast<Ctrl*>(ws);  // first carve of every layout
     RS_CUDA_TRY(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), st));
     int design = options().pass_design;
-    if (design == 5 && P > 0) {
+    if ((design == 5 || design == 6) && P > 0) {
         bool ar_ok = false;
         rs_status_t s = rank_order_ok(ctrl, st, &ar_ok);
         if (s != RS_OK) return s;

@@ -139,7 +139,7 @@ rs_status_t rs_set_option(const char* name, long long value) {
     else if (n == "hist_shared" && value <= 1) options().hist_shared = value != 0;
     else if (n == "match_every" && (value == 0 || value == 4 || value == 6 || value == 8))
         options().match_every = (int)value;
-    else if (n == "pass_design" && value <= 5) options().pass_design = (int)value;
+    else if (n == "pass_design" && value <= 6) options().pass_design = (int)value;
     else if (n == "rank_variant" && value <= 4) options().rank_variant = (int)value;
     else return fail(RS_EINVAL, "rs_set_option: unknown option or value: " + n);
     return RS_OK;

@@ -310,7 +310,7 @@ def test_rank_variants(option, variant):
     assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
 
 
-@pytest.mark.parametrize("design", [0, 1, 2, 3, 4, 5])
+@pytest.mark.parametrize("design", [0, 1, 2, 3, 4, 5, 6])
 @pytest.mark.parametrize("wide", [0, 1])
 def test_pass_designs(option, design, wide):
     """Every radix-256 pass kernel design (classic; early counts with a
