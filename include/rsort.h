@@ -161,8 +161,11 @@ int rs_comm_size(void* comm);
  * on a mismatch).  n may differ per rank.  Rank j receives Y_j, the j-th
  * contiguous slice of the global sorted order, in out[0 .. *n_out).  `keys`
  * (and vals) are used as scratch (they hold X_j, the locally sorted block, on
- * return).  The call blocks the host once, on the p×p count exchange; *n_out is
- * valid on return.  out_cap < |Y_j| → RS_ECAPACITY (on that rank). */
+ * return).  The call blocks the host twice (the header exchange and the p×p
+ * count exchange); *n_out is valid on return.  Receive capacity: out_cap <
+ * |Y_j| on any rank → RS_ECAPACITY on every rank.  Argument errors on any rank
+ * (bad pointers, digit width, workspace too small, mismatched settings) are
+ * agreed on in the header exchange: every rank returns RS_EINVAL, none hangs. */
 
 /* rs_gsd_exchange_plan: the host-side plan of GSD's all-to-all (PAPER.md:797-803,
  * "Processor k sends to processor j sequence X_{k,j}") from the all-gathered

@@ -27,10 +27,13 @@ rs_status_t sort_entry(int key_bytes, void* keys, uint32_t* vals, bool want_vals
                        void* out, uint32_t* vout, size_t out_cap, size_t* n_out, void* ws, size_t ws_bytes,
                        void* stream) {
     rs_status_t s = check_common(key_bytes, keys, vals, want_vals, n, b, out, vout);
-    if (s != RS_OK) return s;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    if (comm) return gsd_sort(static_cast<Comm*>(comm), key_bytes, keys, want_vals ? vals : nullptr, n, b, out,
-                              want_vals ? vout : nullptr, out_cap, n_out, ws, ws_bytes, st);
+    // collective: a rank whose arguments fail still takes part in the header
+    // exchange, so every rank returns RS_EINVAL instead of the others hanging
+    if (comm)
+        return gsd_sort(static_cast<Comm*>(comm), key_bytes, keys, want_vals ? vals : nullptr, n, b, out,
+                        want_vals ? vout : nullptr, out_cap, n_out, ws, ws_bytes, st, s);
+    if (s != RS_OK) return s;
     if (out_cap < n) return fail(RS_ECAPACITY, "out_cap < n");
     const size_t need = local_ws_bytes(key_bytes, want_vals, n, b);
     if (n && (!ws || ws_bytes < need))

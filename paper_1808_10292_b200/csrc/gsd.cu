@@ -223,8 +223,6 @@ struct GsdLayout {
     size_t local_ws_bytes;
     void* recv_keys;
     uint32_t* recv_vals;
-    uint64_t* hdr_local;  // 8 words
-    uint64_t* hdr_all;    // p*8
     Comp* samp_local;     // s
     Comp* samp_all;       // p*s
     Comp* splitters;      // p-1
@@ -262,8 +260,6 @@ static GsdLayout gsd_layout(void* ws, int key_bytes, bool has_val, size_t n, siz
     L.local_ws = c.take(L.local_ws_bytes);
     L.recv_keys = c.take(recv_slots * cap * key_bytes);
     L.recv_vals = static_cast<uint32_t*>(has_val ? c.take(recv_slots * cap * 4) : nullptr);
-    L.hdr_local = static_cast<uint64_t*>(c.take(8 * 8));
-    L.hdr_all = static_cast<uint64_t*>(c.take((size_t)p * 8 * 8));
     L.samp_local = static_cast<Comp*>(c.take(s * sizeof(Comp)));
     L.samp_all = static_cast<Comp*>(c.take((size_t)p * s * sizeof(Comp)));
     L.splitters = static_cast<Comp*>(c.take((size_t)p * sizeof(Comp)));
@@ -457,51 +453,58 @@ static rs_status_t merge_runs(int key_bytes, void* runs, uint32_t* vruns, const 
     } while (0)
 
 rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t n, int b, void* out, uint32_t* vout,
-                     size_t out_cap, size_t* n_out, void* ws, size_t ws_bytes, cudaStream_t st) {
+                     size_t out_cap, size_t* n_out, void* ws, size_t ws_bytes, cudaStream_t st,
+                     rs_status_t local_status) {
     const int p = c->nranks, rank = c->rank, r = c->r;
     const size_t s = (size_t)r * p;
     const bool hv = vals != nullptr;
     const bool ger = c->sampling >= 1;          // random sample (GER or GVR)
     const bool gvr = c->sampling == 2;          // split before sorting
-    if (!ger && (size_t)p * s > (size_t)kMaxSample)
-        return fail(RS_EINVAL, "r*p^2 exceeds the one-CTA sample sort limit of 8192");
-    GsdLayout L = gsd_layout(ws, key_bytes, hv, n, out_cap, b, p, r, 1);  // GER region carved once n is known
-    if (!ws || ws_bytes < L.bytes || !aligned16(ws))
-        return fail(RS_EINVAL, "GSD workspace too small / misaligned: need " + std::to_string(L.bytes));
-    if (out_cap && (!out || (hv && !vout))) return fail(RS_EINVAL, "NULL output with out_cap > 0");
+    std::string local_err = local_status != RS_OK ? rs_last_error() : "";
+    if (local_err.empty() && out_cap && (!out || (hv && !vout))) local_err = "NULL output with out_cap > 0";
+    if (local_err.empty() && (!ws || !aligned16(ws))) local_err = "GSD workspace NULL or misaligned";
 
-    // header all-gather: a mismatch is an error on every rank, not a hang
+    // header all-gather on comm-owned buffers, before anything else: a mismatch or a
+    // failed local validation on any rank is RS_EINVAL on every rank, not a hang
     uint64_t* h = c->h_pinned;
     const uint64_t samp_id =
         ger ? ((0x4745520000000000ull + (uint64_t)c->sampling) ^ (uint64_t)c->ger_s ^ (c->ger_seed * 0x9E3779B97F4A7C15ull))
             : (uint64_t)r;
-    uint64_t hdr[8] = {0x52534F5254ull, (uint64_t)key_bytes, (uint64_t)hv, (uint64_t)b, samp_id, (uint64_t)p,
-                       (uint64_t)out_cap, (uint64_t)n};
+    const uint64_t hdr[kHdrWords] = {0x52534F5254ull, (uint64_t)key_bytes, (uint64_t)hv, (uint64_t)b, samp_id,
+                                     (uint64_t)p, (uint64_t)out_cap, (uint64_t)n, (uint64_t)ws_bytes,
+                                     local_err.empty() ? 0ull : 1ull, 0, 0};
     std::memcpy(h, hdr, sizeof(hdr));
-    RS_CUDA_TRY(cudaMemcpyAsync(L.hdr_local, h, sizeof(hdr), cudaMemcpyHostToDevice, st));
-    RS_NCCL_TRY(ncclAllGather(L.hdr_local, L.hdr_all, 8, ncclUint64, c->nccl, st));
-    RS_CUDA_TRY(cudaMemcpyAsync(h, L.hdr_all, (size_t)p * 64, cudaMemcpyDeviceToHost, st));
+    RS_CUDA_TRY(cudaMemcpyAsync(c->d_hdr, h, sizeof(hdr), cudaMemcpyHostToDevice, st));
+    RS_NCCL_TRY(ncclAllGather(c->d_hdr, c->d_hdr + kHdrWords, kHdrWords, ncclUint64, c->nccl, st));
+    RS_CUDA_TRY(cudaMemcpyAsync(h, c->d_hdr + kHdrWords, (size_t)p * kHdrWords * 8, cudaMemcpyDeviceToHost, st));
     RS_CUDA_TRY(cudaStreamSynchronize(st));
+    if (!local_err.empty()) return fail(RS_EINVAL, local_err);
     std::vector<uint64_t> caps(p), noff(p + 1, 0);
     for (int k = 0; k < p; ++k) {
+        const uint64_t* hk = h + (size_t)k * kHdrWords;
         for (int f = 0; f < 6; ++f)
-            if (h[k * 8 + f] != hdr[f])
+            if (hk[f] != hdr[f])
                 return fail(RS_EINVAL, "GSD header mismatch with rank " + std::to_string(k) + " (field " +
                                            std::to_string(f) + ")");
-        caps[k] = h[k * 8 + 6];
-        if (h[k * 8 + 7] >= (1ull << 32)) return fail(RS_EINVAL, "n >= 2^32 on rank " + std::to_string(k));
-        noff[k + 1] = noff[k] + h[k * 8 + 7];
+        if (hk[9]) return fail(RS_EINVAL, "rank " + std::to_string(k) + " failed argument validation");
+        caps[k] = hk[6];
+        if (hk[7] >= (1ull << 32)) return fail(RS_EINVAL, "n >= 2^32 on rank " + std::to_string(k));
+        noff[k + 1] = noff[k] + hk[7];
     }
+    if (!ger && (size_t)p * s > (size_t)kMaxSample)
+        return fail(RS_EINVAL, "r*p^2 exceeds the one-CTA sample sort limit of 8192");
     const uint64_t n_total = noff[p];
-    size_t ger_s = 0, M = 0;
-    if (ger) {
-        ger_s = ger_s_for(c, n_total);
-        M = ger_draws(ger_s, p);
-        L = gsd_layout(ws, key_bytes, hv, n, out_cap, b, p, r, 1, M, gvr);
-        if (ws_bytes < L.bytes)
-            return fail(RS_EINVAL, "GER workspace too small: need " + std::to_string(L.bytes) +
-                                       " (size it with the largest local n)");
+    const size_t ger_s = ger ? ger_s_for(c, n_total) : 0;
+    const size_t M = ger ? ger_draws(ger_s, p) : 0;
+    // every rank checks every rank's workspace (sizes from the headers): all agree
+    for (int k = 0; k < p; ++k) {
+        const uint64_t* hk = h + (size_t)k * kHdrWords;
+        const size_t need = gsd_layout(nullptr, key_bytes, hv, hk[7], hk[6], b, p, r, 1, M, gvr).bytes;
+        if (hk[8] < need)
+            return fail(RS_EINVAL, "GSD workspace of rank " + std::to_string(k) + " too small: need " +
+                                       std::to_string(need) + " (size it with the largest local n)");
     }
+    const GsdLayout L = gsd_layout(ws, key_bytes, hv, n, out_cap, b, p, r, 1, M, gvr);
 
     // step 1: local sort in place -> X_k  (GVR sorts last)
     rs_status_t sst = (n && !gvr) ? local_sort(key_bytes, keys, vals, n, b, key_bytes * 8, keys, vals, L.local_ws,
@@ -639,17 +642,24 @@ rs_status_t rs_comm_create(const void* uid128, int nranks, int rank, int cuda_de
         delete c;
         return cuda_fail(e, "cudaSetDevice");
     }
-    c->h_pinned_words = std::max<size_t>((size_t)nranks * nranks, (size_t)nranks * 8) + 64;
+    c->h_pinned_words = std::max<size_t>((size_t)nranks * nranks, (size_t)nranks * kHdrWords) + 64;
     e = cudaMallocHost(&c->h_pinned, c->h_pinned_words * 8);
     if (e != cudaSuccess) {
         delete c;
         return cuda_fail(e, "cudaMallocHost");
+    }
+    e = cudaMalloc(&c->d_hdr, ((size_t)nranks + 1) * kHdrWords * 8);
+    if (e != cudaSuccess) {
+        cudaFreeHost(c->h_pinned);
+        delete c;
+        return cuda_fail(e, "cudaMalloc (comm header buffer)");
     }
     ncclUniqueId id;
     std::memcpy(&id, uid128, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, id, rank);
     if (r != ncclSuccess) {
         cudaFreeHost(c->h_pinned);
+        cudaFree(c->d_hdr);
         delete c;
         return fail(RS_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     }
@@ -662,6 +672,7 @@ rs_status_t rs_comm_destroy(void* comm) {
     Comm* c = static_cast<Comm*>(comm);
     if (c->nccl) ncclCommDestroy(c->nccl);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
+    if (c->d_hdr) cudaFree(c->d_hdr);
     delete c;
     return RS_OK;
 }

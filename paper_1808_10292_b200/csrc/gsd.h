@@ -19,6 +19,7 @@ struct Comm {
     size_t ger_s = 0;              // GER: samples per rank (s·p − 1 in all); 0 = 2⌈ω⌉²⌈lg n⌉, ω = lg lg n
     uint64_t ger_seed = 0;         // GER: SplitMix64 seed of the sample draws
     uint64_t* h_pinned = nullptr;  // p*p counts + headers (pinned host)
+    uint64_t* d_hdr = nullptr;     // device: this rank's header + all ranks' headers (kHdrWords each)
     size_t h_pinned_words = 0;
     std::vector<uint64_t> last_counts;  // p×p count matrix of the last sort (rs_comm_last_counts)
 };
@@ -32,13 +33,17 @@ struct Comp {
 };
 constexpr uint32_t kPosInf = 0xFFFFFFFFu;
 constexpr int kMaxSample = 8192;  // r·p² composites sorted in one CTA
+constexpr int kHdrWords = 12;     // per-rank header of a collective sort call
 
 // GER's s for n keys in all when the caller did not fix it (reading R30)
 size_t ger_default_s(uint64_t n_total);
 
 size_t gsd_capacity(Comm* c, size_t n_local_max);
 size_t gsd_ws_bytes(Comm* c, int key_bytes, bool has_val, size_t n_local_max, int b);
+// local_status: the caller's validation of this rank's arguments; a failure on
+// any rank makes every rank return RS_EINVAL after the header exchange (no hang)
 rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t n, int b, void* out,
-                     uint32_t* vout, size_t out_cap, size_t* n_out, void* ws, size_t ws_bytes, cudaStream_t st);
+                     uint32_t* vout, size_t out_cap, size_t* n_out, void* ws, size_t ws_bytes, cudaStream_t st,
+                     rs_status_t local_status = RS_OK);
 
 }  // namespace rs

@@ -2,6 +2,7 @@
 NCCL communicator bootstrapped over a torch.distributed process group: header
 all-gather, local sort, sample/splitters/split, count all-gather, the
 (self-)exchange and the merge all run through the multi-GPU code."""
+import ctypes
 import os
 import socket
 
@@ -94,3 +95,26 @@ def test_last_counts_after_a_sort(comm):
     a = inputs.gen_u32(12345, 64)
     rs.sort(dev(a), comm=comm)
     assert comm.last_counts().tolist() == [[12345]]
+
+
+def test_collective_validation_errors(comm):
+    """Bad arguments on a collective call are agreed on in the header exchange
+    (every rank returns RS_EINVAL; a rank never returns early and leaves the
+    others waiting): too-small workspace, bad digit width, NULL keys."""
+    L = rs.lib()
+    a = dev(inputs.gen_u32(5000, 65))
+    out = torch.empty(6000, dtype=torch.int32, device="cuda")
+    ws = torch.empty(4096, dtype=torch.uint8, device="cuda")
+    n_out = ctypes.c_size_t()
+    s = torch.cuda.current_stream().cuda_stream
+    assert L.rs_sort_u32(a.data_ptr(), a.numel(), 8, comm.handle, out.data_ptr(), 6000, ctypes.byref(n_out),
+                         ws.data_ptr(), ws.numel(), s) == 1
+    assert b"too small" in L.rs_last_error()
+    big = torch.empty(L.rs_workspace_bytes(4, 0, 5000, 8, comm.handle), dtype=torch.uint8, device="cuda")
+    assert L.rs_sort_u32(a.data_ptr(), a.numel(), 7, comm.handle, out.data_ptr(), 6000, ctypes.byref(n_out),
+                         big.data_ptr(), big.numel(), s) == 1
+    assert L.rs_sort_u32(None, 5000, 8, comm.handle, out.data_ptr(), 6000, ctypes.byref(n_out),
+                         big.data_ptr(), big.numel(), s) == 1
+    # the communicator still works afterwards
+    y = rs.sort(a, comm=comm)
+    assert (host(y, np.uint32) == np.sort(host(a, np.uint32))).all()
