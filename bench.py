@@ -315,6 +315,9 @@ def main():
     xchg = None
     if p > 1:
         L.rs_timing_query(b"gsd_exchange", ctypes.byref(ms_q), ctypes.byref(cnt_q))
+        pulled = cnt_q.value == 0  # pull merge: the transfer is the first merge level's NVLink reads
+        if pulled:
+            L.rs_timing_query(b"gsd_pull_merge", ctypes.byref(ms_q), ctypes.byref(cnt_q))
         x_ms = ms_q.value / max(cnt_q.value, 1)
         cm = comm.last_counts().astype(np.float64)
         w = KEY_BYTES[kind] + (4 if kind == "pairs" else 0)
@@ -325,7 +328,9 @@ def main():
         x_ms, x_bytes = float(t[0]), float(t[1])
         nvl_peak = 770.0
         ach = x_bytes / (x_ms / 1e3) / 1e9 if x_ms > 0 else None
-        xchg = {"kernel": "grouped ncclSend/ncclRecv all-to-all (GSD step 4)", "bound": "nvlink",
+        xchg = {"kernel": ("pull merge: merge tree whose first level reads the peers' blocks over NVLink "
+                           "(CUDA IPC); time = the whole merge" if pulled
+                           else "grouped ncclSend/ncclRecv all-to-all (GSD step 4)"), "bound": "nvlink",
                 "bytes_max_rank": int(x_bytes), "ms": round(x_ms, 4),
                 "achieved": round(ach, 1) if ach else None, "peak": nvl_peak, "unit": "GB/s",
                 "frac": round(ach / nvl_peak, 4) if ach else None,

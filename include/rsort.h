@@ -224,6 +224,17 @@ rs_status_t rs_gvr_emulate(int key_bytes, int p, size_t s, uint64_t seed, int di
                            size_t* n_out, uint64_t* splitters, uint64_t* counts,
                            void* ws, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------ CUDA IPC -- */
+/* Device-buffer mappings used by the GSD pull merge (gsd_merge = 2): export
+ * the IPC handle (64 bytes) of the cudaMalloc allocation containing `ptr` and
+ * ptr's byte offset in it; open a peer's (handle, offset) as a local pointer
+ * (each handle is opened once per device and cached; rs_ipc_close_all unmaps).
+ * Export fails with RS_ECUDA for memory that has no IPC handle (VMM / cuMem
+ * allocations); the pull merge then falls back to the all-to-all. */
+rs_status_t rs_ipc_export(const void* ptr, void* handle64, uint64_t* offset);
+rs_status_t rs_ipc_open(const void* handle64, uint64_t offset, void** ptr);
+rs_status_t rs_ipc_close_all(void);
+
 /* --------------------------------------------------------------- options -- */
 /* Process-wide tuning / test knobs (not needed for normal use):
  *   "wide_status"    1 = use 64-bit look-back status words at any n (they are
@@ -241,8 +252,14 @@ rs_status_t rs_gvr_emulate(int key_bytes, int p, size_t s, uint64_t seed, int di
  *                    sweep (rank, look-back, reorder, store).
  *   "match_every"    0, 4, 6 or 8: in the default pass (u32 keys) every k-th key is
  *                    ranked with match.any (ADU pipe) instead of ballots (ALU pipe).
- *   "gsd_merge"      GSD step 5: 0 = tree of stable 2-way merge-path merges (default),
- *                    1 = stable radix re-sort of the received runs (same result).
+ *   "gsd_merge"      GSD step 5 (all give the same Y_j): 2 = pull merge (default):
+ *                    no all-to-all; the merge tree's first level reads every
+ *                    peer's X_{k,j} in place over NVLink through CUDA IPC
+ *                    mappings (see below; emulation: the blocks in place); if
+ *                    any rank cannot export or map a block, every rank falls
+ *                    back to 0 for that call.  0 = NCCL all-to-all into a
+ *                    receive buffer, then the tree of stable 2-way merge-path
+ *                    merges; 1 = all-to-all, then a stable radix re-sort.
  *   "compact"        1 = default pass with 16-bit per-warp counters (smaller
  *                    shared-memory footprint; ballots only).
  *   "hist_shared"    1 = digit-histogram kernel with one shared histogram per

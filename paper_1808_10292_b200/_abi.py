@@ -35,6 +35,9 @@ SIGNATURES = {
     "rs_comm_set_oversampling": (_i32, [_vp, _i32]),
     "rs_comm_set_sampling": (_i32, [_vp, _i32, _sz, ctypes.c_uint64]),
     "rs_comm_last_counts": (_i32, [_vp, _u64p]),
+    "rs_ipc_export": (_i32, [_vp, _vp, _u64p]),
+    "rs_ipc_open": (_i32, [_vp, ctypes.c_uint64, _vpp]),
+    "rs_ipc_close_all": (_i32, []),
     "rs_ger_default_s": (_sz, [ctypes.c_uint64]),
     "rs_ger_capacity": (_sz, [_sz, _i32, _sz]),
     "rs_ger_emulate_ws_bytes": (_sz, [_i32, _i32, _i32, _sz, _i32, _sz, _sz]),

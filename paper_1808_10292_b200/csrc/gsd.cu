@@ -553,6 +553,63 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
     uint64_t total = 0;
     if ((sst = rs_gsd_exchange_plan(p, rank, cnt.data(), caps.data(), soff.data(), roff.data(), &total)) != RS_OK)
         return sst;
+    // pull merge (gsd_merge = 2): no all-to-all; the merge
+    // tree's first level reads the peers' X_{k,j} in place over NVLink through
+    // CUDA IPC mappings exchanged now (falls back to the all-to-all on every
+    // rank if any rank cannot export its block, e.g. VMM memory)
+    if (options().gsd_merge == 2 && !gvr && p > 1) {
+        uint64_t* rec = h;
+        std::memset(rec, 0, kIpcWords * 8);
+        bool ok = ipc_export(keys, rec, &rec[8]) == RS_OK;
+        if (ok && hv) ok = ipc_export(vals, &rec[9], &rec[17]) == RS_OK;
+        rec[18] = ok ? 1 : 0;
+        RS_CUDA_TRY(cudaMemcpyAsync(c->d_ipc, rec, kIpcWords * 8, cudaMemcpyHostToDevice, st));
+        RS_NCCL_TRY(ncclAllGather(c->d_ipc, c->d_ipc + kIpcWords, kIpcWords, ncclUint64, c->nccl, st));
+        RS_CUDA_TRY(cudaMemcpyAsync(h, c->d_ipc + kIpcWords, (size_t)p * kIpcWords * 8, cudaMemcpyDeviceToHost, st));
+        RS_CUDA_TRY(cudaStreamSynchronize(st));
+        bool all_ok = true;
+        for (int k = 0; k < p; ++k) all_ok = all_ok && h[(size_t)k * kIpcWords + 18] == 1;
+        std::vector<const void*> rk(p);
+        std::vector<const uint32_t*> rv(hv ? p : 0);
+        std::vector<uint64_t> len(p);
+        if (all_ok) {
+            // map the peers' blocks; whether every rank could is agreed on collectively
+            bool opened = true;
+            for (int k = 0; k < p && opened; ++k) {
+                uint64_t so = 0;  // start of X_{k,rank} in rank k's sorted block
+                for (int jj = 0; jj < rank; ++jj) so += cnt[(size_t)k * p + jj];
+                len[k] = cnt[(size_t)k * p + rank];
+                const uint64_t* rk_rec = h + (size_t)k * kIpcWords;
+                void* kb = keys;
+                void* vb = vals;
+                if (k != rank) {
+                    opened = ipc_open(rk_rec, rk_rec[8], &kb) == RS_OK;
+                    if (opened && hv) opened = ipc_open(&rk_rec[9], rk_rec[17], &vb) == RS_OK;
+                }
+                rk[k] = static_cast<const char*>(kb) + so * key_bytes;
+                if (hv) rv[k] = static_cast<const uint32_t*>(vb) + so;
+            }
+            h[0] = opened ? 0 : 1;
+            RS_CUDA_TRY(cudaMemcpyAsync(c->d_ipc, h, 8, cudaMemcpyHostToDevice, st));
+            RS_NCCL_TRY(ncclAllReduce(c->d_ipc, c->d_ipc, 1, ncclUint64, ncclMax, c->nccl, st));
+            RS_CUDA_TRY(cudaMemcpyAsync(h, c->d_ipc, 8, cudaMemcpyDeviceToHost, st));
+            RS_CUDA_TRY(cudaStreamSynchronize(st));
+            all_ok = h[0] == 0;
+        }
+        if (all_ok) {
+            {
+                LaunchScope ls("gsd_pull_merge", st, false);
+                if ((sst = merge_runs_ptrs(key_bytes, rk, rv, len, L.merge_keys, L.merge_vals, out, vout,
+                                           L.merge_split, st)) != RS_OK)
+                    return sst;
+            }
+            // no rank may reuse its block before every peer has read its slices
+            RS_NCCL_TRY(ncclAllReduce(c->d_ipc, c->d_ipc, 1, ncclUint64, ncclMax, c->nccl, st));
+            if (n_out) *n_out = total;
+            RS_CUDA_TRY(cudaGetLastError());
+            return RS_OK;
+        }
+    }
     // exchange X_{k,j}: grouped send/recv; the self slice is a device copy
     char* kx = static_cast<char*>(gvr && p > 1 ? L.gv_keys : keys);
     if (gvr && p > 1) vals = L.gv_vals;
@@ -642,14 +699,16 @@ rs_status_t rs_comm_create(const void* uid128, int nranks, int rank, int cuda_de
         delete c;
         return cuda_fail(e, "cudaSetDevice");
     }
-    c->h_pinned_words = std::max<size_t>((size_t)nranks * nranks, (size_t)nranks * kHdrWords) + 64;
+    c->h_pinned_words = std::max<size_t>((size_t)nranks * nranks, (size_t)nranks * kIpcWords) + 64;
     e = cudaMallocHost(&c->h_pinned, c->h_pinned_words * 8);
     if (e != cudaSuccess) {
         delete c;
         return cuda_fail(e, "cudaMallocHost");
     }
     e = cudaMalloc(&c->d_hdr, ((size_t)nranks + 1) * kHdrWords * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&c->d_ipc, ((size_t)nranks + 1) * kIpcWords * 8);
     if (e != cudaSuccess) {
+        if (c->d_hdr) cudaFree(c->d_hdr);
         cudaFreeHost(c->h_pinned);
         delete c;
         return cuda_fail(e, "cudaMalloc (comm header buffer)");
@@ -660,6 +719,7 @@ rs_status_t rs_comm_create(const void* uid128, int nranks, int rank, int cuda_de
     if (r != ncclSuccess) {
         cudaFreeHost(c->h_pinned);
         cudaFree(c->d_hdr);
+        cudaFree(c->d_ipc);
         delete c;
         return fail(RS_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
     }
@@ -673,6 +733,7 @@ rs_status_t rs_comm_destroy(void* comm) {
     if (c->nccl) ncclCommDestroy(c->nccl);
     if (c->h_pinned) cudaFreeHost(c->h_pinned);
     if (c->d_hdr) cudaFree(c->d_hdr);
+    if (c->d_ipc) cudaFree(c->d_ipc);
     delete c;
     return RS_OK;
 }
@@ -796,6 +857,25 @@ static rs_status_t emulate(int mode, int key_bytes, int p, int r, size_t ger_s, 
                 return sst;
             n_out[j] = tot;
         }
+    }
+    if (mode != 2 && options().gsd_merge == 2 && p > 1) {  // pull merge: the blocks are read in place
+        for (int j = 0; j < p; ++j) {
+            std::vector<const void*> rk(p);
+            std::vector<const uint32_t*> rv(hv ? p : 0);
+            std::vector<uint64_t> len(p);
+            for (int k = 0; k < p; ++k) {
+                const uint64_t so = cut[(size_t)k * (p + 1) + j];
+                len[k] = cnt[(size_t)k * p + j];
+                rk[k] = static_cast<const char*>(keys[k]) + so * key_bytes;
+                if (hv) rv[k] = vals[k] + so;
+            }
+            LaunchScope ls("gsd_pull_merge", st, false);
+            if ((sst = merge_runs_ptrs(key_bytes, rk, rv, len, L.merge_keys, L.merge_vals, out_keys[j],
+                                       hv ? out_vals[j] : nullptr, L.merge_split, st)) != RS_OK)
+                return sst;
+        }
+        RS_CUDA_TRY(cudaGetLastError());
+        return RS_OK;
     }
     for (int j = 0; j < p; ++j) {  // step 4 exchange + step 5 merge, rank by rank
         char* rk = static_cast<char*>(L.recv_keys);

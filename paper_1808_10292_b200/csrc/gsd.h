@@ -20,6 +20,7 @@ struct Comm {
     uint64_t ger_seed = 0;         // GER: SplitMix64 seed of the sample draws
     uint64_t* h_pinned = nullptr;  // p*p counts + headers (pinned host)
     uint64_t* d_hdr = nullptr;     // device: this rank's header + all ranks' headers (kHdrWords each)
+    uint64_t* d_ipc = nullptr;     // device: IPC handle exchange of the pull merge (kIpcWords per rank)
     size_t h_pinned_words = 0;
     std::vector<uint64_t> last_counts;  // p×p count matrix of the last sort (rs_comm_last_counts)
 };
@@ -34,6 +35,7 @@ struct Comp {
 constexpr uint32_t kPosInf = 0xFFFFFFFFu;
 constexpr int kMaxSample = 8192;  // r·p² composites sorted in one CTA
 constexpr int kHdrWords = 12;     // per-rank header of a collective sort call
+constexpr int kIpcWords = 20;     // per-rank IPC record: key handle + offset, value handle + offset, ok
 
 // GER's s for n keys in all when the caller did not fix it (reading R30)
 size_t ger_default_s(uint64_t n_total);

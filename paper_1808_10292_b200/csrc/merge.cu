@@ -230,6 +230,90 @@ static rs_status_t merge_tree(K* runs, uint32_t* vruns, const std::vector<uint64
     return RS_OK;
 }
 
+// Tree whose level 0 reads p runs at arbitrary addresses (e.g. peers' sorted
+// blocks over NVLink, mapped by CUDA IPC): level 0 merges run pairs into a level
+// buffer, later levels alternate between `out` and `tmp` so the last writes `out`.
+template <typename K, bool V>
+static rs_status_t merge_tree_ptrs(const std::vector<const void*>& rk, const std::vector<const uint32_t*>& rv,
+                                   const std::vector<uint64_t>& len, K* tmp, uint32_t* vtmp, K* out, uint32_t* vout,
+                                   size_t* split, cudaStream_t st) {
+    const int p = (int)len.size();
+    std::vector<uint64_t> off(p + 1, 0);
+    for (int k = 0; k < p; ++k) off[k + 1] = off[k] + len[k];
+    const size_t total = off[p];
+    if (total == 0) return RS_OK;
+    int levels = 0;
+    for (int q = p; q > 1; q = (q + 1) / 2) ++levels;
+    auto buf = [&](int level) { return ((levels - 1 - level) % 2 == 0) ? out : tmp; };
+    auto vbuf = [&](int level) { return ((levels - 1 - level) % 2 == 0) ? vout : vtmp; };
+    K* dst = levels == 0 ? out : buf(0);
+    uint32_t* vdst = V ? (levels == 0 ? vout : vbuf(0)) : nullptr;
+    std::vector<uint64_t> noff(1, 0);
+    for (int k = 0; k < p; k += 2) {  // level 0 (or the single run)
+        const K* A = static_cast<const K*>(rk[k]);
+        if (k + 1 < p) {
+            const K* B = static_cast<const K*>(rk[k + 1]);
+            rs_status_t s = merge2<K, V>(A, V ? rv[k] : nullptr, len[k], B, V ? rv[k + 1] : nullptr, len[k + 1],
+                                         dst + off[k], V ? vdst + off[k] : nullptr, split, st);
+            if (s != RS_OK) return s;
+            noff.push_back(off[k + 2]);
+        } else {
+            if (len[k]) {
+                RS_CUDA_TRY(cudaMemcpyAsync(dst + off[k], A, len[k] * sizeof(K), cudaMemcpyDefault, st));
+                if (V) RS_CUDA_TRY(cudaMemcpyAsync(vdst + off[k], rv[k], len[k] * 4, cudaMemcpyDefault, st));
+            }
+            noff.push_back(off[k + 1]);
+        }
+    }
+    if (levels <= 1) return RS_OK;
+    // levels 1..: contiguous runs in buf(l-1) -> buf(l); the generic tree clobbers its input
+    // buffer, which here is free scratch (tmp or out)
+    for (int l = 1; l < levels; ++l) {
+        K* src = buf(l - 1);
+        uint32_t* vsrc = V ? vbuf(l - 1) : nullptr;
+        K* d = buf(l);
+        uint32_t* vd = V ? vbuf(l) : nullptr;
+        const int q = (int)noff.size() - 1;
+        std::vector<uint64_t> nn(1, 0);
+        for (int k = 0; k < q; k += 2) {
+            const uint64_t a0 = noff[k], a1 = noff[k + 1];
+            if (k + 1 < q) {
+                const uint64_t b1 = noff[k + 2];
+                rs_status_t s = merge2<K, V>(src + a0, V ? vsrc + a0 : nullptr, a1 - a0, src + a1,
+                                             V ? vsrc + a1 : nullptr, b1 - a1, d + a0, V ? vd + a0 : nullptr, split, st);
+                if (s != RS_OK) return s;
+                nn.push_back(b1);
+            } else {
+                if (a1 > a0) {
+                    RS_CUDA_TRY(cudaMemcpyAsync(d + a0, src + a0, (a1 - a0) * sizeof(K), cudaMemcpyDeviceToDevice, st));
+                    if (V) RS_CUDA_TRY(cudaMemcpyAsync(vd + a0, vsrc + a0, (a1 - a0) * 4, cudaMemcpyDeviceToDevice, st));
+                }
+                nn.push_back(a1);
+            }
+        }
+        noff.swap(nn);
+    }
+    return RS_OK;
+}
+
+rs_status_t merge_runs_ptrs(int key_bytes, const std::vector<const void*>& rk, const std::vector<const uint32_t*>& rv,
+                            const std::vector<uint64_t>& len, void* tmp, uint32_t* vtmp, void* out, uint32_t* vout,
+                            size_t* split, cudaStream_t st) {
+    const bool V = !rv.empty() && rv[0] != nullptr;
+    if (key_bytes == 4) {
+        if (V)
+            return merge_tree_ptrs<uint32_t, true>(rk, rv, len, static_cast<uint32_t*>(tmp), vtmp,
+                                                   static_cast<uint32_t*>(out), vout, split, st);
+        return merge_tree_ptrs<uint32_t, false>(rk, rv, len, static_cast<uint32_t*>(tmp), nullptr,
+                                                static_cast<uint32_t*>(out), nullptr, split, st);
+    }
+    if (V)
+        return merge_tree_ptrs<uint64_t, true>(rk, rv, len, static_cast<uint64_t*>(tmp), vtmp,
+                                               static_cast<uint64_t*>(out), vout, split, st);
+    return merge_tree_ptrs<uint64_t, false>(rk, rv, len, static_cast<uint64_t*>(tmp), nullptr,
+                                            static_cast<uint64_t*>(out), nullptr, split, st);
+}
+
 rs_status_t merge_runs_tree(int key_bytes, void* runs, uint32_t* vruns, const std::vector<uint64_t>& roff, void* tmp,
                             uint32_t* vtmp, void* out, uint32_t* vout, size_t* split, cudaStream_t st) {
     const bool V = vruns != nullptr;

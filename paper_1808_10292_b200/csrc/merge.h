@@ -14,4 +14,10 @@ size_t merge_scratch_bytes(size_t total);
 rs_status_t merge_runs_tree(int key_bytes, void* runs, uint32_t* vruns, const std::vector<uint64_t>& roff, void* tmp,
                             uint32_t* vtmp, void* out, uint32_t* vout, size_t* split, cudaStream_t st);
 
+// runs at arbitrary addresses rk[k] (+ rv[k]) of len[k] keys, read but not written
+// (peers' blocks over NVLink in the pull merge); tmp and out: total keys each.
+rs_status_t merge_runs_ptrs(int key_bytes, const std::vector<const void*>& rk, const std::vector<const uint32_t*>& rv,
+                            const std::vector<uint64_t>& len, void* tmp, uint32_t* vtmp, void* out, uint32_t* vout,
+                            size_t* split, cudaStream_t st);
+
 }  // namespace rs

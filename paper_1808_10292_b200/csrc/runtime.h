@@ -40,7 +40,8 @@ struct Options {
     bool wide_status = false;     // force 64-bit look-back status words (tests)
     unsigned debug_skip = 0;      // timing ablations (invalid output): 1 look-back, 2 rank, 4 store, 8 reorder
     int rank_variant = 3;         // 0 ballot peers, 1 match.any, 2 atomic-OR peers, 3 hybrid pairs
-    int gsd_merge = 0;            // GSD step 5: 0 merge tree, 1 stable radix re-sort
+    int gsd_merge = 2;            // GSD step 5: 0 merge tree, 1 stable radix re-sort, 2 pull merge
+                                  // (the tree reads the source blocks in place: peers over NVLink)
     bool compact = false;         // design 2: 16-bit per-warp counters, ballots only (4 CTAs/SM)
     int match_every = 0;          // design 2, u32 keys: every k-th key ranked by match.any (0 = none)
     bool hist_shared = false;     // K1: 1 = one histogram copy per 4 warps (previous default)
@@ -51,6 +52,9 @@ struct Options {
 };
 // design 5 precondition (radix.cu): -1 not probed yet on this device, 0 failed, 1 passed
 int rank_probe_state();
+// CUDA IPC mappings (ipc.cu)
+rs_status_t ipc_export(const void* ptr, void* handle64, uint64_t* offset);
+rs_status_t ipc_open(const void* handle64, uint64_t offset, void** ptr);
 // radix-256 tile (keys) of the selected pass design (radix.cu)
 int tile_keys_for(int key_bytes, bool has_val);
 Options& options();

@@ -51,11 +51,11 @@ L.rs_timing_enable(0)
 sort_ms = sum(q(x)[0] for x in ("hist", "plan", "onesweep", "final_copy"))
 merge_ms = sum(q(x)[0] for x in ("merge_split", "merge_tile"))
 gsd_ms = sum(q(x)[0] for x in ("gsd_sample", "gsd_splitters", "gsd_split", "ger_sample", "gvr_split"))
-all_ms = q("")[0]
+all_ms = q("")[0] - q("gsd_pull_merge")[0]  # the pull scope wraps kernels timed on their own
 ex_ms = q("gsd_exchange")[0]
 counts = got["counts"].astype(np.int64)
 off_rank = max(int(counts[k].sum() - counts[k, k]) for k in range(p))
-print(f"{mode.upper()} emulation n=2^{log2n} p={p} merge={'tree' if merge == 0 else 're-sort'}")
+print(f"{mode.upper()} emulation n=2^{log2n} p={p} merge={['tree', 're-sort', 'pull'][merge]}")
 print(f"  per rank: all device time {all_ms / p:.3f} ms")
 print(f"  per rank: local sort {sort_ms / p:.3f} ms (incl. re-sort if merge=1), sample/split kernels {gsd_ms / p:.3f} ms,"
       f" merge-tree {merge_ms / p:.3f} ms, device-copy exchange {ex_ms / p:.3f} ms")

@@ -96,11 +96,13 @@ def option():
         rs.lib().rs_set_option(name.encode(), value)
 
 
-@pytest.mark.parametrize("merge", [0, 1])
+@pytest.mark.parametrize("merge", [0, 1, 2])
 @pytest.mark.parametrize("p", [2, 3, 5, 6, 7, 8])
 def test_gsd_merge_tree_and_resort(option, merge, p):
-    """Step 5 as the merge tree (0) and as a stable re-sort (1): identical Y_j,
-    for odd run counts too; narrow pair keys check the tie rule (lower rank first)."""
+    """Step 5 as the merge tree (0), as a stable re-sort (1) and as the pull merge
+    (2: no exchange copies, the tree's first level reads every rank's block in
+    place): identical Y_j, for odd run counts too; narrow pair keys check the tie
+    rule (lower rank first)."""
     option("gsd_merge", merge)
     N = 9000 + 37 * p
     k = inputs.gen_u64(p * N, 70 + p, "mod1024")
@@ -221,3 +223,12 @@ def test_gvr_pairs_global_stability_and_u64(b):
 def test_gvr_uneven_and_empty_blocks():
     a = inputs.gen_u32(9000, 94)
     _check_gvr([a[:0], a[:5000], a[5000:5003], a[5003:]], s=6, seed=4)
+
+
+def test_pull_merge_ger_and_large(option):
+    """The pull merge under GER sampling and over large uneven runs."""
+    option("gsd_merge", 2)
+    a = inputs.gen_u32(600000, 95)
+    cuts = [0, 100000, 350001, 350002, 600000]
+    _check_ger([a[cuts[k]:cuts[k + 1]] for k in range(4)], s=0, seed=9)
+    _check([a[cuts[k]:cuts[k + 1]] for k in range(4)], r=8, b=8)
