@@ -41,13 +41,10 @@
 #ifndef RS_AR_CT16
 #define RS_AR_CT16 1
 #endif
-// RANK2: [rank] only counts (atomics without return); after [offset] has turned
-// the counters into warp start offsets, [scatter] takes each key's slot from a
-// second returning atomic (start + stable rank, lane-ordered as in [rank]) — no
-// rank registers and no counter load in the scatter
-#ifndef RS_AR_RANK2
-#define RS_AR_RANK2 0
-#endif
+// RANK2 (template): [rank] only counts (atomics without return); after [offset]
+// has turned the counters into warp start offsets, [scatter] takes each key's
+// slot from a second returning atomic (start + stable rank, lane-ordered as in
+// [rank]) — no rank registers and no counter load in the scatter
 
 namespace rs {
 
@@ -79,7 +76,8 @@ struct OnesweepArCfg {
 //      L2 by the TMA engine): no s_in, no shared-memory write/read of the input
 //   2  as 1, but the keys are not kept: the scatter loads them again (from L2),
 //      which frees the registers for larger tiles
-template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, bool KREG_, int KSRC = 0>
+template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, bool KREG_, int KSRC = 0,
+          bool RANK2 = false>
 __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
     static_assert(KSRC == 0 || !HAS_VAL, "register/global tiles are for keys-only sorts");
     constexpr bool LDGK = KSRC != 0;
@@ -155,7 +153,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
     static_assert(KPT % 2 == 0 && WK <= 65536, "ranks are packed two per register");
     constexpr int G = KPT % 8 == 0 ? 8 : (KPT % 6 == 0 ? 6 : (KPT % 4 == 0 ? 4 : 2));  // batch of keys
     K kr[KREG ? KPT : 2];  // this thread's keys of the tile (rows j, lane)
-    uint32_t rr[RS_AR_RANK2 ? 1 : KPT / 2];  // stable ranks within the warp's keys of their digit, 16 bits each
+    uint32_t rr[RANK2 ? 1 : KPT / 2];  // stable ranks within the warp's keys of their digit, 16 bits each
 
     while (tile < a.num_tiles) {
         const size_t base = (size_t)tile * TILE;
@@ -210,7 +208,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                 for (int i = 0; i < G; ++i) {
                     if (KREG && KSRC == 0) kr[KREG ? g + i : 0] = kk[i];
                     const uint32_t d = digit8<K>(kk[i], shift);
-                    if (RS_AR_RANK2) {
+                    if (RANK2) {
                         atomicAdd(&wc[RS_AR_CT16 ? d >> 1 : d], RS_AR_CT16 ? 1u << ((d & 1u) << 4) : 1u);
                         rg[i] = 0;
                     } else if (RS_AR_CT16) {
@@ -220,10 +218,10 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                         rg[i] = atomicAdd(&wc[d], 1u);
                     }
                 }
-                if (!RS_AR_RANK2) {
+                if (!RANK2) {
 #pragma unroll
                     for (int i = 0; i < G; i += 2)
-                        rr[RS_AR_RANK2 ? 0 : (g + i) / 2] = __byte_perm(rg[i], rg[i + 1], 0x5410);
+                        rr[RANK2 ? 0 : (g + i) / 2] = __byte_perm(rg[i], rg[i + 1], 0x5410);
                 }
             }
         }
@@ -283,7 +281,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                 for (int i = 0; i < G; ++i) {
                     const int j = g + i;
                     const uint32_t d = digit8<K>(kk[i], shift);
-                    if (RS_AR_RANK2) {
+                    if (RANK2) {
                         if (RS_AR_CT16) {
                             const uint32_t sh = (d & 1u) << 4;
                             pos[i] = (atomicAdd(&wcp[d >> 1], 1u << sh) >> sh) & 0xFFFFu;
@@ -292,7 +290,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                         }
                     } else {
                         pos[i] = (RS_AR_CT16 ? (uint32_t)wc16[d] : wc[d]) +
-                                 ((rr[RS_AR_RANK2 ? 0 : j / 2] >> (16 * (j & 1))) & 0xFFFFu);
+                                 ((rr[RANK2 ? 0 : j / 2] >> (16 * (j & 1))) & 0xFFFFu);
                     }
                     if (HAS_VAL) vv[HAS_VAL ? i : 0] = s_vin[ibase + j * 32];
                 }

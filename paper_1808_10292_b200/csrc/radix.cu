@@ -125,8 +125,11 @@ struct TuneN4<uint32_t, true> : TuneT<256, 12, 3> {};
 
 // atomic-rank design (5): (threads, keys per thread, min CTAs per SM).  Large
 // tiles amortise the per-tile offsets and look-back (measured on B200, 2^27 and
-// 2^31 keys: u32 256x48 with 2 CTAs/SM beats 256x24x3, 256x30x3, 256x40x2,
-// 256x64x1, 256x96x1, 512x20x2, 512x24x1, 512x32x1; pairs 256x32x1 beats
+// 2^31 keys).  u32, input tile by TMA: 256x48 with 2 CTAs/SM beats 256x24x3,
+// 256x30x3, 256x40x2, 256x64x1, 256x96x1, 512x20x2, 512x24x1, 512x32x1; u32 with
+// the keys read from global memory twice and count-then-rank (no s_in, no rank
+// registers): 256x88x2 (4.85 ms per 2^31 pass) beats 256x48x2 with TMA (5.14),
+// 256x72x2 (4.90), 256x80x2 (5.03), 256x96x2 (5.77); pairs 256x32x1 beats
 // 256x12x2, 256x16x2, 256x24x1; u64 keys 256x24x2 beats 256x12x3, 512x12x1)
 template <typename K, bool V>
 struct TuneAr;
@@ -137,7 +140,10 @@ struct TuneAr;
 // shared memory, 1 registers, 2 global memory twice.  Measured per 2^27 pass:
 // u64 KSRC 0 -> 1 0.576 -> 0.533 ms; u32 at 256x48 KSRC 1 no gain (register-bound)
 #ifndef RS_AR_KSRC_U32
-#define RS_AR_KSRC_U32 0
+#define RS_AR_KSRC_U32 2  // u32 keys: from global memory twice (no input tile in shared memory)
+#endif
+#ifndef RS_AR_RANK2_U32
+#define RS_AR_RANK2_U32 1  // u32 keys: count-then-rank scatter (onesweep_ar.cuh RANK2): no rank registers
 #endif
 #ifndef RS_AR_KSRC_U64
 #define RS_AR_KSRC_U64 1
@@ -146,7 +152,7 @@ struct TuneAr;
 #define RS_AR_KREG 2  // 0 never, 1 always, 2 with values (pairs: 2 CTAs/SM leave room)
 #endif
 #ifndef RS_AR_U32_KPT
-#define RS_AR_U32_KPT 48
+#define RS_AR_U32_KPT 88  // with KSRC 2 + RANK2: shared memory holds only s_out, so the tile can grow
 #endif
 #ifndef RS_AR_U32_T
 #define RS_AR_U32_T 256
@@ -304,8 +310,10 @@ template <typename K, bool V, typename S>
 static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st) {
     using TN = TuneAr<K, V>;
     constexpr int KSRC = V ? 0 : (sizeof(K) == 8 ? RS_AR_KSRC_U64 : RS_AR_KSRC_U32);
+    constexpr bool RANK2 = !V && sizeof(K) == 4 && RS_AR_RANK2_U32;
     using C = OnesweepArCfg<K, V, TN::THREADS, TN::KPT, KSRC>;
-    auto kern = k_onesweep_ar<K, V, TN::THREADS, TN::KPT, TN::MINB, S, (RS_AR_KREG == 1 || (RS_AR_KREG == 2 && V)), KSRC>;
+    auto kern = k_onesweep_ar<K, V, TN::THREADS, TN::KPT, TN::MINB, S, (RS_AR_KREG == 1 || (RS_AR_KREG == 2 && V)), KSRC,
+                              RANK2>;
     static int grid_cap = 0;
     if (!grid_cap) {
         RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
