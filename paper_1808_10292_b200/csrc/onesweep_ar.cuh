@@ -58,7 +58,7 @@ struct OnesweepArCfg {
     static constexpr size_t in_off = 0;
     static constexpr size_t out_off = in_off + (KSRC != 0 ? 0 : (size_t)TILE * sizeof(K));
     static constexpr size_t vin_off = out_off + (size_t)TILE * sizeof(K);
-    static constexpr size_t vout_off = vin_off + (HAS_VAL ? (size_t)TILE * 4 : 0);
+    static constexpr size_t vout_off = vin_off + ((HAS_VAL && KSRC == 0) ? (size_t)TILE * 4 : 0);
     static constexpr size_t wc_off = vout_off + (HAS_VAL ? (size_t)TILE * 4 : 0);
     static constexpr size_t texcl_off = wc_off + (size_t)W * R * (RS_AR_CT16 ? 2 : 4);
     static constexpr size_t tcnt_off = texcl_off + R * 4;
@@ -79,7 +79,7 @@ struct OnesweepArCfg {
 template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, bool KREG_, int KSRC = 0,
           bool RANK2 = false>
 __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
-    static_assert(KSRC == 0 || !HAS_VAL, "register/global tiles are for keys-only sorts");
+    static_assert(KSRC != 1 || !HAS_VAL, "register tiles are for keys-only sorts");
     constexpr bool LDGK = KSRC != 0;
     constexpr bool KREG = (KREG_ && KSRC != 2) || KSRC == 1;
     using ST = Status<S>;
@@ -124,8 +124,10 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         const size_t base = (size_t)t * TILE;
         const uint32_t valid = (uint32_t)min((size_t)TILE, (size_t)a.n - base);
         const uint32_t kbytes = (valid * (uint32_t)sizeof(K)) & ~15u;
-        if (LDGK) {  // L2 prefetch only; the threads load their keys themselves
+        if (LDGK) {  // L2 prefetch only; the threads load their keys (and values) themselves
             if (kbytes) bulk_prefetch_l2(src + base, kbytes);
+            const uint32_t vb = HAS_VAL ? ((valid * 4u) & ~15u) : 0u;
+            if (HAS_VAL && vb) bulk_prefetch_l2(vsrc + base, vb);
             return;
         }
         const uint32_t vbytes = HAS_VAL ? ((valid * 4u) & ~15u) : 0u;
@@ -172,7 +174,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
 #pragma unroll
                 for (int j = 0; j < KPT; ++j) kr[KREG ? j : 0] = (uint32_t)(j * 32) < lim ? g[j * 32] : ~K(0);
             }
-        } else if (valid < (uint32_t)TILE) {
+        } else if (KSRC == 0 && valid < (uint32_t)TILE) {
             const uint32_t kdone = ((valid * (uint32_t)sizeof(K)) & ~15u) / sizeof(K);
             for (uint32_t i = kdone + tid; i < (uint32_t)TILE; i += THREADS)
                 s_in[i] = i < valid ? src[base + i] : ~K(0);
@@ -292,7 +294,9 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                         pos[i] = (RS_AR_CT16 ? (uint32_t)wc16[d] : wc[d]) +
                                  ((rr[RANK2 ? 0 : j / 2] >> (16 * (j & 1))) & 0xFFFFu);
                     }
-                    if (HAS_VAL) vv[HAS_VAL ? i : 0] = s_vin[ibase + j * 32];
+                    if (HAS_VAL)
+                        vv[HAS_VAL ? i : 0] = KSRC == 2 ? ((uint32_t)(j * 32) < lim ? __ldcs(vsrc + base + ibase + j * 32) : 0u)
+                                                        : s_vin[ibase + j * 32];
                 }
 #pragma unroll
                 for (int i = 0; i < G; ++i) {

@@ -142,11 +142,21 @@ struct TuneAr;
 #ifndef RS_AR_KSRC_U32
 #define RS_AR_KSRC_U32 2  // u32 keys: from global memory twice (no input tile in shared memory)
 #endif
+#ifndef RS_AR_KSRC_PAIRS
+#define RS_AR_KSRC_PAIRS 2  // pairs: keys and values from global memory (TMA tile 256x32x1: 0.801 ms per
+                            // 2^27 pass; global 256x24x2: 0.753; with RANK2 0.760; 256x28x2 0.767; 256x32x2 0.898)
+#endif
+#ifndef RS_AR_RANK2_PAIRS
+#define RS_AR_RANK2_PAIRS 0
+#endif
+#ifndef RS_AR_RANK2_U64
+#define RS_AR_RANK2_U64 1
+#endif
 #ifndef RS_AR_RANK2_U32
 #define RS_AR_RANK2_U32 1  // u32 keys: count-then-rank scatter (onesweep_ar.cuh RANK2): no rank registers
 #endif
 #ifndef RS_AR_KSRC_U64
-#define RS_AR_KSRC_U64 1
+#define RS_AR_KSRC_U64 2  // measured per 2^27 pass: KSRC 1 at 256x24 0.534 ms; KSRC 2 + RANK2 at 256x40 0.516
 #endif
 #ifndef RS_AR_KREG
 #define RS_AR_KREG 2  // 0 never, 1 always, 2 with values (pairs: 2 CTAs/SM leave room)
@@ -161,15 +171,15 @@ template <>
 struct TuneAr<uint32_t, false> : TuneT<RS_AR_U32_T, RS_AR_U32_KPT, RS_AR_U32_MINB> {};
 #ifndef RS_AR_U64_T
 #define RS_AR_U64_T 256
-#define RS_AR_U64_KPT 24
+#define RS_AR_U64_KPT 40
 #define RS_AR_U64_MINB 2
 #endif
 template <>
 struct TuneAr<uint64_t, false> : TuneT<RS_AR_U64_T, RS_AR_U64_KPT, RS_AR_U64_MINB> {};
 #ifndef RS_AR_PAIRS_T
 #define RS_AR_PAIRS_T 256
-#define RS_AR_PAIRS_KPT 32
-#define RS_AR_PAIRS_MINB 1
+#define RS_AR_PAIRS_KPT 24
+#define RS_AR_PAIRS_MINB 2
 #endif
 template <>
 struct TuneAr<uint64_t, true> : TuneT<RS_AR_PAIRS_T, RS_AR_PAIRS_KPT, RS_AR_PAIRS_MINB> {};
@@ -309,8 +319,8 @@ static rs_status_t launch_pass_ts(const PassArgs& a, size_t T, cudaStream_t st) 
 template <typename K, bool V, typename S>
 static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st) {
     using TN = TuneAr<K, V>;
-    constexpr int KSRC = V ? 0 : (sizeof(K) == 8 ? RS_AR_KSRC_U64 : RS_AR_KSRC_U32);
-    constexpr bool RANK2 = !V && sizeof(K) == 4 && RS_AR_RANK2_U32;
+    constexpr int KSRC = V ? RS_AR_KSRC_PAIRS : (sizeof(K) == 8 ? RS_AR_KSRC_U64 : RS_AR_KSRC_U32);
+    constexpr bool RANK2 = V ? RS_AR_RANK2_PAIRS : (sizeof(K) == 4 ? RS_AR_RANK2_U32 : RS_AR_RANK2_U64);
     using C = OnesweepArCfg<K, V, TN::THREADS, TN::KPT, KSRC>;
     auto kern = k_onesweep_ar<K, V, TN::THREADS, TN::KPT, TN::MINB, S, (RS_AR_KREG == 1 || (RS_AR_KREG == 2 && V)), KSRC,
                               RANK2>;
