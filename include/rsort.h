@@ -262,6 +262,9 @@ rs_status_t rs_ipc_close_all(void);
  *                    merges; 1 = all-to-all, then a stable radix re-sort.
  *   "compact"        1 = default pass with 16-bit per-warp counters (smaller
  *                    shared-memory footprint; ballots only).
+ *   "small_tiles"    design-5 tiles: 0 = small tiles when the input makes fewer
+ *                    than three large tiles per SM (default), 1 = always large,
+ *                    2 = always small.
  *   "hist_shared"    1 = digit-histogram kernel with one shared histogram per
  *                    4 warps (0, default: lane-private copies, conflict-free).
  *   "debug_skip"     timing ablations, OUTPUT INVALID: bit 0 no look-back,

@@ -185,8 +185,30 @@ template <>
 struct TuneAr<uint64_t, true> : TuneT<RS_AR_PAIRS_T, RS_AR_PAIRS_KPT, RS_AR_PAIRS_MINB> {};
 template <>
 struct TuneAr<uint32_t, true> : TuneT<256, 24, 2> {};
+// design 5 for small inputs (fewer than three large tiles per SM): smaller tiles
+// keep every SM busy (2^20 u32 keys are 47 tiles of 22528 keys but 256 of 4096)
 template <typename K, bool V>
-static int tile_keys(int design) {
+struct TuneArSmall;
+template <>
+struct TuneArSmall<uint32_t, false> : TuneT<256, 16, 4> {};
+template <>
+struct TuneArSmall<uint64_t, false> : TuneT<256, 8, 4> {};
+template <>
+struct TuneArSmall<uint64_t, true> : TuneT<256, 8, 4> {};
+template <>
+struct TuneArSmall<uint32_t, true> : TuneT<256, 8, 4> {};
+
+template <typename K, bool V>
+static bool small_input(size_t n) {
+    if (options().small_tiles != 0) return options().small_tiles == 2;
+    const size_t big = (size_t)TuneAr<K, V>::THREADS * TuneAr<K, V>::KPT;
+    return (n + big - 1) / big < 3 * (size_t)sm_count();  // measured crossover: 2^23 small, 2^24 large (u32)
+}
+
+template <typename K, bool V>
+static int tile_keys(int design, size_t n = ~size_t(0)) {
+    if (design == 5 && n != ~size_t(0) && small_input<K, V>(n))
+        return TuneArSmall<K, V>::THREADS * TuneArSmall<K, V>::KPT;
     if (design == 5 || design == 6) return TuneAr<K, V>::THREADS * TuneAr<K, V>::KPT;
     if (design == 4) return TuneN4<K, V>::THREADS * TuneN4<K, V>::KPT;
     if (design == 3) return TuneCr<K, V>::THREADS * TuneCr<K, V>::KPT;
@@ -194,18 +216,18 @@ static int tile_keys(int design) {
     return Tune<K, V>::THREADS * Tune<K, V>::KPT;
 }
 
-static int tile_for(int key_bytes, bool has_val, int design) {
-    if (key_bytes == 4) return has_val ? tile_keys<uint32_t, true>(design) : tile_keys<uint32_t, false>(design);
-    return has_val ? tile_keys<uint64_t, true>(design) : tile_keys<uint64_t, false>(design);
+static int tile_for(int key_bytes, bool has_val, int design, size_t n = ~size_t(0)) {
+    if (key_bytes == 4) return has_val ? tile_keys<uint32_t, true>(design, n) : tile_keys<uint32_t, false>(design, n);
+    return has_val ? tile_keys<uint64_t, true>(design, n) : tile_keys<uint64_t, false>(design, n);
 }
 
 int tile_keys_for(int key_bytes, bool has_val) { return tile_for(key_bytes, has_val, options().pass_design); }
 
 // the tile size the workspace is sized for: design 5 may fall back to design 2
 // after its probe, so size for the smaller of the two tiles (more status rows)
-static int ws_tile_for(int key_bytes, bool has_val) {
+static int ws_tile_for(int key_bytes, bool has_val, size_t n) {
     const int d = options().pass_design;
-    const int t = tile_for(key_bytes, has_val, d);
+    const int t = tile_for(key_bytes, has_val, d, n);
     return (d == 5 || d == 6) ? std::min(t, tile_for(key_bytes, has_val, 2)) : t;
 }
 
@@ -239,7 +261,7 @@ static Layout8 layout8(void* ws, int key_bytes, bool has_val, size_t n, size_t t
 }
 
 size_t local_ws_bytes(int key_bytes, bool has_val, size_t n, int b) {
-    if (b == 8) return layout8(nullptr, key_bytes, has_val, n, (size_t)ws_tile_for(key_bytes, has_val)).bytes;
+    if (b == 8) return layout8(nullptr, key_bytes, has_val, n, (size_t)ws_tile_for(key_bytes, has_val, n)).bytes;
     return radix16_ws_bytes(key_bytes, has_val, n);
 }
 
@@ -316,9 +338,9 @@ static rs_status_t launch_pass_ts(const PassArgs& a, size_t T, cudaStream_t st) 
     return RS_OK;
 }
 
-template <typename K, bool V, typename S>
+template <typename K, bool V, typename S, bool SMALL>
 static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st) {
-    using TN = TuneAr<K, V>;
+    using TN = typename std::conditional<SMALL, TuneArSmall<K, V>, TuneAr<K, V>>::type;
     constexpr int KSRC = V ? RS_AR_KSRC_PAIRS : (sizeof(K) == 8 ? RS_AR_KSRC_U64 : RS_AR_KSRC_U32);
     constexpr bool RANK2 = V ? RS_AR_RANK2_PAIRS : (sizeof(K) == 4 ? RS_AR_RANK2_U32 : RS_AR_RANK2_U64);
     using C = OnesweepArCfg<K, V, TN::THREADS, TN::KPT, KSRC>;
@@ -429,8 +451,9 @@ static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStrea
         return launch_pass_ts<K, uint32_t>(a, T, st);
     }
     if (design == 5 || design == 6) {
-        if (wide) return launch_pass_ar<K, V, uint64_t>(a, T, st);
-        return launch_pass_ar<K, V, uint32_t>(a, T, st);
+        const bool small = design == 5 && small_input<K, V>(a.n);  // must match tile_keys()
+        if (wide) return small ? launch_pass_ar<K, V, uint64_t, true>(a, T, st) : launch_pass_ar<K, V, uint64_t, false>(a, T, st);
+        return small ? launch_pass_ar<K, V, uint32_t, true>(a, T, st) : launch_pass_ar<K, V, uint32_t, false>(a, T, st);
     }
     if (design == 4) {
         if (wide) return launch_pass_n4<K, V, uint64_t>(a, T, st);
@@ -520,7 +543,7 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
         if (s != RS_OK) return s;
         if (!ar_ok) design = 2;
     }
-    const Layout8 L = layout8(ws, sizeof(K), V, n, (size_t)tile_for(sizeof(K), V, design));
+    const Layout8 L = layout8(ws, sizeof(K), V, n, (size_t)tile_for(sizeof(K), V, design, n));
     RS_CUDA_TRY(cudaMemsetAsync(L.hist, 0, (size_t)P * 256 * 4, st));
     // K1 also zeroes the first pass's status region (as u32 words)
     rs_status_t s = launch_hist<K>(keys_in, n, P, L.hist, static_cast<uint32_t*>(L.status), L.status_bytes / 4, st);

@@ -86,6 +86,29 @@ EDGE_N = sorted({1, 2, 3, 31, 32, 33, 1000, TILE64 - 1, TILE64, TILE64 + 1, TILE
                  TILE32 - 1, TILE32, TILE32 + 1, 2 * TILE32 + 3, 7 * TILE32 + 4095})
 
 
+@pytest.mark.parametrize("tiles", [1, 2])
+def test_edge_sizes_large_and_small_tiles(option, tiles):
+    """Both design-5 tile sizes (large: the size-dependent default above ~6.7 M
+    u32 keys; small: below) at every edge size, u32 keys, u64 keys and pairs."""
+    option("small_tiles", tiles)
+    for n in EDGE_N:
+        a = inputs.gen_u32(n, 125 + n)
+        assert (_sort_u32(a, 8) == oracle.sr(a, 8)).all(), n
+        k = inputs.gen_u64(n, 126 + n, "mod1024")
+        v = inputs.iota_u32(n)
+        tk, tv = dev(k), dev(v)
+        rs.sort_pairs(tk, tv)
+        wk, wv = oracle.sr(k, 8, vals=v)
+        assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all(), n
+        t = dev(k)
+        rs.sort(t)
+        assert (host(t, np.uint64) == wk).all(), n
+    a = inputs.gen_u32((1 << 21) + 77, 127)
+    for t in range(1, 5):
+        got = host(rs.sort_bits(dev(a), end_bit=8 * t, digit_bits=8), np.uint32)
+        assert (got == oracle.sr(a, 8, rounds=t)).all(), t
+
+
 @pytest.mark.parametrize("b", [8, 16])
 @pytest.mark.parametrize("inplace", [True, False])
 def test_edge_sizes_u32(b, inplace):
