@@ -145,6 +145,17 @@ rs_status_t rs_comm_set_oversampling(void* comm, int r);
  * The output capacity (rs_output_capacity) then follows Lemma Sampling1 with
  * ρ = 1: exceeding it has probability ≤ 1/n and returns RS_ECAPACITY. */
 rs_status_t rs_comm_set_sampling(void* comm, int mode, size_t s, uint64_t seed);
+/* mode 3 (not a sample sort) = the paper's PR4 across GPUs:
+ * per 8-bit digit, a local count-sort round, an all-gather of the p×256 counts,
+ * and each rank pulling from every peer (CUDA IPC over NVLink) the keys whose
+ * global rank (SPEC.md:206 formula) falls in its range; rank j ends with exactly
+ * its input count of the sorted order (balanced).  digit_bits 8 only; every rank
+ * must be able to map its peers' memory (else RS_ECUDA on every rank).
+ * rs_pr_emulate runs all ranks on one GPU (ws: rs_pr_emulate_ws_bytes). */
+size_t rs_pr_emulate_ws_bytes(int key_bytes, int val_bytes, int p, size_t n_max);
+rs_status_t rs_pr_emulate(int key_bytes, int p, void* const* keys, uint32_t* const* vals, const size_t* n,
+                          void* const* out_keys, uint32_t* const* out_vals, void* ws, size_t ws_bytes,
+                          void* stream);
 /* GER's default s for n keys in all, and the Lemma-Sampling1 capacity for a
  * largest block of n_local_max keys over p ranks (s = 0: the default s). */
 size_t rs_ger_default_s(uint64_t n_total);

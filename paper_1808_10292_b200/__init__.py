@@ -207,7 +207,7 @@ class Comm:
         """"gsd" (regular oversampling, default), "ger" (random oversampling
         with s samples per rank, s = 0 the paper's choice, SplitMix64 seed) or
         "gvr" (the same sample, split before sorting)."""
-        m = {"gsd": 0, "ger": 1, "gvr": 2}[mode]
+        m = {"gsd": 0, "ger": 1, "gvr": 2, "pr4": 3}[mode]
         check(lib().rs_comm_set_sampling(self.handle, m, s, seed), "rs_comm_set_sampling")
         self.sampling = mode
 
@@ -249,6 +249,27 @@ def ger_emulate(blocks: list[torch.Tensor], s: int = 0, seed: int = 0, digit_bit
     """GER (random oversampling) over p = len(blocks) ranks on
     this GPU; s = 0 selects the paper's s.  Same result dict as gsd_emulate."""
     return _emulate(1, blocks, 1, s, seed, digit_bits, vals, out_cap, stream)
+
+
+def pr_emulate(blocks: list[torch.Tensor], vals: list[torch.Tensor] | None = None, stream=None):
+    """PR4 across p = len(blocks) ranks held on this GPU (per-digit local round,
+    count exchange, pull of each rank's global-rank range): returns dict(Y, Yv)
+    with |Y_j| = |blocks[j]|.  The blocks are scratch."""
+    p = len(blocks)
+    kb = _KEY_BYTES[blocks[0].dtype]
+    n = [b.numel() for b in blocks]
+    dev = blocks[0].device
+    outs = [torch.empty(max(x, 1), dtype=blocks[0].dtype, device=dev) for x in n]
+    vouts = [torch.empty(max(x, 1), dtype=torch.int32, device=dev) for x in n] if vals is not None else None
+    ws = _workspace(lib().rs_pr_emulate_ws_bytes(kb, 4 if vals is not None else 0, p, max(n) if n else 0), dev)
+    arr = ctypes.c_void_p * p
+    check(lib().rs_pr_emulate(kb, p, arr(*[b.data_ptr() for b in blocks]),
+                              arr(*[v.data_ptr() for v in vals]) if vals is not None else None,
+                              (ctypes.c_size_t * p)(*n), arr(*[o.data_ptr() for o in outs]),
+                              arr(*[o.data_ptr() for o in vouts]) if vals is not None else None,
+                              ws.data_ptr(), ws.numel(), _stream(stream)), "rs_pr_emulate")
+    return dict(Y=[outs[j][: n[j]] for j in range(p)],
+                Yv=[vouts[j][: n[j]] for j in range(p)] if vals is not None else None)
 
 
 def gvr_emulate(blocks: list[torch.Tensor], s: int = 0, seed: int = 0, digit_bits: int = 8,

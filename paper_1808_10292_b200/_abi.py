@@ -38,6 +38,8 @@ SIGNATURES = {
     "rs_ipc_export": (_i32, [_vp, _vp, _u64p]),
     "rs_ipc_open": (_i32, [_vp, ctypes.c_uint64, _vpp]),
     "rs_ipc_close_all": (_i32, []),
+    "rs_pr_emulate_ws_bytes": (_sz, [_i32, _i32, _i32, _sz]),
+    "rs_pr_emulate": (_i32, [_i32, _i32, _vpp, _vpp, _szp, _vpp, _vpp, _vp, _sz, _vp]),
     "rs_ger_default_s": (_sz, [ctypes.c_uint64]),
     "rs_ger_capacity": (_sz, [_sz, _i32, _sz]),
     "rs_ger_emulate_ws_bytes": (_sz, [_i32, _i32, _i32, _sz, _i32, _sz, _sz]),

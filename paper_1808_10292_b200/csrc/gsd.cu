@@ -317,11 +317,13 @@ static size_t ger_capacity_for(size_t n_local_max, int p, size_t s) {
 static size_t ger_s_for(Comm* c, uint64_t n_total) { return c->ger_s ? c->ger_s : ger_default_s(n_total); }
 
 size_t gsd_capacity(Comm* c, size_t n_local_max) {
+    if (c->sampling == 3) return n_local_max;  // PR4: rank j receives exactly its input size
     if (c->sampling >= 1) return ger_capacity_for(n_local_max, c->nranks, ger_s_for(c, (uint64_t)n_local_max * c->nranks));
     return capacity_for(n_local_max, c->r, c->nranks);
 }
 
 size_t gsd_ws_bytes(Comm* c, int key_bytes, bool has_val, size_t n_local_max, int b) {
+    if (c->sampling == 3) return pr_ws_bytes(key_bytes, has_val, n_local_max, c->nranks);
     const size_t cap = gsd_capacity(c, n_local_max);
     const size_t M = c->sampling >= 1 ? ger_draws(ger_s_for(c, (uint64_t)n_local_max * c->nranks), c->nranks) : 0;
     return gsd_layout(nullptr, key_bytes, has_val, n_local_max, cap, b, c->nranks, c->r, 1, M, c->sampling == 2).bytes;
@@ -458,7 +460,7 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
     const int p = c->nranks, rank = c->rank, r = c->r;
     const size_t s = (size_t)r * p;
     const bool hv = vals != nullptr;
-    const bool ger = c->sampling >= 1;          // random sample (GER or GVR)
+    const bool ger = c->sampling == 1 || c->sampling == 2;  // random sample (GER or GVR)
     const bool gvr = c->sampling == 2;          // split before sorting
     std::string local_err = local_status != RS_OK ? rs_last_error() : "";
     if (local_err.empty() && out_cap && (!out || (hv && !vout))) local_err = "NULL output with out_cap > 0";
@@ -469,7 +471,7 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
     uint64_t* h = c->h_pinned;
     const uint64_t samp_id =
         ger ? ((0x4745520000000000ull + (uint64_t)c->sampling) ^ (uint64_t)c->ger_s ^ (c->ger_seed * 0x9E3779B97F4A7C15ull))
-            : (uint64_t)r;
+            : ((uint64_t)r | ((uint64_t)c->sampling << 56));
     const uint64_t hdr[kHdrWords] = {0x52534F5254ull, (uint64_t)key_bytes, (uint64_t)hv, (uint64_t)b, samp_id,
                                      (uint64_t)p, (uint64_t)out_cap, (uint64_t)n, (uint64_t)ws_bytes,
                                      local_err.empty() ? 0ull : 1ull, 0, 0};
@@ -490,6 +492,18 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
         caps[k] = hk[6];
         if (hk[7] >= (1ull << 32)) return fail(RS_EINVAL, "n >= 2^32 on rank " + std::to_string(k));
         noff[k + 1] = noff[k] + hk[7];
+    }
+    if (c->sampling == 3) {  // PR4 across GPUs: sizes, digit width and capacity agreed here
+        if (b != 8) return fail(RS_EINVAL, "PR4 routing across GPUs is radix 256 (digit_bits 8)");
+        std::vector<uint64_t> n_all(p);
+        for (int k = 0; k < p; ++k) {
+            const uint64_t* hk = h + (size_t)k * kHdrWords;
+            n_all[k] = hk[7];
+            if (hk[8] < pr_ws_bytes(key_bytes, hv, hk[7], p))
+                return fail(RS_EINVAL, "PR workspace of rank " + std::to_string(k) + " too small");
+            if (hk[6] < hk[7]) return fail(RS_ECAPACITY, "PR: out_cap < n on rank " + std::to_string(k));
+        }
+        return pr_sort(c, key_bytes, keys, vals, n, out, vout, n_out, ws, n_all, st);
     }
     if (!ger && (size_t)p * s > (size_t)kMaxSample)
         return fail(RS_EINVAL, "r*p^2 exceeds the one-CTA sample sort limit of 8192");
@@ -699,7 +713,8 @@ rs_status_t rs_comm_create(const void* uid128, int nranks, int rank, int cuda_de
         delete c;
         return cuda_fail(e, "cudaSetDevice");
     }
-    c->h_pinned_words = std::max<size_t>((size_t)nranks * nranks, (size_t)nranks * kIpcWords) + 64;
+    c->h_pinned_words = std::max<size_t>(std::max<size_t>((size_t)nranks * nranks, (size_t)nranks * kIpcWords),
+                                          ((size_t)nranks * 256 + 1) * 4) + 64;  // + PR4's piece list
     e = cudaMallocHost(&c->h_pinned, c->h_pinned_words * 8);
     if (e != cudaSuccess) {
         delete c;
@@ -966,7 +981,7 @@ size_t rs_ger_capacity(size_t n_local_max, int p, size_t s) {
 size_t rs_ger_default_s(uint64_t n_total) { return ger_default_s(n_total); }
 
 rs_status_t rs_comm_set_sampling(void* comm, int mode, size_t s, uint64_t seed) {
-    if (!comm || mode < 0 || mode > 2) return fail(RS_EINVAL, "bad comm / sampling mode");
+    if (!comm || mode < 0 || mode > 3) return fail(RS_EINVAL, "bad comm / sampling mode");
     Comm* c = static_cast<Comm*>(comm);
     c->sampling = mode;
     c->ger_s = s;

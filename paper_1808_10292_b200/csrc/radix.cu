@@ -532,7 +532,8 @@ static rs_status_t launch_hist(const K* keys, size_t n, int P, uint32_t* hist,
 
 template <typename K, bool V>
 static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, int end_bit, K* out,
-                         uint32_t* vout, void* ws, cudaStream_t st) {
+                         uint32_t* vout, void* ws, cudaStream_t st, int first_pass = 0,
+                         uint32_t* hist_copy = nullptr) {
     const int P = (end_bit + 7) / 8;
     Ctrl* ctrl = static_cast<Ctrl*>(ws);  // first carve of every layout
     RS_CUDA_TRY(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), st));
@@ -548,10 +549,12 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
     // K1 also zeroes the first pass's status region (as u32 words)
     rs_status_t s = launch_hist<K>(keys_in, n, P, L.hist, static_cast<uint32_t*>(L.status), L.status_bytes / 4, st);
     if (s != RS_OK) return s;
+    if (hist_copy)
+        RS_CUDA_TRY(cudaMemcpyAsync(hist_copy, L.hist + (size_t)first_pass * 256, 256 * 4, cudaMemcpyDeviceToDevice, st));
     {
         LaunchScope ls("plan", st);
         k_plan<<<1, 256, 0, st>>>(L.hist, (uint32_t)n, P, L.bases, L.ctrl,
-                                  (const void*)keys_in == (const void*)out ? 1 : 0);
+                                  (const void*)keys_in == (const void*)out ? 1 : 0, first_pass);
     }
     PassArgs a{};
     a.keys_in = keys_in;
@@ -602,6 +605,27 @@ rs_status_t local_sort(int key_bytes, const void* keys_in, const uint32_t* vals_
                                      static_cast<uint64_t*>(out), vout, ws, st);
     return sort8<uint64_t, false>(static_cast<const uint64_t*>(keys_in), nullptr, n, end_bit,
                                   static_cast<uint64_t*>(out), nullptr, ws, st);
+}
+
+rs_status_t local_sort_digit(int key_bytes, const void* keys_in, const uint32_t* vals_in, size_t n, int pass_t,
+                             void* out, uint32_t* vout, void* ws, cudaStream_t st, uint32_t* hist_copy) {
+    if (n == 0) {
+        if (hist_copy) RS_CUDA_TRY(cudaMemsetAsync(hist_copy, 0, 256 * 4, st));
+        return RS_OK;
+    }
+    const int end_bit = 8 * (pass_t + 1);
+    if (key_bytes == 4) {
+        if (vals_in)
+            return sort8<uint32_t, true>(static_cast<const uint32_t*>(keys_in), vals_in, n, end_bit,
+                                         static_cast<uint32_t*>(out), vout, ws, st, pass_t, hist_copy);
+        return sort8<uint32_t, false>(static_cast<const uint32_t*>(keys_in), nullptr, n, end_bit,
+                                      static_cast<uint32_t*>(out), nullptr, ws, st, pass_t, hist_copy);
+    }
+    if (vals_in)
+        return sort8<uint64_t, true>(static_cast<const uint64_t*>(keys_in), vals_in, n, end_bit,
+                                     static_cast<uint64_t*>(out), vout, ws, st, pass_t, hist_copy);
+    return sort8<uint64_t, false>(static_cast<const uint64_t*>(keys_in), nullptr, n, end_bit,
+                                  static_cast<uint64_t*>(out), nullptr, ws, st, pass_t, hist_copy);
 }
 
 rs_status_t digit_histogram(int key_bytes, const void* keys, size_t n, int b, uint32_t* hist, void* ws,

@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_digit_hist_lp(const K* __restric
 // call with an odd count ends in `alt` and needs the final copy.
 __global__ void __launch_bounds__(256) k_plan(const uint32_t* __restrict__ hist, uint32_t n, int P,
                                               uint32_t* __restrict__ bases, Ctrl* __restrict__ ctrl,
-                                              int inplace) {
+                                              int inplace, int first = 0) {
     __shared__ uint32_t s_warp[8];
     __shared__ int s_active[kMaxPasses];
     const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(256) k_plan(const uint32_t* __restrict__ hist,
         uint32_t pre = 0;
         for (int w = 0; w < warp; ++w) pre += s_warp[w];
         bases[t * 256 + d] = pre + x - tot;  // exclusive over digits
-        if (d == 0) s_active[t] = !full;
+        if (d == 0) s_active[t] = !full && t >= first;  // passes below `first` are not run
         __syncthreads();
     }
     if (d == 0) {

@@ -83,6 +83,11 @@ size_t local_ws_bytes(int key_bytes, bool has_val, size_t n, int b);
 rs_status_t local_sort(int key_bytes, const void* keys_in, const uint32_t* vals_in, size_t n, int b,
                        int end_bit, void* out, uint32_t* vout, void* ws, size_t ws_bytes,
                        cudaStream_t stream);
+// one stable radix-256 count-sort round on digit `pass_t` only (PR4 across GPUs):
+// keys_in -> out (out-of-place), the round's 256-bin histogram copied to hist_copy
+// (device); ws sized by local_ws_bytes(key_bytes, vals, n, 8)
+rs_status_t local_sort_digit(int key_bytes, const void* keys_in, const uint32_t* vals_in, size_t n, int pass_t,
+                             void* out, uint32_t* vout, void* ws, cudaStream_t st, uint32_t* hist_copy);
 rs_status_t digit_histogram(int key_bytes, const void* keys, size_t n, int b, uint32_t* hist, void* ws,
                             size_t ws_bytes, cudaStream_t stream);
 

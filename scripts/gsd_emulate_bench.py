@@ -1,7 +1,8 @@
 """Time GSD's device phases through rs_gsd_emulate (all p ranks on one GPU, run
 rank by rank): per-rank local sort, sample/splitters/split kernels and step-5
 merge, as averages per rank.  Development aid for projecting the multi-GPU step.
-Usage: python scripts/gsd_emulate_bench.py [log2_total] [p] [merge(0 tree|1 resort)] [gsd|ger|gvr]"""
+Usage: python scripts/gsd_emulate_bench.py [log2_total] [p] [merge(0 tree|1 resort|2 pull)] [gsd|ger|gvr|pr4]
+(pr4: "sample/split kernels" is the per-round pull of the routed keys)"""
 import ctypes
 import os
 import sys
@@ -44,13 +45,16 @@ for it in range(3):
         got = rs.gsd_emulate(blocks, r=8, digit_bits=8)
     elif mode == "ger":
         got = rs.ger_emulate(blocks, s=0, seed=1, digit_bits=8)
-    else:
+    elif mode == "gvr":
         got = rs.gvr_emulate(blocks, s=0, seed=1, digit_bits=8)
+    else:
+        got = rs.pr_emulate(blocks)
+        got.update(counts=np.zeros((p, p), dtype=np.uint64), n_out=[N] * p)
     torch.cuda.synchronize()
 L.rs_timing_enable(0)
 sort_ms = sum(q(x)[0] for x in ("hist", "plan", "onesweep", "final_copy"))
 merge_ms = sum(q(x)[0] for x in ("merge_split", "merge_tile"))
-gsd_ms = sum(q(x)[0] for x in ("gsd_sample", "gsd_splitters", "gsd_split", "ger_sample", "gvr_split"))
+gsd_ms = sum(q(x)[0] for x in ("gsd_sample", "gsd_splitters", "gsd_split", "ger_sample", "gvr_split", "pr_pull"))
 all_ms = q("")[0] - q("gsd_pull_merge")[0]  # the pull scope wraps kernels timed on their own
 ex_ms = q("gsd_exchange")[0]
 counts = got["counts"].astype(np.int64)

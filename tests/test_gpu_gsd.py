@@ -232,3 +232,33 @@ def test_pull_merge_ger_and_large(option):
     cuts = [0, 100000, 350001, 350002, 600000]
     _check_ger([a[cuts[k]:cuts[k + 1]] for k in range(4)], s=0, seed=9)
     _check([a[cuts[k]:cuts[k + 1]] for k in range(4)], r=8, b=8)
+
+
+# ---------------------------------------------------------- PR4 across GPUs ----
+@pytest.mark.parametrize("p", [1, 2, 3, 8])
+@pytest.mark.parametrize("dist", ["uniform", "mod16", "equal", "sorted"])
+def test_pr4_across_ranks_matches_the_sort(p, dist):
+    """PR4 routing (PAPER.md:685-709, SPEC.md:206 rank formula; rs_pr_emulate):
+    after the four rounds rank j holds exactly positions [off_j, off_j + n_j) of
+    the stable sorted order — the oracle's SR4 result sliced by the input sizes."""
+    sizes = [7000 + 1311 * k for k in range(p)]
+    a = inputs.gen_u32(sum(sizes), 150 + p, dist)
+    cuts = np.concatenate([[0], np.cumsum(sizes)])
+    blocks = [a[cuts[k]:cuts[k + 1]] for k in range(p)]
+    got = rs.pr_emulate([dev(x) for x in blocks])
+    want = oracle.sr(a, 8)
+    for j in range(p):
+        assert (host(got["Y"][j], np.uint32) == want[cuts[j]:cuts[j + 1]]).all(), j
+
+
+def test_pr4_pairs_stability_u64_uneven_and_empty_blocks():
+    sizes = [0, 20000, 3, 0, 15001]
+    k = inputs.gen_u64(sum(sizes), 151, "mod1024")
+    v = inputs.iota_u32(k.size)
+    cuts = np.concatenate([[0], np.cumsum(sizes)])
+    got = rs.pr_emulate([dev(k[cuts[i]:cuts[i + 1]]) for i in range(5)],
+                        vals=[dev(v[cuts[i]:cuts[i + 1]]) for i in range(5)])
+    wk, wv = oracle.sr(k, 8, vals=v)
+    for j in range(5):
+        assert (host(got["Y"][j], np.uint64) == wk[cuts[j]:cuts[j + 1]]).all(), j
+        assert (host(got["Yv"][j], np.uint32) == wv[cuts[j]:cuts[j + 1]]).all(), j

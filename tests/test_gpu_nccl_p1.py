@@ -118,3 +118,20 @@ def test_collective_validation_errors(comm):
     # the communicator still works afterwards
     y = rs.sort(a, comm=comm)
     assert (host(y, np.uint32) == np.sort(host(a, np.uint32))).all()
+
+
+def test_pr4_p1_through_nccl(comm):
+    """PR4 routing selected on the communicator: at p = 1 every round pulls the
+    whole locally sorted block from itself (no IPC mapping needed)."""
+    comm.set_sampling("pr4")
+    try:
+        k = inputs.gen_u64(30001, 66, "mod1024")
+        v = inputs.iota_u32(k.size)
+        yk, yv = rs.sort_pairs(dev(k), dev(v), comm=comm)
+        wk, wv = oracle.sr(k, 8, vals=v)
+        assert (host(yk, np.uint64) == wk).all() and (host(yv, np.uint32) == wv).all()
+        a = inputs.gen_u32(50001, 67)
+        y = rs.sort(dev(a), comm=comm)
+        assert (host(y, np.uint32) == oracle.sr(a, 8)).all()
+    finally:
+        comm.set_sampling("gsd")
