@@ -484,7 +484,7 @@ static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStrea
 
 template <typename K, int C, int P>
 static rs_status_t launch_hist_lp(const K* keys, size_t n, uint32_t* hist, uint32_t* zero_ptr, size_t zero_words,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, int first = 0) {
     constexpr int T = 1024;
     constexpr size_t smem = (size_t)P * 256 * C * 4;
     auto kern = k_digit_hist_lp<K, T, C, P>;
@@ -494,13 +494,25 @@ static rs_status_t launch_hist_lp(const K* keys, size_t n, uint32_t* hist, uint3
         attr = true;
     }
     LaunchScope ls("hist", st);
-    kern<<<sm_count(), T, smem, st>>>(keys, n, hist, zero_ptr, zero_words);
+    kern<<<sm_count(), T, smem, st>>>(keys, n, hist + (size_t)first * 256, zero_ptr, zero_words, 8 * first);
     return RS_OK;
 }
 
+// histograms of passes [first, P) (rows first.. of hist); first > 0 only with
+// the lane-private kernel (single-digit rounds of PR4 across GPUs)
 template <typename K>
 static rs_status_t launch_hist(const K* keys, size_t n, int P, uint32_t* hist,
-                               uint32_t* zero_ptr, size_t zero_words, cudaStream_t st) {
+                               uint32_t* zero_ptr, size_t zero_words, cudaStream_t st, int first = 0) {
+    if (first > 0 && !options().hist_shared) {
+        const int np = P - first;
+        switch (np) {
+            case 1: return launch_hist_lp<K, 32, 1>(keys, n, hist, zero_ptr, zero_words, st, first);
+            case 2: return launch_hist_lp<K, 32, 2>(keys, n, hist, zero_ptr, zero_words, st, first);
+            case 3: return launch_hist_lp<K, 32, 3>(keys, n, hist, zero_ptr, zero_words, st, first);
+            case 4: return launch_hist_lp<K, 32, 4>(keys, n, hist, zero_ptr, zero_words, st, first);
+            default: break;  // more passes: count from 0 below
+        }
+    }
     if (!options().hist_shared) {
         // lane-private copies (default): C = 32 for <= 4 passes, 16 for <= 8
         switch (P) {
@@ -547,7 +559,8 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
     const Layout8 L = layout8(ws, sizeof(K), V, n, (size_t)tile_for(sizeof(K), V, design, n));
     RS_CUDA_TRY(cudaMemsetAsync(L.hist, 0, (size_t)P * 256 * 4, st));
     // K1 also zeroes the first pass's status region (as u32 words)
-    rs_status_t s = launch_hist<K>(keys_in, n, P, L.hist, static_cast<uint32_t*>(L.status), L.status_bytes / 4, st);
+    rs_status_t s = launch_hist<K>(keys_in, n, P, L.hist, static_cast<uint32_t*>(L.status), L.status_bytes / 4, st,
+                                   first_pass);
     if (s != RS_OK) return s;
     if (hist_copy)
         RS_CUDA_TRY(cudaMemcpyAsync(hist_copy, L.hist + (size_t)first_pass * 256, 256 * 4, cudaMemcpyDeviceToDevice, st));

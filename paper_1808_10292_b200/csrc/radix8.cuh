@@ -109,7 +109,8 @@ __global__ void __launch_bounds__(THREADS) k_digit_hist(const K* __restrict__ ke
 template <typename K, int THREADS, int C, int P>
 __global__ void __launch_bounds__(THREADS, 1) k_digit_hist_lp(const K* __restrict__ keys, size_t n,
                                                              uint32_t* __restrict__ hist,
-                                                             uint32_t* __restrict__ zero_ptr, size_t zero_words) {
+                                                             uint32_t* __restrict__ zero_ptr, size_t zero_words,
+                                                             int shift0 = 0) {
     extern __shared__ __align__(16) uint32_t s_h[];  // [P][256][C]
     const int tid = threadIdx.x, lane = tid & 31;
     const size_t gtid = (size_t)blockIdx.x * THREADS + tid;
@@ -123,7 +124,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_digit_hist_lp(const K* __restric
     const uint4* vbase = reinterpret_cast<const uint4*>(keys);
     auto count = [&](K k) {
 #pragma unroll
-        for (int t = 0; t < P; ++t) atomicAdd(&my[(t * 256 + digit_of<K>(k, 8 * t, 0xFFu)) * C], 1u);
+        for (int t = 0; t < P; ++t) atomicAdd(&my[(t * 256 + digit_of<K>(k, shift0 + 8 * t, 0xFFu)) * C], 1u);
     };
     size_t v = gtid;
     for (; v + 3 * gstride < nvec; v += 4 * gstride) {  // four 16-byte loads in flight
