@@ -1,7 +1,8 @@
 """ORACLE — TEST INFRASTRUCTURE ONLY.
 
 ctypes wrapper of the plain serial C oracle (oracle/*.c), written from the paper
-(PAPER.md:653-681 SR4 count-sort rounds; Algorithm 1 GSD).
+(PAPER.md:653-681 SR4 count-sort rounds; Algorithm 1 GSD;
+PAPER.md:471-535 BTN and OET).
 Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl
 reference leg may import this package.  The product path
 (paper_1808_10292_b200/) never does, and shares no code with it.
@@ -21,7 +22,7 @@ import subprocess
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRCS = [os.path.join(_HERE, f) for f in ("sr.c", "gsd.c", "verify.c")]
+_SRCS = [os.path.join(_HERE, f) for f in ("sr.c", "gsd.c", "net.c", "verify.c")]
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
@@ -64,6 +65,12 @@ def lib():
         L.or_gvr_u64.restype = i32
         L.or_gvr_u32.argtypes = [i32, sz, u64, i32, vp, vp, vp, sz, vp, vp, vp]
         L.or_gvr_u32.restype = i32
+        for name in ("or_btn_u32", "or_oet_u32"):
+            getattr(L, name).argtypes = [i32, i32, vp, sz, i32, vp]
+            getattr(L, name).restype = i32
+        for name in ("or_btn_u64", "or_oet_u64"):
+            getattr(L, name).argtypes = [i32, i32, vp, vp, sz, i32, vp]
+            getattr(L, name).restype = i32
         L.or_splitmix64_at.argtypes = [u64, u64]
         L.or_splitmix64_at.restype = u64
         for name in ("or_is_nondecreasing_u32", "or_is_nondecreasing_u64"):
@@ -148,6 +155,47 @@ def gvr(shards, s: int, seed: int, b: int = 8, vals=None, cap: int | None = None
 
 def splitmix64_at(seed: int, i: int) -> int:
     return int(lib().or_splitmix64_at(seed, i))
+
+
+def _net(mode, blocks, b, vals, max_stages):
+    p = len(blocks)
+    N = blocks[0].size if p else 0
+    if any(x.size != N for x in blocks):
+        raise ValueError("BTN/OET need equal block sizes (reading R34)")
+    is32 = blocks[0].dtype == np.uint32
+    dt = np.uint32 if is32 else np.uint64
+    K = np.ascontiguousarray(np.concatenate([np.asarray(x, dtype=dt) for x in blocks]) if p else
+                             np.empty(0, dt))
+    Vv = None
+    if vals is not None:
+        assert not is32, "values ride with u64 keys"
+        Vv = np.ascontiguousarray(np.concatenate([np.asarray(v, dtype=np.uint32) for v in vals]))
+    st = ctypes.c_int(0)
+    L = lib()
+    if is32:
+        assert vals is None
+        fn = L.or_btn_u32 if mode == 0 else L.or_oet_u32
+        rc = fn(p, b, K.ctypes.data, N, max_stages, ctypes.byref(st))
+    else:
+        fn = L.or_btn_u64 if mode == 0 else L.or_oet_u64
+        rc = fn(p, b, K.ctypes.data, None if Vv is None else Vv.ctypes.data, N, max_stages, ctypes.byref(st))
+    if rc:
+        raise ValueError("BTN needs p a power of two" if mode == 0 else "bad OET arguments")
+    out = dict(Y=[K[k * N:(k + 1) * N] for k in range(p)], stages=st.value)
+    out["Yv"] = None if Vv is None else [Vv[k * N:(k + 1) * N] for k in range(p)]
+    return out
+
+
+def btn(blocks, b: int = 8, vals=None, max_stages: int = -1):
+    """BTN: local SR-b of each equal-size block, then the
+    lg p (lg p + 1)/2-stage bitonic merge-split network.  Returns dict(Y, Yv, stages)."""
+    return _net(0, blocks, b, vals, max_stages)
+
+
+def oet(blocks, b: int = 8, vals=None, max_stages: int = -1):
+    """OET: local SR-b, then p rounds of odd-even transposition
+    merge-splits.  Returns dict(Y, Yv, stages)."""
+    return _net(1, blocks, b, vals, max_stages)
 
 
 def _sample_sort(shards, mode, r_or_s, seed, b, vals, cap):

@@ -13,6 +13,8 @@
  *   gsd.c     GSD: deterministic regular oversampling sort, simulated for p
  *             processors in one process (Algorithm 1), and
  *             GER, its random-oversampling variant.
+ *   net.c     BTN and OET: bitonic / odd-even transposition merge-split
+ *             networks over p sorted blocks.
  *   verify.c  invariants: nondecreasing order, multiset hash, pair stability.
  *
  * Pins (tests/test_oracle.py, tests/test_oracle_gsd.py): library sort
@@ -80,6 +82,17 @@ int or_gvr_u32(int p, size_t s, uint64_t seed, int b,
                uint64_t* splitters, uint64_t* counts);
 /* the i-th output of SplitMix64 seeded `seed` (the generator GER draws with) */
 uint64_t or_splitmix64_at(uint64_t seed, uint64_t i);
+
+/* ---- net.c ---------------------------------------------------------------- */
+/* BTN and OET over p blocks of N keys held
+ * contiguously in keys[] (block k at k·N), in place: SR-b of every block, then
+ * the merge-split network (readings R32-R34).  max_stages >= 0 stops after that
+ * many stages (BTN) / rounds (OET); *stages = the number executed.  vals (u64
+ * only) may be NULL.  Returns 0, or -1 (bad argument; BTN: p not a power of 2). */
+int or_btn_u32(int p, int b, uint32_t* keys, size_t N, int max_stages, int* stages);
+int or_btn_u64(int p, int b, uint64_t* keys, uint32_t* vals, size_t N, int max_stages, int* stages);
+int or_oet_u32(int p, int b, uint32_t* keys, size_t N, int max_stages, int* stages);
+int or_oet_u64(int p, int b, uint64_t* keys, uint32_t* vals, size_t N, int max_stages, int* stages);
 
 /* ---- verify.c ------------------------------------------------------------ */
 int or_is_nondecreasing_u32(const uint32_t* a, size_t n);
