@@ -156,6 +156,32 @@ size_t rs_pr_emulate_ws_bytes(int key_bytes, int val_bytes, int p, size_t n_max)
 rs_status_t rs_pr_emulate(int key_bytes, int p, void* const* keys, uint32_t* const* vals, const size_t* n,
                           void* const* out_keys, uint32_t* const* out_vals, void* ws, size_t ws_bytes,
                           void* stream);
+/* modes 4 and 5 (network sorts; costs PAPER.md:717-763):
+ * every rank sorts its block locally (the SR-b above), then the ranks run the
+ * p-processor merge-split network over their sorted blocks — mode 4 BTN, the
+ * lg p (lg p + 1)/2-stage bitonic network (p must be a power of two), mode 5
+ * OET, p rounds of odd-even transposition (round t pairs (0,1),(2,3),… for even
+ * t, (1,2),(3,4),… for odd t).  In a BTN stage k (1-based), substage j, rank i
+ * pairs with i XOR 2^(j−1) and the pair is ascending iff bit k of i is 0; an
+ * ascending pair gives the smaller n keys to the lower rank, a descending pair to
+ * the higher (R32-R34).  Each rank computes only its own half of the
+ * merge, reading its partner's current block in place over NVLink (CUDA IPC;
+ * every rank must be able to map its peers' workspace, else RS_ECUDA on every
+ * rank).  Every rank must pass the same n (else RS_EINVAL on every rank); rank j
+ * ends with positions [j·n, (j+1)·n) of the sorted order, so out_cap ≥ n.  Ties
+ * merge the lower-indexed block first: OET keeps pairs stable, BTN only moves
+ * each value with its key.  The workspace must be one cudaMalloc'd allocation
+ * region (it is exported whole); rs_ws_bytes sizes it.
+ * rs_net_stages: the number of stages (BTN) / rounds (OET) for p ranks, −1 if
+ * p is invalid for the mode.  rs_net_emulate runs all p ranks on this GPU:
+ * keys[k] / vals[k] (N each, vals NULL or u32 values of every block; read only),
+ * out_keys[j] / out_vals[j] (N each), ws of rs_net_emulate_ws_bytes (device,
+ * 16-byte aligned), stream-ordered, no sync. */
+int rs_net_stages(int mode, int p);
+size_t rs_net_emulate_ws_bytes(int key_bytes, int val_bytes, int p, int digit_bits, size_t N);
+rs_status_t rs_net_emulate(int mode, int key_bytes, int p, int digit_bits, void* const* keys,
+                           const uint32_t* const* vals, size_t N, void* const* out_keys,
+                           uint32_t* const* out_vals, void* ws, size_t ws_bytes, void* stream);
 /* GER's default s for n keys in all, and the Lemma-Sampling1 capacity for a
  * largest block of n_local_max keys over p ranks (s = 0: the default s). */
 size_t rs_ger_default_s(uint64_t n_total);

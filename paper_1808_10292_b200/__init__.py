@@ -17,6 +17,7 @@ from . import _abi
 from ._abi import RSortError, check, lib
 
 __all__ = ["sort", "sort_pairs", "sort_bits", "digit_histogram", "workspace_bytes", "Comm", "gsd_emulate",
+           "ger_emulate", "gvr_emulate", "pr_emulate", "net_emulate", "net_stages",
            "RSortError", "lib", "rs_sort_u32", "rs_sort_u64", "rs_sort_pairs_u64_u32"]
 
 _KEY_BYTES = {torch.uint32: 4, torch.int32: 4, torch.uint64: 8, torch.int64: 8}
@@ -205,9 +206,11 @@ class Comm:
 
     def set_sampling(self, mode: str = "gsd", s: int = 0, seed: int = 0):
         """"gsd" (regular oversampling, default), "ger" (random oversampling
-        with s samples per rank, s = 0 the paper's choice, SplitMix64 seed) or
-        "gvr" (the same sample, split before sorting)."""
-        m = {"gsd": 0, "ger": 1, "gvr": 2, "pr4": 3}[mode]
+        with s samples per rank, s = 0 the paper's choice, SplitMix64 seed),
+        "gvr" (the same sample, split before sorting), "pr4" (PR4 routing across
+        GPUs), "btn" / "oet" (the bitonic / odd-even transposition merge-split
+        networks over equal sorted blocks)."""
+        m = {"gsd": 0, "ger": 1, "gvr": 2, "pr4": 3, "btn": 4, "oet": 5}[mode]
         check(lib().rs_comm_set_sampling(self.handle, m, s, seed), "rs_comm_set_sampling")
         self.sampling = mode
 
@@ -270,6 +273,38 @@ def pr_emulate(blocks: list[torch.Tensor], vals: list[torch.Tensor] | None = Non
                               ws.data_ptr(), ws.numel(), _stream(stream)), "rs_pr_emulate")
     return dict(Y=[outs[j][: n[j]] for j in range(p)],
                 Yv=[vouts[j][: n[j]] for j in range(p)] if vals is not None else None)
+
+
+def net_stages(mode: str, p: int) -> int:
+    """Stages of BTN (lg p (lg p + 1)/2) or rounds of OET (p) for p ranks."""
+    st = lib().rs_net_stages({"btn": 4, "oet": 5}[mode], p)
+    if st < 0:
+        raise ValueError(f"{mode} is not defined for p = {p}")
+    return st
+
+
+def net_emulate(mode: str, blocks: list[torch.Tensor], digit_bits: int = 8,
+                vals: list[torch.Tensor] | None = None, stream=None):
+    """BTN ("btn") or OET ("oet") over p = len(blocks) ranks held on this GPU:
+    local radix sort of every block, then the merge-split network.
+    Blocks must have equal sizes; they are read only.  Returns dict(Y, Yv)."""
+    p = len(blocks)
+    kb = _KEY_BYTES[blocks[0].dtype]
+    N = blocks[0].numel()
+    if any(b.numel() != N for b in blocks):
+        raise ValueError("BTN/OET need equal block sizes")
+    dev = blocks[0].device
+    outs = [torch.empty(max(N, 1), dtype=blocks[0].dtype, device=dev) for _ in range(p)]
+    vouts = [torch.empty(max(N, 1), dtype=torch.int32, device=dev) for _ in range(p)] if vals is not None else None
+    vb = 4 if vals is not None else 0
+    ws = _workspace(lib().rs_net_emulate_ws_bytes(kb, vb, p, digit_bits, N), dev)
+    arr = ctypes.c_void_p * p
+    check(lib().rs_net_emulate({"btn": 4, "oet": 5}[mode], kb, p, digit_bits, arr(*[b.data_ptr() for b in blocks]),
+                               arr(*[v.data_ptr() for v in vals]) if vals is not None else None, N,
+                               arr(*[o.data_ptr() for o in outs]),
+                               arr(*[o.data_ptr() for o in vouts]) if vals is not None else None,
+                               ws.data_ptr(), ws.numel(), _stream(stream)), "rs_net_emulate")
+    return dict(Y=[o[:N] for o in outs], Yv=[o[:N] for o in vouts] if vals is not None else None)
 
 
 def gvr_emulate(blocks: list[torch.Tensor], s: int = 0, seed: int = 0, digit_bits: int = 8,

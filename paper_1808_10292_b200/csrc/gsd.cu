@@ -317,13 +317,14 @@ static size_t ger_capacity_for(size_t n_local_max, int p, size_t s) {
 static size_t ger_s_for(Comm* c, uint64_t n_total) { return c->ger_s ? c->ger_s : ger_default_s(n_total); }
 
 size_t gsd_capacity(Comm* c, size_t n_local_max) {
-    if (c->sampling == 3) return n_local_max;  // PR4: rank j receives exactly its input size
+    if (c->sampling >= 3) return n_local_max;  // PR4 / BTN / OET: rank j ends with exactly its input size
     if (c->sampling >= 1) return ger_capacity_for(n_local_max, c->nranks, ger_s_for(c, (uint64_t)n_local_max * c->nranks));
     return capacity_for(n_local_max, c->r, c->nranks);
 }
 
 size_t gsd_ws_bytes(Comm* c, int key_bytes, bool has_val, size_t n_local_max, int b) {
     if (c->sampling == 3) return pr_ws_bytes(key_bytes, has_val, n_local_max, c->nranks);
+    if (c->sampling >= 4) return net_ws_bytes(key_bytes, has_val, n_local_max, b);
     const size_t cap = gsd_capacity(c, n_local_max);
     const size_t M = c->sampling >= 1 ? ger_draws(ger_s_for(c, (uint64_t)n_local_max * c->nranks), c->nranks) : 0;
     return gsd_layout(nullptr, key_bytes, has_val, n_local_max, cap, b, c->nranks, c->r, 1, M, c->sampling == 2).bytes;
@@ -504,6 +505,18 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
             if (hk[6] < hk[7]) return fail(RS_ECAPACITY, "PR: out_cap < n on rank " + std::to_string(k));
         }
         return pr_sort(c, key_bytes, keys, vals, n, out, vout, n_out, ws, n_all, st);
+    }
+    if (c->sampling >= 4) {  // BTN / OET: equal blocks (reading R34), agreed here
+        if (c->sampling == 4 && (p & (p - 1))) return fail(RS_EINVAL, "BTN needs a power-of-two number of ranks");
+        for (int k = 0; k < p; ++k) {
+            const uint64_t* hk = h + (size_t)k * kHdrWords;
+            if (hk[7] != n) return fail(RS_EINVAL, "BTN/OET need the same n on every rank (rank " +
+                                                       std::to_string(k) + ")");
+            if (hk[8] < net_ws_bytes(key_bytes, hv, hk[7], b))
+                return fail(RS_EINVAL, "BTN/OET workspace of rank " + std::to_string(k) + " too small");
+            if (hk[6] < hk[7]) return fail(RS_ECAPACITY, "BTN/OET: out_cap < n on rank " + std::to_string(k));
+        }
+        return net_sort(c, key_bytes, keys, vals, n, b, out, vout, n_out, ws, st);
     }
     if (!ger && (size_t)p * s > (size_t)kMaxSample)
         return fail(RS_EINVAL, "r*p^2 exceeds the one-CTA sample sort limit of 8192");
@@ -981,7 +994,7 @@ size_t rs_ger_capacity(size_t n_local_max, int p, size_t s) {
 size_t rs_ger_default_s(uint64_t n_total) { return ger_default_s(n_total); }
 
 rs_status_t rs_comm_set_sampling(void* comm, int mode, size_t s, uint64_t seed) {
-    if (!comm || mode < 0 || mode > 3) return fail(RS_EINVAL, "bad comm / sampling mode");
+    if (!comm || mode < 0 || mode > 5) return fail(RS_EINVAL, "bad comm / sampling mode");
     Comm* c = static_cast<Comm*>(comm);
     c->sampling = mode;
     c->ger_s = s;

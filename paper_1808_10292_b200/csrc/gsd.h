@@ -16,7 +16,8 @@ struct Comm {
     int rank = 0, nranks = 1, device = 0;
     int r = 8;                     // oversampling factor, s = r·p
     int sampling = 0;              // 0 GSD (regular), 1 GER (random),
-                                   // 2 GVR, 3 PR4 routing
+                                   // 2 GVR, 3 PR4 routing,
+                                   // 4 BTN, 5 OET
     size_t ger_s = 0;              // GER: samples per rank (s·p − 1 in all); 0 = 2⌈ω⌉²⌈lg n⌉, ω = lg lg n
     uint64_t ger_seed = 0;         // GER: SplitMix64 seed of the sample draws
     uint64_t* h_pinned = nullptr;  // p*p counts + headers (pinned host)
@@ -45,6 +46,11 @@ size_t ger_default_s(uint64_t n_total);
 size_t pr_ws_bytes(int key_bytes, bool hv, size_t n_local_max, int p);
 rs_status_t pr_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t n, void* out, uint32_t* vout,
                     size_t* n_out, void* ws, const std::vector<uint64_t>& n_all, cudaStream_t st);
+
+// BTN / OET across GPUs (net.cu; Comm::sampling = 4 / 5)
+size_t net_ws_bytes(int key_bytes, bool hv, size_t n_local, int b);
+rs_status_t net_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t n, int b, void* out, uint32_t* vout,
+                     size_t* n_out, void* ws, cudaStream_t st);
 
 size_t gsd_capacity(Comm* c, size_t n_local_max);
 size_t gsd_ws_bytes(Comm* c, int key_bytes, bool has_val, size_t n_local_max, int b);

@@ -40,10 +40,10 @@ __device__ __forceinline__ size_t corank(const K* A, size_t na, const K* B, size
 
 template <typename K>
 __global__ void k_merge_split(const K* __restrict__ A, size_t na, const K* __restrict__ B, size_t nb, size_t ntiles,
-                              size_t* __restrict__ split) {
+                              size_t d_base, size_t d_end, size_t* __restrict__ split) {
     const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (t > ntiles) return;
-    const size_t diag = min(t * (size_t)kMTile, na + nb);
+    const size_t diag = min(d_base + t * (size_t)kMTile, d_end);
     split[t] = corank<K>(A, na, B, nb, diag);
 }
 
@@ -55,16 +55,19 @@ constexpr int kMTilePad = kMTile + kMTile / 32 + 1;
 template <typename K, bool V>
 __global__ void __launch_bounds__(kMT) k_merge_tile(const K* __restrict__ A, const uint32_t* __restrict__ VA, size_t na,
                                                     const K* __restrict__ B, const uint32_t* __restrict__ VB, size_t nb,
-                                                    const size_t* __restrict__ split, K* __restrict__ out,
-                                                    uint32_t* __restrict__ vout) {
+                                                    const size_t* __restrict__ split, size_t d_base, size_t d_end,
+                                                    K* __restrict__ out, uint32_t* __restrict__ vout) {
     // s_k: A segment then B segment (padded index); reused for the merged tile
     extern __shared__ __align__(16) unsigned char merge_smem[];
     K* s_k = reinterpret_cast<K*>(merge_smem);
     uint32_t* s_v = reinterpret_cast<uint32_t*>(merge_smem + (size_t)kMTilePad * sizeof(K));
     const size_t t = blockIdx.x;
-    const size_t d0 = t * (size_t)kMTile, d1 = min(d0 + kMTile, na + nb);
+    // merged positions [d0, d1) of the diagonal range [d_base, d_end) -> out[d - d_base]
+    const size_t d0 = d_base + t * (size_t)kMTile, d1 = min(d0 + kMTile, d_end);
     const size_t a0 = split[t], a1 = split[t + 1];
     const size_t b0 = d0 - a0, b1 = d1 - a1;
+    out += d0 - d_base;
+    if (V) vout += d0 - d_base;
     const int la = (int)(a1 - a0), lb = (int)(b1 - b0), len = la + lb;
     // stage a segment: scalar head up to 16-byte alignment, 16-byte vector body, scalar tail
     auto stage = [&](const K* src, size_t s0, int l, int at) {
@@ -129,36 +132,36 @@ __global__ void __launch_bounds__(kMT) k_merge_tile(const K* __restrict__ A, con
     __syncthreads();
     // store: scalar head up to 16-byte alignment of the destination, vector body, scalar tail
     constexpr int VE = 16 / sizeof(K);
-    const int mis = (int)((reinterpret_cast<uintptr_t>(out + d0) / sizeof(K)) % VE);
+    const int mis = (int)((reinterpret_cast<uintptr_t>(out) / sizeof(K)) % VE);
     const int head = min(len, (VE - mis) % VE);
     const int nvec = (len - head) / VE;
-    for (int i = threadIdx.x; i < head; i += kMT) out[d0 + i] = s_k[mpad(i)];
-    uint4* vo = reinterpret_cast<uint4*>(out + d0 + head);
+    for (int i = threadIdx.x; i < head; i += kMT) out[i] = s_k[mpad(i)];
+    uint4* vo = reinterpret_cast<uint4*>(out + head);
     for (int v = threadIdx.x; v < nvec; v += kMT) {
         uint4 x;
         K* xs = reinterpret_cast<K*>(&x);
 #pragma unroll
         for (int e = 0; e < VE; ++e) xs[e] = s_k[mpad(head + v * VE + e)];
-        RS_DCHECK(d0 + head + (size_t)v * VE + VE <= na + nb);
+        RS_DCHECK(d0 + head + (size_t)v * VE + VE <= d_end);
         vo[v] = x;
     }
-    for (int i = head + nvec * VE + threadIdx.x; i < len; i += kMT) out[d0 + i] = s_k[mpad(i)];
+    for (int i = head + nvec * VE + threadIdx.x; i < len; i += kMT) out[i] = s_k[mpad(i)];
     if (V)
         for (int i = threadIdx.x; i < len; i += kMT) {
-            RS_DCHECK(d0 + i < na + nb);
-            vout[d0 + i] = s_v[mpad(i)];
+            RS_DCHECK(d0 + i < d_end);
+            vout[i] = s_v[mpad(i)];
         }
 }
 
+// merged positions [lo, hi) of the stable merge of A and B (ties to A) -> out[0, hi - lo)
 template <typename K, bool V>
-static rs_status_t merge2(const K* A, const uint32_t* VA, size_t na, const K* B, const uint32_t* VB, size_t nb, K* out,
-                          uint32_t* vout, size_t* split, cudaStream_t st) {
-    const size_t total = na + nb;
-    if (total == 0) return RS_OK;
-    const size_t ntiles = (total + kMTile - 1) / kMTile;
+static rs_status_t merge2_range(const K* A, const uint32_t* VA, size_t na, const K* B, const uint32_t* VB, size_t nb,
+                                size_t lo, size_t hi, K* out, uint32_t* vout, size_t* split, cudaStream_t st) {
+    if (hi <= lo) return RS_OK;
+    const size_t ntiles = (hi - lo + kMTile - 1) / kMTile;
     {
         LaunchScope ls("merge_split", st);
-        k_merge_split<K><<<(unsigned)((ntiles + 1 + 255) / 256), 256, 0, st>>>(A, na, B, nb, ntiles, split);
+        k_merge_split<K><<<(unsigned)((ntiles + 1 + 255) / 256), 256, 0, st>>>(A, na, B, nb, ntiles, lo, hi, split);
     }
     {
         const size_t smem = (size_t)kMTilePad * (sizeof(K) + (V ? 4 : 0));
@@ -168,10 +171,16 @@ static rs_status_t merge2(const K* A, const uint32_t* VA, size_t na, const K* B,
             attr = true;
         }
         LaunchScope ls("merge_tile", st);
-        k_merge_tile<K, V><<<(unsigned)ntiles, kMT, smem, st>>>(A, VA, na, B, VB, nb, split, out, vout);
+        k_merge_tile<K, V><<<(unsigned)ntiles, kMT, smem, st>>>(A, VA, na, B, VB, nb, split, lo, hi, out, vout);
     }
     RS_CUDA_TRY(cudaGetLastError());
     return RS_OK;
+}
+
+template <typename K, bool V>
+static rs_status_t merge2(const K* A, const uint32_t* VA, size_t na, const K* B, const uint32_t* VB, size_t nb, K* out,
+                          uint32_t* vout, size_t* split, cudaStream_t st) {
+    return merge2_range<K, V>(A, VA, na, B, VB, nb, 0, na + nb, out, vout, split, st);
 }
 
 size_t merge_scratch_bytes(size_t total) { return ((total + kMTile - 1) / kMTile + 2) * sizeof(size_t); }
@@ -312,6 +321,24 @@ rs_status_t merge_runs_ptrs(int key_bytes, const std::vector<const void*>& rk, c
                                                static_cast<uint64_t*>(out), vout, split, st);
     return merge_tree_ptrs<uint64_t, false>(rk, rv, len, static_cast<uint64_t*>(tmp), nullptr,
                                             static_cast<uint64_t*>(out), nullptr, split, st);
+}
+
+rs_status_t merge_range(int key_bytes, const void* A, const uint32_t* VA, size_t na, const void* B, const uint32_t* VB,
+                        size_t nb, size_t lo, size_t hi, void* out, uint32_t* vout, size_t* split, cudaStream_t st) {
+    const bool V = VA != nullptr;
+    if (key_bytes == 4) {
+        if (V)
+            return merge2_range<uint32_t, true>(static_cast<const uint32_t*>(A), VA, na, static_cast<const uint32_t*>(B),
+                                                VB, nb, lo, hi, static_cast<uint32_t*>(out), vout, split, st);
+        return merge2_range<uint32_t, false>(static_cast<const uint32_t*>(A), nullptr, na,
+                                             static_cast<const uint32_t*>(B), nullptr, nb, lo, hi,
+                                             static_cast<uint32_t*>(out), nullptr, split, st);
+    }
+    if (V)
+        return merge2_range<uint64_t, true>(static_cast<const uint64_t*>(A), VA, na, static_cast<const uint64_t*>(B), VB,
+                                            nb, lo, hi, static_cast<uint64_t*>(out), vout, split, st);
+    return merge2_range<uint64_t, false>(static_cast<const uint64_t*>(A), nullptr, na, static_cast<const uint64_t*>(B),
+                                         nullptr, nb, lo, hi, static_cast<uint64_t*>(out), nullptr, split, st);
 }
 
 rs_status_t merge_runs_tree(int key_bytes, void* runs, uint32_t* vruns, const std::vector<uint64_t>& roff, void* tmp,

@@ -20,4 +20,10 @@ rs_status_t merge_runs_ptrs(int key_bytes, const std::vector<const void*>& rk, c
                             const std::vector<uint64_t>& len, void* tmp, uint32_t* vtmp, void* out, uint32_t* vout,
                             size_t* split, cudaStream_t st);
 
+// merged positions [lo, hi) (0 <= lo <= hi <= na + nb) of the stable 2-way merge of
+// sorted A and B (ties to A) -> out[0, hi - lo): one half of a merge-split (BTN/OET).
+// A and B may be peer memory; split: merge_scratch_bytes(hi - lo).
+rs_status_t merge_range(int key_bytes, const void* A, const uint32_t* VA, size_t na, const void* B, const uint32_t* VB,
+                        size_t nb, size_t lo, size_t hi, void* out, uint32_t* vout, size_t* split, cudaStream_t st);
+
 }  // namespace rs

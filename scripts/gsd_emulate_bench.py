@@ -1,8 +1,9 @@
 """Time GSD's device phases through rs_gsd_emulate (all p ranks on one GPU, run
 rank by rank): per-rank local sort, sample/splitters/split kernels and step-5
 merge, as averages per rank.  Development aid for projecting the multi-GPU step.
-Usage: python scripts/gsd_emulate_bench.py [log2_total] [p] [merge(0 tree|1 resort|2 pull)] [gsd|ger|gvr|pr4]
-(pr4: "sample/split kernels" is the per-round pull of the routed keys)"""
+Usage: python scripts/gsd_emulate_bench.py [log2_total] [p] [merge(0 tree|1 resort|2 pull)] [gsd|ger|gvr|pr4|btn|oet]
+(pr4: "sample/split kernels" is the per-round pull of the routed keys; btn/oet:
+"merge-tree" is the merge-split stages, each rank's half per stage)"""
 import ctypes
 import os
 import sys
@@ -47,6 +48,9 @@ for it in range(3):
         got = rs.ger_emulate(blocks, s=0, seed=1, digit_bits=8)
     elif mode == "gvr":
         got = rs.gvr_emulate(blocks, s=0, seed=1, digit_bits=8)
+    elif mode in ("btn", "oet"):
+        got = rs.net_emulate(mode, blocks)
+        got.update(counts=np.zeros((p, p), dtype=np.uint64), n_out=[N] * p)
     else:
         got = rs.pr_emulate(blocks)
         got.update(counts=np.zeros((p, p), dtype=np.uint64), n_out=[N] * p)

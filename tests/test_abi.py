@@ -92,6 +92,21 @@ def test_emulate_validation(L):
                             None) == RS_EINVAL
 
 
+def test_net_host_logic(L):
+    """BTN / OET stage counts (lg p (lg p + 1)/2; OET p rounds)
+    and argument validation, all before any device work."""
+    for m in range(7):
+        assert L.rs_net_stages(4, 1 << m) == m * (m + 1) // 2
+    assert L.rs_net_stages(4, 12) == -1 and L.rs_net_stages(6, 4) == -1
+    assert [L.rs_net_stages(5, p) for p in (1, 2, 9)] == [1, 2, 9]
+    assert L.rs_net_emulate_ws_bytes(4, 0, 4, 8, 1000) > 0
+    assert L.rs_net_emulate_ws_bytes(4, 0, 4, 12, 1000) == 0
+    arr = (ctypes.c_void_p * 3)(0x10000, 0x10000, 0x10000)
+    assert L.rs_net_emulate(4, 4, 3, 8, arr, None, 10, arr, None, 0x10000, 1 << 30, None) == RS_EINVAL  # p=3
+    assert L.rs_net_emulate(5, 4, 3, 12, arr, None, 10, arr, None, 0x10000, 1 << 30, None) == RS_EINVAL
+    assert L.rs_net_emulate(5, 4, 3, 8, arr, None, 1 << 32, arr, None, 0x10000, 1 << 30, None) == RS_EINVAL
+
+
 def test_timing_api_without_gpu(L):
     L.rs_timing_reset()
     ms = ctypes.c_double(-1)

@@ -135,3 +135,22 @@ def test_pr4_p1_through_nccl(comm):
         assert (host(y, np.uint32) == oracle.sr(a, 8)).all()
     finally:
         comm.set_sampling("gsd")
+
+
+@pytest.mark.parametrize("mode", ["btn", "oet"])
+def test_net_sorts_p1_through_nccl(comm, mode):
+    """BTN / OET selected on the communicator (header validation, workspace and
+    capacity sizing through the collective path); at p = 1 the network has no
+    exchange and the result is the local sort."""
+    comm.set_sampling(mode)
+    try:
+        k = inputs.gen_u64(30001, 68, "mod1024")
+        v = inputs.iota_u32(k.size)
+        yk, yv = rs.sort_pairs(dev(k), dev(v), comm=comm)
+        wk, wv = oracle.sr(k, 8, vals=v)
+        assert (host(yk, np.uint64) == wk).all() and (host(yv, np.uint32) == wv).all()
+        a = inputs.gen_u32(50001, 69)
+        y = rs.sort(dev(a), comm=comm, digit_bits=16)
+        assert (host(y, np.uint32) == oracle.sr(a, 16)).all()
+    finally:
+        comm.set_sampling("gsd")
