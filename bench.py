@@ -204,9 +204,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sampling", default="gsd", choices=["gsd", "ger", "gvr"],
+    ap.add_argument("--sampling", default="gsd", choices=["gsd", "ger", "gvr", "pr4", "btn", "oet"],
                     help="N > 1: sample sort of the paper's §3.3 (GSD regular oversampling r=8, default; "
-                         "GER / GVR random oversampling with the paper's s)")
+                         "GER / GVR random oversampling with the paper's s), or the comparison paths "
+                         "PR4 across GPUs / BTN / OET (PAPER.md:471-535, 685-709)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -313,7 +314,7 @@ def main():
     # GSD all-to-all (N > 1): bytes that cross NVLink from the count matrix, time of
     # the grouped send/recv from events on the sort stream (max over ranks below)
     xchg = None
-    if p > 1:
+    if p > 1 and args.sampling in ("gsd", "ger", "gvr"):
         L.rs_timing_query(b"gsd_exchange", ctypes.byref(ms_q), ctypes.byref(cnt_q))
         pulled = cnt_q.value == 0  # pull merge: the transfer is the first merge level's NVLink reads
         if pulled:
@@ -431,7 +432,9 @@ def main():
         "dtype": "u32" if kind == "u32" else "u64+u32", "data": "synthetic",
         "config": {"workload": args.config, "description": desc, "n": n_total, "keys_per_gpu": n,
                    "digit_bits": b, "seed": seed, "dist": dist_name,
-                   "parallelism": (f"gsd-p{p} (r=8)" if args.sampling == "gsd" else f"{args.sampling}-p{p} (paper's s)")
+                   "parallelism": (f"gsd-p{p} (r=8)" if args.sampling == "gsd" else
+                                   f"{args.sampling}-p{p} (paper's s)" if args.sampling in ("ger", "gvr") else
+                                   f"{args.sampling}-p{p}")
                    if p > 1 else "single GPU",
                    "l2": "inputs larger than L2 (no flush)", "inputs": "resident in HBM, reset outside timed region"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
