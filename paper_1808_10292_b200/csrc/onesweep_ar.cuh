@@ -29,6 +29,8 @@
 // counter load/store round trip: per 32 keys one conflicted atomic replaces an
 // atomic + ~30 ALU instructions + a conflicted load and store.
 #pragma once
+#include <cstdio>
+
 #include "onesweep_ec.cuh"
 
 // timing ablations of design 5 (development builds only, OUTPUT INVALID):
@@ -38,13 +40,24 @@
 #endif
 // per-warp digit counters as 16-bit halves of shared words (digits 2w, 2w+1
 // share word w): 128 words per warp instead of 256, so fewer bank conflicts
+#ifndef RS_AR_EARLY_NEXT
+#define RS_AR_EARLY_NEXT 0
+#endif
+// per-phase cycle counts of thread 0 (development builds only: printf per CTA)
+#ifndef RS_AR_PROF
+#define RS_AR_PROF 0
+#endif
 #ifndef RS_AR_CT16
 #define RS_AR_CT16 1
 #endif
 // RANK2 (template): [rank] only counts (atomics without return); after [offset]
 // has turned the counters into warp start offsets, [scatter] takes each key's
 // slot from a second returning atomic (start + stable rank, lane-ordered as in
-// [rank]) — no rank registers and no counter load in the scatter
+// [rank]) — no rank registers and no counter load in the scatter.
+// RANK2 = 2: [rank] keeps the returning atomics' stable ranks, but parks them (16
+// bits each) in tensor memory with tcgen05.st instead of registers and [scatter]
+// reads them back with tcgen05.ld: one random shared-memory access per key fewer
+// than RANK2 = 1, and no rank registers (TMEM is otherwise idle in a sort)
 
 namespace rs {
 
@@ -77,7 +90,7 @@ struct OnesweepArCfg {
 //   2  as 1, but the keys are not kept: the scatter loads them again (from L2),
 //      which frees the registers for larger tiles
 template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, bool KREG_, int KSRC = 0,
-          bool RANK2 = false>
+          int RANK2 = 0>
 __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
     static_assert(KSRC != 1 || !HAS_VAL, "register tiles are for keys-only sorts");
     constexpr bool LDGK = KSRC != 0;
@@ -149,16 +162,56 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
     constexpr int WCW = W * R / (RS_AR_CT16 ? 2 : 1);  // counter words
     uint16_t* s_wc16 = reinterpret_cast<uint16_t*>(smem + C::wc_off);
     for (int i = tid; i < WCW; i += THREADS) s_wc[i] = 0;
+    constexpr bool R2A = RANK2 == 1, RTM = RANK2 == 2;
+    constexpr bool EARLY_NEXT = RS_AR_EARLY_NEXT && LDGK;  // TMA tiles need s_in free first
+    constexpr int kRankCols = (W + 3) / 4 * (KPT / 2);  // TMEM columns per lane quarter
+    static_assert(!RTM || kRankCols <= 512, "ranks must fit in 512 TMEM columns");
+    constexpr uint32_t kTmemCols = kRankCols <= 32 ? 32u : kRankCols <= 64 ? 64u : kRankCols <= 128 ? 128u
+                                                       : kRankCols <= 256 ? 256u : 512u;
+    if (RTM && warp == 0) tmem_alloc(&s_misc[60], kTmemCols);
+    if (RTM) tmem_fence_before_sync();
     __syncthreads();
+    if (RTM) tmem_fence_after_sync();
     uint32_t tile = s_misc[0];
     uint32_t phase = 0;
     static_assert(KPT % 2 == 0 && WK <= 65536, "ranks are packed two per register");
+#ifdef RS_AR_G
+    constexpr int G = KPT % RS_AR_G == 0 ? RS_AR_G : (KPT % 8 == 0 ? 8 : (KPT % 6 == 0 ? 6 : (KPT % 4 == 0 ? 4 : 2)));
+#else
     constexpr int G = KPT % 8 == 0 ? 8 : (KPT % 6 == 0 ? 6 : (KPT % 4 == 0 ? 4 : 2));  // batch of keys
+#endif
+    static_assert(G % 2 == 0 || R2A || RTM, "rank registers pack two 16-bit ranks");
     K kr[KREG ? KPT : 2];  // this thread's keys of the tile (rows j, lane)
-    uint32_t rr[RANK2 ? 1 : KPT / 2];  // stable ranks within the warp's keys of their digit, 16 bits each
+    uint32_t rr[(R2A || RTM) ? 1 : KPT / 2];  // stable ranks within the warp's keys of their digit, 16 bits each
+    // RTM: this thread's TMEM columns (lane quarter warp % 4; warps w and w + 4 side by side)
+    uint32_t tcol = 0;
+    if (RTM) tcol = s_misc[60] + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * (KPT / 2));
 
+#if RS_AR_PROF
+    unsigned long long prof_acc[5] = {0, 0, 0, 0, 0}, prof_t = clock64(), prof_tiles = 0;
+#define RS_AR_PROF_MARK(i)                                  \
+    do {                                                    \
+        const unsigned long long t_ = clock64();            \
+        prof_acc[i] += t_ - prof_t;                         \
+        prof_t = t_;                                        \
+    } while (0)
+#else
+#define RS_AR_PROF_MARK(i) \
+    do {                   \
+    } while (0)
+#endif
     while (tile < a.num_tiles) {
         const size_t base = (size_t)tile * TILE;
+#if RS_AR_PROF
+        ++prof_tiles;
+#endif
+        // EARLY_NEXT: the next tile id (and its L2 prefetch) is taken as this tile
+        // starts, so the id's global atomic round trip is off the [next] path
+        if (EARLY_NEXT && tid == 0) {
+            const uint32_t nt = atomicAdd(&ctrl->tile_ctr[a.pass], 1u);
+            s_misc[2] = nt;
+            if (nt < a.num_tiles) issue_load(nt);
+        }
         const uint32_t valid = (uint32_t)min((size_t)TILE, (size_t)a.n - base);
 
         // ---- [load] wait for the tile; ragged tail by scalar loads, all-ones padding
@@ -210,7 +263,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                 for (int i = 0; i < G; ++i) {
                     if (KREG && KSRC == 0) kr[KREG ? g + i : 0] = kk[i];
                     const uint32_t d = digit8<K>(kk[i], shift);
-                    if (RANK2) {
+                    if (R2A) {
                         atomicAdd(&wc[RS_AR_CT16 ? d >> 1 : d], RS_AR_CT16 ? 1u << ((d & 1u) << 4) : 1u);
                         rg[i] = 0;
                     } else if (RS_AR_CT16) {
@@ -220,14 +273,26 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                         rg[i] = atomicAdd(&wc[d], 1u);
                     }
                 }
-                if (!RANK2) {
+                if (RTM) {
+                    uint32_t rp[G / 2];
+#pragma unroll
+                    for (int i = 0; i < G; i += 2) rp[i / 2] = __byte_perm(rg[i], rg[i + 1], 0x5410);
+                    if (G == 8) {
+                        tmem_st4(tcol + g / 2, rp[0], rp[1 % (G / 2)], rp[2 % (G / 2)], rp[3 % (G / 2)]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < G / 2; ++i) tmem_st1(tcol + g / 2 + i, rp[i]);
+                    }
+                } else if (!R2A) {
 #pragma unroll
                     for (int i = 0; i < G; i += 2)
-                        rr[RANK2 ? 0 : (g + i) / 2] = __byte_perm(rg[i], rg[i + 1], 0x5410);
+                        rr[(R2A || RTM) ? 0 : (g + i) / 2] = __byte_perm(rg[i], rg[i + 1], 0x5410);
                 }
             }
+            if (RTM) tmem_wait_st();  // this thread reads its ranks back in [scatter]
         }
         __syncthreads();
+        RS_AR_PROF_MARK(0);
 
         // ---- [offset] thread d: tile count, in-tile offset, warp start offsets; publish
         if (tid < R) {
@@ -262,6 +327,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             }
         }
         __syncthreads();
+        RS_AR_PROF_MARK(1);
 
         // ---- [scatter] each key to its stable slot of the tile sorted by digit
         {
@@ -274,16 +340,27 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             for (int g = 0; g < ((RS_AR_ABLATE & 4) ? 0 : KPT); g += G) {
                 K kk[G];
                 uint32_t pos[G], vv[HAS_VAL ? G : 1];
+                uint32_t rq[RTM ? G / 2 : 1];
+                if (RTM) {
+                    if (G == 8) {
+                        tmem_ld4(tcol + g / 2, rq[0], rq[1 % (RTM ? G / 2 : 1)], rq[2 % (RTM ? G / 2 : 1)],
+                                 rq[3 % (RTM ? G / 2 : 1)]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < (RTM ? G / 2 : 0); ++i) tmem_ld1(tcol + g / 2 + i, rq[i]);
+                    }
+                }
 #pragma unroll
                 for (int i = 0; i < G; ++i)
                     kk[i] = KREG        ? kr[KREG ? g + i : 0]
                             : KSRC == 2 ? ((uint32_t)((g + i) * 32) < lim ? __ldcs(gk + (g + i) * 32) : ~K(0))
                                         : s_in[ibase + (g + i) * 32];
+                if (RTM) tmem_wait_ld();
 #pragma unroll
                 for (int i = 0; i < G; ++i) {
                     const int j = g + i;
                     const uint32_t d = digit8<K>(kk[i], shift);
-                    if (RANK2) {
+                    if (R2A) {
                         if (RS_AR_CT16) {
                             const uint32_t sh = (d & 1u) << 4;
                             pos[i] = (atomicAdd(&wcp[d >> 1], 1u << sh) >> sh) & 0xFFFFu;
@@ -291,8 +368,8 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                             pos[i] = atomicAdd(&wc[d], 1u);
                         }
                     } else {
-                        pos[i] = (RS_AR_CT16 ? (uint32_t)wc16[d] : wc[d]) +
-                                 ((rr[RANK2 ? 0 : j / 2] >> (16 * (j & 1))) & 0xFFFFu);
+                        const uint32_t rw = RTM ? rq[RTM ? i / 2 : 0] : rr[(R2A || RTM) ? 0 : j / 2];
+                        pos[i] = (RS_AR_CT16 ? (uint32_t)wc16[d] : wc[d]) + ((rw >> (16 * (j & 1))) & 0xFFFFu);
                     }
                     if (HAS_VAL)
                         vv[HAS_VAL ? i : 0] = KSRC == 2 ? ((uint32_t)(j * 32) < lim ? __ldcs(vsrc + base + ibase + j * 32) : 0u)
@@ -308,6 +385,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         }
 
         // ---- [look-back] one digit per thread, windowed walk over earlier tiles
+        RS_AR_PROF_MARK(2);
         if (tid < R) {
             S excl = 0;
             if (tile != 0 && (RS_AR_ABLATE & 1)) {
@@ -336,12 +414,17 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             s_gofs[tid] = a.bases[a.pass * R + tid] + (uint32_t)excl - s_texcl[tid];
         }
         __syncthreads();
+        RS_AR_PROF_MARK(3);
 
         // ---- [next] take the next tile and start its load; s_in and the counters are free
         if (tid == 0) {
-            const uint32_t nt = atomicAdd(&ctrl->tile_ctr[a.pass], 1u);
-            s_misc[0] = nt;
-            if (nt < a.num_tiles) issue_load(nt);
+            if (EARLY_NEXT) {
+                s_misc[0] = s_misc[2];
+            } else {
+                const uint32_t nt = atomicAdd(&ctrl->tile_ctr[a.pass], 1u);
+                s_misc[0] = nt;
+                if (nt < a.num_tiles) issue_load(nt);
+            }
         }
 #pragma unroll
         for (int i = 0; i < (WCW + THREADS - 1) / THREADS; ++i)
@@ -350,7 +433,11 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         // ---- [store] bucket runs leave as coalesced bursts (full tiles in batches
         // of SG loads, SG offset lookups, SG stores)
         if (valid == (uint32_t)TILE && !(RS_AR_ABLATE & 2)) {
+#ifdef RS_AR_SG
+            constexpr int SG = KPT % RS_AR_SG == 0 ? RS_AR_SG : (KPT % 8 == 0 ? 8 : (KPT % 4 == 0 ? 4 : 2));
+#else
             constexpr int SG = KPT % 8 == 0 ? 8 : (KPT % 4 == 0 ? 4 : 2);
+#endif
 #pragma unroll 1
             for (int b = 0; b < KPT; b += SG) {
                 K k[SG];
@@ -381,7 +468,23 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             }
         }
         __syncthreads();
+        RS_AR_PROF_MARK(4);
         tile = s_misc[0];
+    }
+#if RS_AR_PROF
+    if (tid == 0 && blockIdx.x % 37 == 0)
+        printf("PROF pass %d cta %d tiles %llu cycles/tile: rank %llu offset %llu scatter(t0) %llu lookback %llu store %llu\n",
+               a.pass, blockIdx.x, prof_tiles, prof_acc[0] / max(prof_tiles, 1ull), prof_acc[1] / max(prof_tiles, 1ull),
+               prof_acc[2] / max(prof_tiles, 1ull), prof_acc[3] / max(prof_tiles, 1ull), prof_acc[4] / max(prof_tiles, 1ull));
+#endif
+#undef RS_AR_PROF_MARK
+    if (RTM) {  // every rank read back and waited for: release the columns
+        tmem_fence_before_sync();
+        __syncthreads();
+        if (warp == 0) {
+            tmem_fence_after_sync();
+            tmem_dealloc(s_misc[60], kTmemCols);
+        }
     }
 }
 

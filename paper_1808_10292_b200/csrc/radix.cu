@@ -322,7 +322,8 @@ static rs_status_t launch_pass_ec_me(const PassArgs& a, size_t T, cudaStream_t s
 
 template <typename K, typename S>
 static rs_status_t launch_pass_ts(const PassArgs& a, size_t T, cudaStream_t st) {
-    using TN = TuneAr<K, false>;
+    using TA = TuneAr<K, false>;
+    using TN = TuneT<256, TA::THREADS * TA::KPT / 256, TA::MINB>;  // one thread per digit; same tile
     using C = OnesweepTsCfg<K, TN::THREADS, TN::KPT>;
     auto kern = k_onesweep_ts<K, TN::THREADS, TN::KPT, TN::MINB, S>;
     static int grid_cap = 0;
@@ -342,7 +343,7 @@ template <typename K, bool V, typename S, bool SMALL>
 static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st) {
     using TN = typename std::conditional<SMALL, TuneArSmall<K, V>, TuneAr<K, V>>::type;
     constexpr int KSRC = V ? RS_AR_KSRC_PAIRS : (sizeof(K) == 8 ? RS_AR_KSRC_U64 : RS_AR_KSRC_U32);
-    constexpr bool RANK2 = V ? RS_AR_RANK2_PAIRS : (sizeof(K) == 4 ? RS_AR_RANK2_U32 : RS_AR_RANK2_U64);
+    constexpr int RANK2 = V ? RS_AR_RANK2_PAIRS : (sizeof(K) == 4 ? RS_AR_RANK2_U32 : RS_AR_RANK2_U64);
     using C = OnesweepArCfg<K, V, TN::THREADS, TN::KPT, KSRC>;
     auto kern = k_onesweep_ar<K, V, TN::THREADS, TN::KPT, TN::MINB, S, (RS_AR_KREG == 1 || (RS_AR_KREG == 2 && V)), KSRC,
                               RANK2>;
