@@ -262,7 +262,7 @@ rs_status_t rs_gvr_emulate(int key_bytes, int p, size_t s, uint64_t seed, int di
                            void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------ CUDA IPC -- */
-/* Device-buffer mappings used by the GSD pull merge (gsd_merge = 2): export
+/* Device-buffer mappings used by the GSD pull merge (gsd_merge = 2, 3): export
  * the IPC handle (64 bytes) of the cudaMalloc allocation containing `ptr` and
  * ptr's byte offset in it; open a peer's (handle, offset) as a local pointer
  * (each handle is opened once per device and cached; rs_ipc_close_all unmaps).
@@ -289,14 +289,18 @@ rs_status_t rs_ipc_close_all(void);
  *                    sweep (rank, look-back, reorder, store).
  *   "match_every"    0, 4, 6 or 8: in the default pass (u32 keys) every k-th key is
  *                    ranked with match.any (ADU pipe) instead of ballots (ALU pipe).
- *   "gsd_merge"      GSD step 5 (all give the same Y_j): 2 = pull merge (default):
- *                    no all-to-all; the merge tree's first level reads every
- *                    peer's X_{k,j} in place over NVLink through CUDA IPC
- *                    mappings (see below; emulation: the blocks in place); if
- *                    any rank cannot export or map a block, every rank falls
- *                    back to 0 for that call.  0 = NCCL all-to-all into a
- *                    receive buffer, then the tree of stable 2-way merge-path
- *                    merges; 1 = all-to-all, then a stable radix re-sort.
+ *   "gsd_merge"      GSD step 5 (all give the same Y_j): 3 = pull merge in one
+ *                    p-way pass (default): no all-to-all; every peer's X_{k,j}
+ *                    is read in place over NVLink through CUDA IPC mappings
+ *                    (see below; emulation: the blocks in place), cut into
+ *                    chunks by a regular sample of the runs and merged chunk by
+ *                    chunk in shared memory, Y_j written once (2 ≤ p ≤ 32, else
+ *                    as 2); 2 = pull merge as a tree of 2-way merges whose first
+ *                    level reads the peers' blocks; if any rank cannot export or
+ *                    map a block, every rank falls back to 0 for that call.
+ *                    0 = NCCL all-to-all into a receive buffer, then the tree of
+ *                    stable 2-way merge-path merges; 1 = all-to-all, then a
+ *                    stable radix re-sort.
  *   "compact"        1 = default pass with 16-bit per-warp counters (smaller
  *                    shared-memory footprint; ballots only).
  *   "small_tiles"    design-5 tiles: 0 = small tiles when the input makes fewer

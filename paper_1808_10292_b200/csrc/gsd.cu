@@ -455,6 +455,19 @@ static rs_status_t merge_runs(int key_bytes, void* runs, uint32_t* vruns, const 
             return fail(RS_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(r_));        \
     } while (0)
 
+// step 5 over runs read in place (pull merge): one-pass p-way merge (gsd_merge 3)
+// when it applies and its scratch fits in the tree's, else the 2-way tree
+static rs_status_t pull_merge(int key_bytes, const std::vector<const void*>& rk, const std::vector<const uint32_t*>& rv,
+                              const std::vector<uint64_t>& len, const GsdLayout& L, size_t cap, void* out,
+                              uint32_t* vout, cudaStream_t st) {
+    uint64_t total = 0;
+    for (uint64_t l : len) total += l;
+    if (options().gsd_merge == 3 && pway_applicable((int)len.size(), len) &&
+        pway_scratch_bytes(key_bytes, total, (int)len.size()) <= cap * (size_t)key_bytes)
+        return merge_pway(key_bytes, rk, rv, len, L.merge_keys, cap * (size_t)key_bytes, out, vout, st);
+    return merge_runs_ptrs(key_bytes, rk, rv, len, L.merge_keys, L.merge_vals, out, vout, L.merge_split, st);
+}
+
 rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t n, int b, void* out, uint32_t* vout,
                      size_t out_cap, size_t* n_out, void* ws, size_t ws_bytes, cudaStream_t st,
                      rs_status_t local_status) {
@@ -584,7 +597,7 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
     // tree's first level reads the peers' X_{k,j} in place over NVLink through
     // CUDA IPC mappings exchanged now (falls back to the all-to-all on every
     // rank if any rank cannot export its block, e.g. VMM memory)
-    if (options().gsd_merge == 2 && !gvr && p > 1) {
+    if (options().gsd_merge >= 2 && !gvr && p > 1) {
         uint64_t* rec = h;
         std::memset(rec, 0, kIpcWords * 8);
         bool ok = ipc_export(keys, rec, &rec[8]) == RS_OK;
@@ -626,8 +639,7 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
         if (all_ok) {
             {
                 LaunchScope ls("gsd_pull_merge", st, false);
-                if ((sst = merge_runs_ptrs(key_bytes, rk, rv, len, L.merge_keys, L.merge_vals, out, vout,
-                                           L.merge_split, st)) != RS_OK)
+                if ((sst = pull_merge(key_bytes, rk, rv, len, L, out_cap, out, vout, st)) != RS_OK)
                     return sst;
             }
             // no rank may reuse its block before every peer has read its slices
@@ -886,7 +898,7 @@ static rs_status_t emulate(int mode, int key_bytes, int p, int r, size_t ger_s, 
             n_out[j] = tot;
         }
     }
-    if (mode != 2 && options().gsd_merge == 2 && p > 1) {  // pull merge: the blocks are read in place
+    if (mode != 2 && options().gsd_merge >= 2 && p > 1) {  // pull merge: the blocks are read in place
         for (int j = 0; j < p; ++j) {
             std::vector<const void*> rk(p);
             std::vector<const uint32_t*> rv(hv ? p : 0);
@@ -898,8 +910,8 @@ static rs_status_t emulate(int mode, int key_bytes, int p, int r, size_t ger_s, 
                 if (hv) rv[k] = vals[k] + so;
             }
             LaunchScope ls("gsd_pull_merge", st, false);
-            if ((sst = merge_runs_ptrs(key_bytes, rk, rv, len, L.merge_keys, L.merge_vals, out_keys[j],
-                                       hv ? out_vals[j] : nullptr, L.merge_split, st)) != RS_OK)
+            if ((sst = pull_merge(key_bytes, rk, rv, len, L, out_cap, out_keys[j], hv ? out_vals[j] : nullptr,
+                                  st)) != RS_OK)
                 return sst;
         }
         RS_CUDA_TRY(cudaGetLastError());

@@ -26,4 +26,12 @@ rs_status_t merge_runs_ptrs(int key_bytes, const std::vector<const void*>& rk, c
 rs_status_t merge_range(int key_bytes, const void* A, const uint32_t* VA, size_t na, const void* B, const uint32_t* VB,
                         size_t nb, size_t lo, size_t hi, void* out, uint32_t* vout, size_t* split, cudaStream_t st);
 
+// one-pass stable p-way merge (pwmerge.cu): runs at rk[k] (+ rv[k]) of len[k],
+// read only (peer memory allowed) -> out (+ vout); 2 <= p <= 32, each run < 2^31.
+bool pway_applicable(int p, const std::vector<uint64_t>& len);
+size_t pway_scratch_bytes(int key_bytes, uint64_t total, int p);
+rs_status_t merge_pway(int key_bytes, const std::vector<const void*>& rk, const std::vector<const uint32_t*>& rv,
+                       const std::vector<uint64_t>& len, void* scratch, size_t scratch_bytes, void* out,
+                       uint32_t* vout, cudaStream_t st);
+
 }  // namespace rs

@@ -1,0 +1,379 @@
+// GSD step 5 as ONE pass: a stable p-way merge of p sorted runs (PAPER.md:800-803,
+// "Subsequences X_{k,j} ... are merged into Y_j using p-way merging"), reading the
+// runs wherever they are (the peers' blocks over NVLink in the pull merge) and
+// writing Y_j once — against ⌈log2 p⌉ read+write passes of the 2-way tree.
+//
+// The output is cut into chunks by a regular sample of the runs, the same device
+// the paper uses one level up (GSD's own splitters):
+//   1 k_pw_sample  every m-th element of run k (the last of each m-block) becomes
+//                  a sample, tagged (k, t);
+//   2 the p sorted sample lists are merged (merge_runs_tree: composite order —
+//    key, then run — since ties go to the lower run) into Sm, and k_pw_pos
+//                  records where each run's samples landed;
+//   3 k_pw_bounds  chunk boundary i is the composite b_i = Sm[i·c − 1]; for every
+//                  run k, cnt[i][k] = #elements of run k that are ≤ b_i.  The
+//                  samples bracket it: if q run-k samples precede Sm position i·c,
+//                  cnt ∈ [q·m, min((q+1)·m − 1, len_k)], found by a binary search of
+//                  ≤ m elements (a handful of remote reads);
+//   4 k_pw_merge   one CTA per chunk: its p pieces [cnt[i−1][k], cnt[i][k]) are
+//                  staged in shared memory, merged there by a ⌈log2 p⌉-level tree
+//                  of merge-path merges (left = lower runs: ties stay stable), and
+//                  stored coalesced at Σ_k cnt[i−1][k].
+// A chunk holds at most c·m + p·(m − 1) elements (each run contributes its
+// bracketed samples plus less than one block), so the shared-memory tile is fixed.
+#include <algorithm>
+#include <vector>
+
+#include "common.cuh"
+#include "merge.h"
+
+namespace rs {
+namespace {
+
+#ifndef RS_PW_M
+#define RS_PW_M 128
+#endif
+#ifndef RS_PW_C
+#define RS_PW_C 0  // 0: 32 samples per chunk for 4-byte keys without values, else 16
+#endif
+#ifndef RS_PW_IT
+#define RS_PW_IT 16
+#endif
+constexpr int kPwM = RS_PW_M;  // sample stride m
+constexpr int kPwCMax = 32;     // samples per chunk c (PwRuns::c) at most
+constexpr int kPwMaxP = 32;   // runs handled by the single-pass merge (shared-memory tile)
+constexpr int kPwT = 256;     // threads per merge CTA
+
+struct PwRuns {
+    const void* k[kPwMaxP];
+    const uint32_t* v[kPwMaxP];
+    uint64_t len[kPwMaxP];
+    uint64_t soff[kPwMaxP + 1];  // sample offsets (run k's samples at [soff[k], soff[k+1]))
+    int p;
+    int c;  // samples per chunk
+};
+
+__device__ __forceinline__ int run_of(const PwRuns& R, uint64_t j) {  // soff[k] <= j < soff[k+1]
+    int lo = 0, hi = R.p - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (R.soff[mid] <= j) lo = mid;
+        else hi = mid - 1;
+    }
+    return lo;
+}
+
+template <typename K>
+__global__ void k_pw_sample(PwRuns R, K* __restrict__ sk, uint32_t* __restrict__ sv) {
+    const uint64_t M = R.soff[R.p];
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += (uint64_t)gridDim.x * blockDim.x) {
+        const int k = run_of(R, j);
+        const uint64_t t = j - R.soff[k];
+        sk[j] = static_cast<const K*>(R.k[k])[(t + 1) * kPwM - 1];
+        sv[j] = ((uint32_t)k << 24) | (uint32_t)t;
+    }
+}
+
+// pos[soff[k] + t] = merged index of run k's sample t
+__global__ void k_pw_pos(PwRuns R, const uint32_t* __restrict__ smv, uint64_t M, uint32_t* __restrict__ pos) {
+    for (uint64_t j = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; j < M; j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = smv[j];
+        pos[R.soff[v >> 24] + (v & 0xFFFFFFu)] = (uint32_t)j;
+    }
+}
+
+// cnt[i * p + k] for boundaries i = 1 .. nch-1 (rows 0 and nch are set by the host)
+template <typename K>
+__global__ void k_pw_bounds(PwRuns R, const K* __restrict__ smk, const uint32_t* __restrict__ smv,
+                            const uint32_t* __restrict__ pos, uint64_t nch, uint32_t* __restrict__ cnt) {
+    const int p = R.p;
+    const uint64_t total = (nch - 1) * (uint64_t)p;
+    for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t i = x / p + 1;
+        const int k = (int)(x % p);
+        const uint64_t bj = i * R.c - 1;  // boundary b_i = Sm[bj]
+        const K bv = smk[bj];
+        const int bk = (int)(smv[bj] >> 24);
+        const uint64_t bpos = ((uint64_t)(smv[bj] & 0xFFFFFFu) + 1) * kPwM - 1;
+        // q = run-k samples with merged index < i·c
+        const uint32_t* pk = pos + R.soff[k];
+        uint64_t lo = 0, hi = R.soff[k + 1] - R.soff[k];
+        while (lo < hi) {
+            const uint64_t mid = (lo + hi) >> 1;
+            if (pk[mid] < i * R.c) lo = mid + 1;
+            else hi = mid;
+        }
+        const uint64_t q = lo;
+        const K* rk = static_cast<const K*>(R.k[k]);
+        uint64_t a = q * kPwM, b = min((q + 1) * kPwM - 1, R.len[k]);  // answer in [a, b]
+        while (a < b) {  // first position whose element is > b_i (composite)
+            const uint64_t mid = (a + b) >> 1;
+            const K e = rk[mid];
+            const bool le = e < bv || (e == bv && (k < bk || (k == bk && mid <= bpos)));
+            if (le) a = mid + 1;
+            else b = mid;
+        }
+        cnt[i * p + k] = (uint32_t)a;
+    }
+}
+
+__device__ __forceinline__ int pw_pad(int i) { return i + (i >> 5); }
+
+template <typename K, bool V>
+__global__ void __launch_bounds__(kPwT) k_pw_merge(PwRuns R, const uint32_t* __restrict__ cnt, int cap,
+                                                   K* __restrict__ out, uint32_t* __restrict__ vout) {
+    extern __shared__ __align__(16) unsigned char pw_smem[];
+    K* X = reinterpret_cast<K*>(pw_smem);
+    K* Y = X + cap;
+    uint32_t* XV = reinterpret_cast<uint32_t*>(Y + cap);
+    uint32_t* YV = XV + (V ? cap : 0);
+    __shared__ uint32_t s_seg[kPwMaxP + 1];  // piece offsets in the chunk
+    __shared__ uint32_t s_src[kPwMaxP];      // piece start in its run
+    __shared__ uint64_t s_o;
+    __shared__ const void* s_rk[kPwMaxP];
+    __shared__ const uint32_t* s_rv[kPwMaxP];
+    const int p = R.p, tid = threadIdx.x;
+    const uint64_t i = blockIdx.x;
+    // piece table: lanes k < p of warp 0 load their bounds in parallel, one warp scan
+    if (tid < 32) {
+        uint32_t c0 = 0, len = 0;
+        if (tid < p) {
+            c0 = cnt[i * p + tid];
+            len = cnt[(i + 1) * p + tid] - c0;
+        }
+        uint32_t incl = len;
+        uint64_t o = c0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+            if (tid >= d) incl += y;
+            o += __shfl_xor_sync(0xffffffffu, o, d);
+        }
+        if (tid < p) {
+            s_seg[tid] = incl - len;
+            s_src[tid] = c0;
+            s_rk[tid] = R.k[tid];
+            s_rv[tid] = R.v[tid];
+        }
+        if (tid == p - 1) s_seg[p] = incl;
+        if (tid == 0) s_o = o;
+    }
+    __syncthreads();
+    const int E = (int)s_seg[p];
+    RS_DCHECK(pw_pad(E) <= cap);
+    // stage the pieces: warp w copies pieces w, w + 8, ...; each lane keeps SB
+    // independent (remote) loads in flight before writing shared memory
+    {
+        const int warp = tid >> 5, lane = tid & 31;
+        constexpr int SB = 8;
+        for (int k = warp; k < p; k += kPwT / 32) {
+            const int s0 = (int)s_seg[k], len = (int)s_seg[k + 1] - s0;
+            const K* src = static_cast<const K*>(s_rk[k]) + s_src[k];
+            const uint32_t* vs = V ? s_rv[k] + s_src[k] : nullptr;
+            for (int b = 0; b < len; b += 32 * SB) {
+                K r[SB];
+                uint32_t rv[V ? SB : 1];
+#pragma unroll
+                for (int j = 0; j < SB; ++j) {
+                    const int e = b + j * 32 + lane;
+                    if (e < len) {
+                        r[j] = src[e];
+                        if (V) rv[V ? j : 0] = vs[e];
+                    }
+                }
+#pragma unroll
+                for (int j = 0; j < SB; ++j) {
+                    const int e = b + j * 32 + lane;
+                    if (e < len) {
+                        X[pw_pad(s0 + e)] = r[j];
+                        if (V) XV[pw_pad(s0 + e)] = rv[V ? j : 0];
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // merge tree in shared memory: segments [seg[j], seg[j+1]) -> pairs -> ...
+    // (padded indices spread the merge-path reads over the banks; each thread
+    // merges IT consecutive outputs with both heads in registers)
+    int nseg = p, stride = 1;  // current segment j covers pieces [j·stride, min((j+1)·stride, p))
+    K* src = X;
+    K* dst = Y;
+    uint32_t* vsrc = XV;
+    uint32_t* vdst = YV;
+    constexpr int IT = RS_PW_IT;  // outputs per thread per round
+    while (nseg > 1) {
+        for (int o0 = tid * IT; o0 < E; o0 += kPwT * IT) {
+            int o = o0;
+            const int oend = min(o0 + IT, E);
+            while (o < oend) {
+                // the merged pair holding output o: largest even segment index with start <= o
+                int pj = 0;
+                for (int j2 = 2; j2 < nseg; j2 += 2)
+                    if ((int)s_seg[j2 * stride] <= o) pj = j2;
+                const int a0 = (int)s_seg[pj * stride];
+                const int a1 = (int)s_seg[min((pj + 1) * stride, p)];
+                const int b1 = (int)s_seg[min((pj + 2) * stride, p)];
+                const int la = a1 - a0, lb = b1 - a1;
+                const int stop = min(oend, b1);
+                const int diag = o - a0;
+                int lo = diag > lb ? diag - lb : 0, hi = diag < la ? diag : la;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (src[pw_pad(a0 + mid)] <= src[pw_pad(a1 + diag - 1 - mid)]) lo = mid + 1;
+                    else hi = mid;
+                }
+                int ia = lo, ib = diag - lo;
+                K ha = ia < la ? src[pw_pad(a0 + ia)] : K(0), hb = ib < lb ? src[pw_pad(a1 + ib)] : K(0);
+                for (; o < stop; ++o) {  // branchless: select, advance, reload the consumed head
+                    const bool takeA = ib >= lb || (ia < la && ha <= hb);
+                    const int from = takeA ? a0 + ia : a1 + ib;
+                    dst[pw_pad(o)] = takeA ? ha : hb;
+                    if (V) vdst[pw_pad(o)] = vsrc[pw_pad(from)];
+                    ia += takeA;
+                    ib += !takeA;
+                    const bool more = takeA ? ia < la : ib < lb;
+                    const K nv = more ? src[pw_pad(from + 1)] : K(0);
+                    ha = takeA ? nv : ha;
+                    hb = takeA ? hb : nv;
+                }
+            }
+        }
+        __syncthreads();
+        nseg = (nseg + 1) / 2;
+        stride *= 2;
+        K* t = src;
+        src = dst;
+        dst = t;
+        uint32_t* tv = vsrc;
+        vsrc = vdst;
+        vdst = tv;
+    }
+    // coalesced store of the merged chunk
+    const uint64_t o = s_o;
+    for (int e = tid; e < E; e += kPwT) {
+        out[o + e] = src[pw_pad(e)];
+        if (V) vout[o + e] = vsrc[pw_pad(e)];
+    }
+}
+
+constexpr int pw_cap(int p, int c) { return c * kPwM + p * kPwM; }
+constexpr int pw_cap_padded(int p, int c) { return pw_cap(p, c) + pw_cap(p, c) / 32 + 1; }
+int pw_c(int key_bytes, bool hv) { return RS_PW_C ? RS_PW_C : (key_bytes == 4 && !hv ? 32 : 16); }
+
+struct PwLayout {
+    void *sk, *tk, *mk;       // samples, tree scratch, merged samples (M keys each)
+    uint32_t *sv, *tv, *mv;   // their tags
+    uint32_t* pos;            // M
+    uint32_t* cnt;            // (nch + 1) * p
+    size_t* split;            // merge_runs_tree co-rank scratch
+    size_t bytes;
+};
+
+PwLayout pw_layout(void* ws, int key_bytes, uint64_t M, uint64_t nch, int p) {
+    PwLayout L{};
+    Carver c(ws);
+    const size_t M1 = std::max<uint64_t>(M, 1);
+    L.sk = c.take(M1 * key_bytes);
+    L.tk = c.take(M1 * key_bytes);
+    L.mk = c.take(M1 * key_bytes);
+    L.sv = static_cast<uint32_t*>(c.take(M1 * 4));
+    L.tv = static_cast<uint32_t*>(c.take(M1 * 4));
+    L.mv = static_cast<uint32_t*>(c.take(M1 * 4));
+    L.pos = static_cast<uint32_t*>(c.take(M1 * 4));
+    L.cnt = static_cast<uint32_t*>(c.take((nch + 1) * (size_t)p * 4));
+    L.split = static_cast<size_t*>(c.take(merge_scratch_bytes(M1)));
+    L.bytes = c.used();
+    return L;
+}
+
+template <typename K, bool V>
+rs_status_t pway(const PwRuns& R, uint64_t M, void* scratch, K* out, uint32_t* vout, cudaStream_t st) {
+    const int p = R.p;
+    const uint64_t nch = std::max<uint64_t>(1, (M + R.c - 1) / R.c);
+    const PwLayout L = pw_layout(scratch, sizeof(K), M, nch, p);
+    const unsigned g = (unsigned)std::min<uint64_t>((M + 255) / 256 + 1, 8192);
+    {
+        LaunchScope ls("pw_sample", st);
+        if (M) k_pw_sample<K><<<g, 256, 0, st>>>(R, static_cast<K*>(L.sk), L.sv);
+    }
+    std::vector<uint64_t> soff(R.soff, R.soff + p + 1);
+    if (M) {
+        rs_status_t s = merge_runs_tree(sizeof(K), L.sk, L.sv, soff, L.tk, L.tv, L.mk, L.mv, L.split, st);
+        if (s != RS_OK) return s;
+        LaunchScope ls("pw_pos", st);
+        k_pw_pos<<<g, 256, 0, st>>>(R, L.mv, M, L.pos);
+    }
+    // rows 0 and nch of the count table
+    std::vector<uint32_t> edge(2 * (size_t)p);
+    for (int k = 0; k < p; ++k) {
+        edge[k] = 0;
+        edge[p + k] = (uint32_t)R.len[k];
+    }
+    RS_CUDA_TRY(cudaMemcpyAsync(L.cnt, edge.data(), p * 4, cudaMemcpyHostToDevice, st));
+    RS_CUDA_TRY(cudaMemcpyAsync(L.cnt + nch * p, edge.data() + p, p * 4, cudaMemcpyHostToDevice, st));
+    if (nch > 1) {
+        LaunchScope ls("pw_bounds", st);
+        const unsigned gb = (unsigned)std::min<uint64_t>(((nch - 1) * p + 255) / 256, 65535);
+        k_pw_bounds<K><<<gb, 256, 0, st>>>(R, static_cast<const K*>(L.mk), L.mv, L.pos, nch, L.cnt);
+    }
+    const int cap = pw_cap_padded(p, R.c);
+    const size_t smem = (size_t)cap * (2 * sizeof(K) + (V ? 8 : 0));
+    static bool attr = false;
+    if (!attr) {
+        RS_CUDA_TRY(cudaFuncSetAttribute(k_pw_merge<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)pw_cap_padded(kPwMaxP, kPwCMax) * (2 * (int)sizeof(K) + (V ? 8 : 0))));
+        attr = true;
+    }
+    {
+        LaunchScope ls("pw_merge", st);
+        k_pw_merge<K, V><<<(unsigned)nch, kPwT, smem, st>>>(R, L.cnt, cap, out, vout);
+    }
+    RS_CUDA_TRY(cudaGetLastError());  // (pageable H2D copies are staged before they return)
+    return RS_OK;
+}
+
+}  // namespace
+
+bool pway_applicable(int p, const std::vector<uint64_t>& len) {
+    if (p < 2 || p > kPwMaxP) return false;
+    for (uint64_t l : len)
+        if (l >= (1ull << 31) || l / kPwM >= (1ull << 24)) return false;
+    return true;
+}
+
+size_t pway_scratch_bytes(int key_bytes, uint64_t total, int p) {
+    const uint64_t M = total / kPwM + (uint64_t)p;
+    return pw_layout(nullptr, key_bytes, M, M + 2, p).bytes;  // nch <= M / c + 1
+}
+
+rs_status_t merge_pway(int key_bytes, const std::vector<const void*>& rk, const std::vector<const uint32_t*>& rv,
+                       const std::vector<uint64_t>& len, void* scratch, size_t scratch_bytes, void* out,
+                       uint32_t* vout, cudaStream_t st) {
+    const int p = (int)len.size();
+    if (!pway_applicable(p, len)) return fail(RS_EINVAL, "p-way merge: p out of range or a run too long");
+    PwRuns R{};
+    R.p = p;
+    R.c = pw_c(key_bytes, vout != nullptr);
+    R.soff[0] = 0;
+    uint64_t total = 0;
+    for (int k = 0; k < p; ++k) {
+        R.k[k] = rk[k];
+        R.v[k] = rv.empty() ? nullptr : rv[k];
+        R.len[k] = len[k];
+        R.soff[k + 1] = R.soff[k] + len[k] / kPwM;
+        total += len[k];
+    }
+    if (total == 0) return RS_OK;
+    const uint64_t M = R.soff[p];
+    if (scratch_bytes < pway_scratch_bytes(key_bytes, total, p)) return fail(RS_EINVAL, "p-way merge scratch too small");
+    const bool V = vout != nullptr;
+    if (key_bytes == 4)
+        return V ? pway<uint32_t, true>(R, M, scratch, static_cast<uint32_t*>(out), vout, st)
+                 : pway<uint32_t, false>(R, M, scratch, static_cast<uint32_t*>(out), nullptr, st);
+    return V ? pway<uint64_t, true>(R, M, scratch, static_cast<uint64_t*>(out), vout, st)
+             : pway<uint64_t, false>(R, M, scratch, static_cast<uint64_t*>(out), nullptr, st);
+}
+
+}  // namespace rs

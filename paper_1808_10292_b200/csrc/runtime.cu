@@ -134,7 +134,7 @@ rs_status_t rs_set_option(const char* name, long long value) {
     const std::string n(name);
     if (n == "wide_status" && value <= 1) options().wide_status = value != 0;
     else if (n == "debug_skip" && value <= 31) options().debug_skip = (unsigned)value;
-    else if (n == "gsd_merge" && value <= 2) options().gsd_merge = (int)value;
+    else if (n == "gsd_merge" && value <= 3) options().gsd_merge = (int)value;
     else if (n == "compact" && value <= 1) options().compact = value != 0;
     else if (n == "hist_shared" && value <= 1) options().hist_shared = value != 0;
     else if (n == "small_tiles" && value <= 2) options().small_tiles = (int)value;

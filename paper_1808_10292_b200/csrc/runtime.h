@@ -40,7 +40,8 @@ struct Options {
     bool wide_status = false;     // force 64-bit look-back status words (tests)
     unsigned debug_skip = 0;      // timing ablations (invalid output): 1 look-back, 2 rank, 4 store, 8 reorder
     int rank_variant = 3;         // 0 ballot peers, 1 match.any, 2 atomic-OR peers, 3 hybrid pairs
-    int gsd_merge = 2;            // GSD step 5: 0 merge tree, 1 stable radix re-sort, 2 pull merge
+    int gsd_merge = 3;            // GSD step 5: 0 merge tree, 1 stable radix re-sort, 2 pull merge (tree),
+                                  // 3 pull merge as one p-way pass (pwmerge.cu; tree when p > 32)
                                   // (the tree reads the source blocks in place: peers over NVLink)
     bool compact = false;         // design 2: 16-bit per-warp counters, ballots only (4 CTAs/SM)
     int match_every = 0;          // design 2, u32 keys: every k-th key ranked by match.any (0 = none)

@@ -96,13 +96,13 @@ def option():
         rs.lib().rs_set_option(name.encode(), value)
 
 
-@pytest.mark.parametrize("merge", [0, 1, 2])
+@pytest.mark.parametrize("merge", [0, 1, 2, 3])
 @pytest.mark.parametrize("p", [2, 3, 5, 6, 7, 8])
 def test_gsd_merge_tree_and_resort(option, merge, p):
-    """Step 5 as the merge tree (0), as a stable re-sort (1) and as the pull merge
+    """Step 5 as the merge tree (0), as a stable re-sort (1), as the pull merge
     (2: no exchange copies, the tree's first level reads every rank's block in
-    place): identical Y_j, for odd run counts too; narrow pair keys check the tie
-    rule (lower rank first)."""
+    place) and as the one-pass p-way pull merge (3): identical Y_j, for odd run
+    counts too; narrow pair keys check the tie rule (lower rank first)."""
     option("gsd_merge", merge)
     N = 9000 + 37 * p
     k = inputs.gen_u64(p * N, 70 + p, "mod1024")
@@ -225,13 +225,42 @@ def test_gvr_uneven_and_empty_blocks():
     _check_gvr([a[:0], a[:5000], a[5000:5003], a[5003:]], s=6, seed=4)
 
 
-def test_pull_merge_ger_and_large(option):
-    """The pull merge under GER sampling and over large uneven runs."""
-    option("gsd_merge", 2)
+@pytest.mark.parametrize("merge", [2, 3])
+def test_pull_merge_ger_and_large(option, merge):
+    """The pull merge (tree and p-way) under GER sampling and over large uneven runs."""
+    option("gsd_merge", merge)
     a = inputs.gen_u32(600000, 95)
     cuts = [0, 100000, 350001, 350002, 600000]
     _check_ger([a[cuts[k]:cuts[k + 1]] for k in range(4)], s=0, seed=9)
     _check([a[cuts[k]:cuts[k + 1]] for k in range(4)], r=8, b=8)
+
+
+@pytest.mark.parametrize("p", [2, 4, 16, 32])
+@pytest.mark.parametrize("dist", ["uniform", "equal", "mod16", "sorted"])
+def test_pway_merge_many_runs(option, p, dist):
+    """The one-pass p-way merge (pwmerge.cu) against the GSD simulator: many runs
+    (p up to 32, r = 8 keeps r·p² ≤ 8192), all-equal keys (every chunk boundary
+    decided by the (run, position) tie rule), sizes spanning many chunks, ragged."""
+    option("gsd_merge", 3)
+    N = 40000 + 77 * p
+    a = inputs.gen_u32(p * N, 400 + p, dist)
+    _check([a[i * N:(i + 1) * N] for i in range(p)], r=8, b=8)
+
+
+def test_pway_merge_pairs_uneven_tiny_and_empty_blocks(option):
+    """p-way merge: stable pairs over uneven blocks, including blocks shorter than
+    one sample stride and empty ones (runs with no samples)."""
+    option("gsd_merge", 3)
+    k = inputs.gen_u64(300000, 411, "mod1024")
+    v = inputs.iota_u32(k.size)
+    cuts = [0, 0, 50, 100000, 100001, 230000, 300000]
+    got = _check([k[cuts[i]:cuts[i + 1]] for i in range(6)], r=8, b=8,
+                 vals_np=[v[cuts[i]:cuts[i + 1]] for i in range(6)])
+    K = np.concatenate([host(y, np.uint64) for y in got["Y"]])
+    V = np.concatenate([host(y, np.uint32) for y in got["Yv"]])
+    assert oracle.pairs_stable(K, V)
+    small = inputs.gen_u32(700, 412)
+    _check([small[:100], small[100:300], small[300:301], small[301:]], r=8, b=8)
 
 
 # ---------------------------------------------------------- PR4 across GPUs ----
