@@ -436,7 +436,10 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
 #ifdef RS_AR_SG
             constexpr int SG = KPT % RS_AR_SG == 0 ? RS_AR_SG : (KPT % 8 == 0 ? 8 : (KPT % 4 == 0 ? 4 : 2));
 #else
-            constexpr int SG = KPT % 8 == 0 ? 8 : (KPT % 4 == 0 ? 4 : 2);
+            // 4 per batch: u32 2^27 pass 0.336 -> 0.326 ms, 2^31 and u64 / pairs unchanged;
+            // 8 was the previous default, 22 / 44 cost 5.78 / 5.73 ms at 2^31 (more
+            // stores in flight per thread make the scattered write stream slower)
+            constexpr int SG = KPT % 4 == 0 ? 4 : 2;
 #endif
 #pragma unroll 1
             for (int b = 0; b < KPT; b += SG) {
