@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(256) k_gvr_dest(const K* __restrict__ X, size_
             else hi = mid;
         }
         dest[q] = (uint32_t)lo;
-        idx[q] = (uint32_t)q;
+        if (idx) idx[q] = (uint32_t)q;
         atomicAdd(&sc[lo], 1u);
     }
     __syncthreads();
@@ -363,6 +363,17 @@ static rs_status_t gvr_partition(const GsdLayout& L, int key_bytes, const void* 
                                  int rank, int p, const Comp* S, uint64_t* counts, cudaStream_t st) {
     if (!N) return RS_OK;
     const int grid = (int)std::min<size_t>((N + 255) / 256, (size_t)sm_count() * 8);
+    if (key_bytes == 4 && !V) {
+        // u32 keys: the keys themselves ride as the values of one stable radix pass
+        // over the destinations — X_{k,j} in source order, no index gather
+        {
+            LaunchScope ls("gvr_split", st);
+            k_gvr_dest<uint32_t><<<grid, 256, 0, st>>>(static_cast<const uint32_t*>(X), N, (uint32_t)rank, S, p,
+                                                       L.gv_dest, nullptr, counts);
+        }
+        return local_sort(4, L.gv_dest, static_cast<const uint32_t*>(X), N, 8, p <= 256 ? 8 : 16, L.gv_sdest,
+                          static_cast<uint32_t*>(L.gv_keys), L.gv_ws, L.gv_ws_bytes, st);
+    }
     {
         LaunchScope ls("gvr_split", st);
         if (key_bytes == 4)
