@@ -178,6 +178,10 @@ rs_status_t rs_pr_emulate(int key_bytes, int p, void* const* keys, uint32_t* con
  * out_keys[j] / out_vals[j] (N each), ws of rs_net_emulate_ws_bytes (device,
  * 16-byte aligned), stream-ordered, no sync. */
 int rs_net_stages(int mode, int p);
+/* The exchange of `rank` in stage `stage` (0-based) of the mode's network, host
+ * only: *partner = the other rank of its merge-split (−1: idle this stage),
+ * *keep_low = 1 if it keeps the smaller half.  Returns 0, or −1 on a bad argument. */
+int rs_net_schedule(int mode, int p, int stage, int rank, int* partner, int* keep_low);
 size_t rs_net_emulate_ws_bytes(int key_bytes, int val_bytes, int p, int digit_bits, size_t N);
 rs_status_t rs_net_emulate(int mode, int key_bytes, int p, int digit_bits, void* const* keys,
                            const uint32_t* const* vals, size_t N, void* const* out_keys,

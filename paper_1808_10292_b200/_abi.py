@@ -41,6 +41,7 @@ SIGNATURES = {
     "rs_pr_emulate_ws_bytes": (_sz, [_i32, _i32, _i32, _sz]),
     "rs_pr_emulate": (_i32, [_i32, _i32, _vpp, _vpp, _szp, _vpp, _vpp, _vp, _sz, _vp]),
     "rs_net_stages": (_i32, [_i32, _i32]),
+    "rs_net_schedule": (_i32, [_i32, _i32, _i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "rs_net_emulate_ws_bytes": (_sz, [_i32, _i32, _i32, _i32, _sz]),
     "rs_net_emulate": (_i32, [_i32, _i32, _i32, _i32, _vpp, _vpp, _sz, _vpp, _vpp, _vp, _sz, _vp]),
     "rs_ger_default_s": (_sz, [ctypes.c_uint64]),

@@ -249,6 +249,15 @@ int rs_net_stages(int mode, int p) {
     return rs::net_stage_count(mode, p);
 }
 
+int rs_net_schedule(int mode, int p, int stage, int rank, int* partner, int* keep_low) {
+    if (!partner || !keep_low || rs_net_stages(mode, p) < 0 || rank < 0 || rank >= p) return -1;
+    const auto S = rs::net_schedule(mode, p);
+    if (stage < 0 || stage >= (int)S.size()) return -1;
+    *partner = S[stage][rank].partner;
+    *keep_low = S[stage][rank].keep_low ? 1 : 0;
+    return 0;
+}
+
 size_t rs_net_emulate_ws_bytes(int key_bytes, int val_bytes, int p, int digit_bits, size_t N) {
     if (p < 1 || (key_bytes != 4 && key_bytes != 8) || (digit_bits != 8 && digit_bits != 16)) return 0;
     return rs::net_ws_bytes(key_bytes, val_bytes != 0, N, digit_bits) * (size_t)p;

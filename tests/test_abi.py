@@ -114,3 +114,37 @@ def test_timing_api_without_gpu(L):
     assert L.rs_timing_query(b"", ctypes.byref(ms), ctypes.byref(cnt)) == RS_OK
     assert cnt.value == 0 and ms.value == 0.0
     assert L.rs_launch_count() == 0
+
+
+@pytest.mark.parametrize("mode,name,ps", [(4, "btn", [1, 2, 4, 8, 16]), (5, "oet", [1, 2, 3, 5, 8])])
+def test_net_schedule_drives_the_oracle_network(L, mode, name, ps):
+    """The library's BTN / OET schedule (host logic of net.cu, the one the GPU
+    stages follow) replayed on tiny blocks in Python reproduces the independent C
+    oracle (oracle/net.c) stage by stage, and pairs are symmetric."""
+    import numpy as np
+    import oracle
+    rng = np.random.default_rng(mode)
+    for p in ps:
+        blocks = [np.sort(rng.integers(0, 20, 3).astype(np.uint32)) for _ in range(p)]
+        cur = [b.copy() for b in blocks]
+        stages = L.rs_net_stages(mode, p)
+        for t in range(stages):
+            nxt = [None] * p
+            for r in range(p):
+                q, kl = ctypes.c_int(), ctypes.c_int()
+                assert L.rs_net_schedule(mode, p, t, r, ctypes.byref(q), ctypes.byref(kl)) == 0
+                if q.value < 0:
+                    nxt[r] = cur[r]
+                    continue
+                q2, kl2 = ctypes.c_int(), ctypes.c_int()
+                assert L.rs_net_schedule(mode, p, t, q.value, ctypes.byref(q2), ctypes.byref(kl2)) == 0
+                assert q2.value == r and kl2.value == 1 - kl.value
+                lo, hi = (r, q.value) if r < q.value else (q.value, r)
+                merged = np.concatenate([cur[lo], cur[hi]])
+                merged = merged[np.argsort(merged, kind="stable")]
+                nxt[r] = merged[:3] if kl.value else merged[3:]
+            cur = nxt
+            want = getattr(oracle, name)(blocks, max_stages=t + 1)
+            assert [c.tolist() for c in cur] == [w.tolist() for w in want["Y"]], (p, t)
+        q, kl = ctypes.c_int(), ctypes.c_int()
+        assert L.rs_net_schedule(mode, p, stages, 0, ctypes.byref(q), ctypes.byref(kl)) == -1
