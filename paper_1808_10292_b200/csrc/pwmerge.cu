@@ -7,9 +7,9 @@
 // the paper uses one level up (GSD's own splitters):
 //   1 k_pw_sample  every m-th element of run k (the last of each m-block) becomes
 //                  a sample, tagged (k, t);
-//   2 the p sorted sample lists are merged (merge_runs_tree: composite order —
-//    key, then run — since ties go to the lower run) into Sm, and k_pw_pos
-//                  records where each run's samples landed;
+//   2 the samples (p sorted lists, laid out run by run) are sorted stably by key
+//                  (radix sort: composite order — key, then run) into Sm, and
+//                  k_pw_pos records where each run's samples landed;
 //   3 k_pw_bounds  chunk boundary i is the composite b_i = Sm[i·c − 1]; for every
 //                  run k, cnt[i][k] = #elements of run k that are ≤ b_i.  The
 //                  samples bracket it: if q run-k samples precede Sm position i·c,
@@ -263,11 +263,12 @@ constexpr int pw_cap_padded(int p, int c) { return pw_cap(p, c) + pw_cap(p, c) /
 int pw_c(int key_bytes, bool hv) { return RS_PW_C ? RS_PW_C : (key_bytes == 4 && !hv ? 32 : 16); }
 
 struct PwLayout {
-    void *sk, *tk, *mk;       // samples, tree scratch, merged samples (M keys each)
-    uint32_t *sv, *tv, *mv;   // their tags
+    void *sk, *mk;            // samples, sorted samples (M keys each)
+    uint32_t *sv, *mv;        // their tags
     uint32_t* pos;            // M
     uint32_t* cnt;            // (nch + 1) * p
-    size_t* split;            // merge_runs_tree co-rank scratch
+    void* sort_ws;            // local_sort scratch for the sample
+    size_t sort_ws_bytes;
     size_t bytes;
 };
 
@@ -276,14 +277,13 @@ PwLayout pw_layout(void* ws, int key_bytes, uint64_t M, uint64_t nch, int p) {
     Carver c(ws);
     const size_t M1 = std::max<uint64_t>(M, 1);
     L.sk = c.take(M1 * key_bytes);
-    L.tk = c.take(M1 * key_bytes);
     L.mk = c.take(M1 * key_bytes);
     L.sv = static_cast<uint32_t*>(c.take(M1 * 4));
-    L.tv = static_cast<uint32_t*>(c.take(M1 * 4));
     L.mv = static_cast<uint32_t*>(c.take(M1 * 4));
     L.pos = static_cast<uint32_t*>(c.take(M1 * 4));
     L.cnt = static_cast<uint32_t*>(c.take((nch + 1) * (size_t)p * 4));
-    L.split = static_cast<size_t*>(c.take(merge_scratch_bytes(M1)));
+    L.sort_ws_bytes = local_ws_bytes(key_bytes, true, M1, 8);
+    L.sort_ws = c.take(L.sort_ws_bytes);
     L.bytes = c.used();
     return L;
 }
@@ -298,9 +298,11 @@ rs_status_t pway(const PwRuns& R, uint64_t M, void* scratch, K* out, uint32_t* v
         LaunchScope ls("pw_sample", st);
         if (M) k_pw_sample<K><<<g, 256, 0, st>>>(R, static_cast<K*>(L.sk), L.sv);
     }
-    std::vector<uint64_t> soff(R.soff, R.soff + p + 1);
     if (M) {
-        rs_status_t s = merge_runs_tree(sizeof(K), L.sk, L.sv, soff, L.tk, L.tv, L.mk, L.mv, L.split, st);
+        // the samples, laid out run by run, sorted stably by key: ties stay in (run, t)
+        // order, i.e. the composite order (a radix sort beats a merge tree at this size)
+        rs_status_t s = local_sort(sizeof(K), L.sk, L.sv, M, 8, (int)sizeof(K) * 8, L.mk, L.mv, L.sort_ws,
+                                   L.sort_ws_bytes, st);
         if (s != RS_OK) return s;
         LaunchScope ls("pw_pos", st);
         k_pw_pos<<<g, 256, 0, st>>>(R, L.mv, M, L.pos);
