@@ -278,10 +278,18 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
+    # inputs smaller than L2 (c1-c3 single GPU): flush L2 after every reset by
+    # writing a buffer twice its size, outside the timed region
+    l2_bytes = torch.cuda.get_device_properties(dev).L2_cache_size
+    in_bytes = n * (KEY_BYTES[kind] + (4 if kind == "pairs" else 0))
+    flush = torch.empty(2 * l2_bytes, dtype=torch.uint8, device=dev) if 2 * in_bytes < 4 * l2_bytes else None
+
     def reset():
         work.copy_(pristine)
         if vals_work is not None:
             vals_work.copy_(vals_pristine)
+        if flush is not None:
+            flush.fill_(1)
 
     # ---- warm-up (includes a full GSD exchange when p > 1: NCCL connects lazily)
     for _ in range(args.warmup):
@@ -454,10 +462,14 @@ def main():
                                    f"{args.sampling}-p{p} (paper's s)" if args.sampling in ("ger", "gvr") else
                                    f"{args.sampling}-p{p}")
                    if p > 1 else "single GPU",
-                   "l2": "inputs larger than L2 (no flush)", "inputs": "resident in HBM, reset outside timed region"},
+                   "l2": ("L2 flushed before every step (2x L2 write)" if flush is not None
+                          else "inputs larger than L2 (no flush)"), "l2_bytes": l2_bytes,
+                   "inputs": "resident in HBM, reset outside timed region"},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         **({"nvlink_roofline": xchg} if xchg else {}),
         "clocks": clocks, "kernel_ms_per_step": round(all_kernels_ms / args.steps, 4),
+        "step_ms_rank0": {"mean": round(statistics.mean(step_ms), 4), "median": round(statistics.median(step_ms), 4),
+                          "min": round(min(step_ms), 4), "max": round(max(step_ms), 4)},
     }
     print(json.dumps(line))
     if p > 1:
