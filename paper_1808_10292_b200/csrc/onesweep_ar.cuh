@@ -34,7 +34,7 @@
 #include "onesweep_ec.cuh"
 
 // timing ablations of design 5 (development builds only, OUTPUT INVALID):
-// 1 no look-back walk, 2 no global store, 4 no scatter
+// 1 no look-back walk, 2 no global store, 4 no scatter, 8 aligned in-place store
 #ifndef RS_AR_ABLATE
 #define RS_AR_ABLATE 0
 #endif
@@ -450,6 +450,8 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
 #pragma unroll
                 for (int i = 0; i < SG; ++i) {
                     g[i] = s_gofs[digit8<K>(k[i], shift)] + (uint32_t)((b + i) * THREADS + tid);
+                    if (RS_AR_ABLATE & 8)  // timing only: the tile stored in place, aligned and coalesced
+                        g[i] = (uint32_t)base + (uint32_t)((b + i) * THREADS + tid) + (g[i] & 0u);
                     if (HAS_VAL) vv[HAS_VAL ? i : 0] = s_vout[(b + i) * THREADS + tid];
                 }
 #pragma unroll
