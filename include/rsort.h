@@ -310,6 +310,9 @@ rs_status_t rs_ipc_close_all(void);
  *   "small_tiles"    design-5 tiles: 0 = small tiles when the input makes fewer
  *                    than three large tiles per SM (default), 1 = always large,
  *                    2 = always small.
+ *   "small_fused"    1 = small-tile full sorts as one cooperative launch (all
+ *                    phases separated by grid barriers); 0 = separate kernels
+ *                    (default: the fused form measured no faster).
  *   "hist_shared"    1 = digit-histogram kernel with one shared histogram per
  *                    4 warps (0, default: lane-private copies, conflict-free).
  *   "debug_skip"     timing ablations, OUTPUT INVALID: bit 0 no look-back,

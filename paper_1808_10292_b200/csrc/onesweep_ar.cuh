@@ -91,7 +91,7 @@ struct OnesweepArCfg {
 //      which frees the registers for larger tiles
 template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, bool KREG_, int KSRC = 0,
           int RANK2 = 0>
-__global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
+__device__ __forceinline__ void onesweep_ar_body(const PassArgs& a) {
     static_assert(KSRC != 1 || !HAS_VAL, "register tiles are for keys-only sorts");
     constexpr bool LDGK = KSRC != 0;
     constexpr bool KREG = (KREG_ && KSRC != 2) || KSRC == 1;
@@ -491,6 +491,13 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             tmem_dealloc(s_misc[60], kTmemCols);
         }
     }
+}
+
+// the pass as its own launch (the fused small-n sort runs the same body in a loop)
+template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, bool KREG_, int KSRC = 0,
+          int RANK2 = 0>
+__global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
+    onesweep_ar_body<K, HAS_VAL, RT, KPT, MINB, S, KREG_, KSRC, RANK2>(a);
 }
 
 // Startup probe of the lane-order property design 5 relies on: every warp ranks

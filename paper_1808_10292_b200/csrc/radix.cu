@@ -12,6 +12,7 @@
 #include "onesweep.cuh"
 #include "onesweep_ec.cuh"
 #include "onesweep_ar.cuh"
+#include "onesweep_fused.cuh"
 #include "onesweep_ts.cuh"
 #include "onesweep_cr.cuh"
 #include "onesweep_n4.cuh"
@@ -339,6 +340,40 @@ static rs_status_t launch_pass_ts(const PassArgs& a, size_t T, cudaStream_t st) 
     return RS_OK;
 }
 
+// the whole small-tile sort as one cooperative launch (onesweep_fused.cuh);
+// *done = false when the device cannot co-schedule the grid (then the caller
+// runs the separate kernels)
+template <typename K, bool V>
+static rs_status_t launch_sort_fused(const FusedArgs& f, cudaStream_t st, bool* done) {
+    using TN = TuneArSmall<K, V>;
+    constexpr int KSRC = V ? RS_AR_KSRC_PAIRS : (sizeof(K) == 8 ? RS_AR_KSRC_U64 : RS_AR_KSRC_U32);
+    constexpr int RANK2 = V ? RS_AR_RANK2_PAIRS : (sizeof(K) == 4 ? RS_AR_RANK2_U32 : RS_AR_RANK2_U64);
+    constexpr int HC = 4;  // K1 lane copies inside the fused kernel (P·256·HC words of shared memory)
+    using C = OnesweepArCfg<K, V, TN::THREADS, TN::KPT, KSRC>;
+    auto kern = k_sort_fused<K, V, TN::THREADS, TN::KPT, TN::MINB, (RS_AR_KREG == 1 || (RS_AR_KREG == 2 && V)), KSRC,
+                             RANK2, HC>;
+    constexpr size_t hist_smem = sizeof(K) * 256 * HC * 4;
+    constexpr size_t smem = C::smem_bytes > hist_smem ? C::smem_bytes : hist_smem;
+    static int grid = -1;
+    if (grid < 0) {
+        RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0, coop = 0, dev = 0;
+        RS_CUDA_TRY(cudaGetDevice(&dev));
+        RS_CUDA_TRY(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev));
+        RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TN::THREADS, smem));
+        grid = coop ? per_sm * sm_count() : 0;
+    }
+    *done = false;
+    if (grid <= 0) return RS_OK;
+    FusedArgs fa = f;
+    void* params[] = {&fa};
+    LaunchScope ls("sort_fused", st);
+    RS_CUDA_TRY(cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3((unsigned)grid),
+                                            dim3(TN::THREADS), params, smem, st));
+    *done = true;
+    return RS_OK;
+}
+
 template <typename K, bool V, typename S, bool SMALL>
 static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st) {
     using TN = typename std::conditional<SMALL, TuneArSmall<K, V>, TuneAr<K, V>>::type;
@@ -558,6 +593,30 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
         if (!ar_ok) design = 2;
     }
     const Layout8 L = layout8(ws, sizeof(K), V, n, (size_t)tile_for(sizeof(K), V, design, n));
+    if (options().small_fused && design == 5 && P == (int)sizeof(K) && first_pass == 0 && !hist_copy && !L.wide &&
+        small_input<K, V>(n)) {
+        RS_CUDA_TRY(cudaMemsetAsync(L.hist, 0, (size_t)P * 256 * 4, st));
+        FusedArgs f{};
+        f.a.keys_in = keys_in;
+        f.a.keys_out = out;
+        f.a.keys_alt = L.alt_keys;
+        f.a.vals_in = vals_in;
+        f.a.vals_out = vout;
+        f.a.vals_alt = L.alt_vals;
+        f.a.n = (uint32_t)n;
+        f.a.num_tiles = (uint32_t)L.T;
+        f.a.P = P;
+        f.a.ctrl = L.ctrl;
+        f.a.bases = L.bases;
+        f.a.debug_skip = options().debug_skip;
+        f.hist = L.hist;
+        f.status = L.status;
+        f.status_bytes = L.status_bytes;
+        f.inplace = (const void*)keys_in == (const void*)out ? 1 : 0;
+        bool done = false;
+        rs_status_t s = launch_sort_fused<K, V>(f, st, &done);
+        if (s != RS_OK || done) return s;
+    }
     RS_CUDA_TRY(cudaMemsetAsync(L.hist, 0, (size_t)P * 256 * 4, st));
     // K1 also zeroes the first pass's status region (as u32 words)
     rs_status_t s = launch_hist<K>(keys_in, n, P, L.hist, static_cast<uint32_t*>(L.status), L.status_bytes / 4, st,

@@ -107,11 +107,9 @@ __global__ void __launch_bounds__(THREADS) k_digit_hist(const K* __restrict__ ke
 // cost ~3.15 wavefronts); C = 16 (u64 keys, 8 passes: 128 KB) ~2.  One CTA of
 // 1024 threads per SM, persistent; each thread loads 16-byte vectors.
 template <typename K, int THREADS, int C, int P>
-__global__ void __launch_bounds__(THREADS, 1) k_digit_hist_lp(const K* __restrict__ keys, size_t n,
-                                                             uint32_t* __restrict__ hist,
-                                                             uint32_t* __restrict__ zero_ptr, size_t zero_words,
-                                                             int shift0 = 0) {
-    extern __shared__ __align__(16) uint32_t s_h[];  // [P][256][C]
+__device__ __forceinline__ void digit_hist_lp_body(const K* __restrict__ keys, size_t n, uint32_t* __restrict__ hist,
+                                                   uint32_t* __restrict__ zero_ptr, size_t zero_words, int shift0,
+                                                   uint32_t* s_h) {  // s_h: [P][256][C] shared
     const int tid = threadIdx.x, lane = tid & 31;
     const size_t gtid = (size_t)blockIdx.x * THREADS + tid;
     const size_t gstride = (size_t)gridDim.x * THREADS;
@@ -154,15 +152,24 @@ __global__ void __launch_bounds__(THREADS, 1) k_digit_hist_lp(const K* __restric
     }
 }
 
+template <typename K, int THREADS, int C, int P>
+__global__ void __launch_bounds__(THREADS, 1) k_digit_hist_lp(const K* __restrict__ keys, size_t n,
+                                                             uint32_t* __restrict__ hist,
+                                                             uint32_t* __restrict__ zero_ptr, size_t zero_words,
+                                                             int shift0 = 0) {
+    extern __shared__ __align__(16) uint32_t s_hist_lp[];
+    digit_hist_lp_body<K, THREADS, C, P>(keys, n, hist, zero_ptr, zero_words, shift0, s_hist_lp);
+}
+
 // ------------------------------------------------------------------ K2 ----
 // One CTA of 256 threads.  bases[t][d] = Σ_{d'<d} hist[t][d'].
 // Pass t is trivial (skipped: it would be the identity permutation) iff one
 // bucket holds all n keys.  Then the ping-pong plan: the last active pass writes
 // `out`, earlier ones alternate with `alt`, the first reads `in`; an in-place
 // call with an odd count ends in `alt` and needs the final copy.
-__global__ void __launch_bounds__(256) k_plan(const uint32_t* __restrict__ hist, uint32_t n, int P,
-                                              uint32_t* __restrict__ bases, Ctrl* __restrict__ ctrl,
-                                              int inplace, int first = 0) {
+__device__ __forceinline__ void plan_body(const uint32_t* __restrict__ hist, uint32_t n, int P,
+                                          uint32_t* __restrict__ bases, Ctrl* __restrict__ ctrl, int inplace,
+                                          int first) {  // threads 0..255 of one CTA
     __shared__ uint32_t s_warp[8];
     __shared__ int s_active[kMaxPasses];
     const int d = threadIdx.x, lane = d & 31, warp = d >> 5;
@@ -211,6 +218,12 @@ __global__ void __launch_bounds__(256) k_plan(const uint32_t* __restrict__ hist,
     }
 }
 
+__global__ void __launch_bounds__(256) k_plan(const uint32_t* __restrict__ hist, uint32_t n, int P,
+                                              uint32_t* __restrict__ bases, Ctrl* __restrict__ ctrl,
+                                              int inplace, int first = 0) {
+    plan_body(hist, n, P, bases, ctrl, inplace, first);
+}
+
 template <typename T>
 __device__ __forceinline__ T* pick(int sel, T* in, T* out, T* alt) {
     return sel == kSelIn ? in : (sel == kSelOut ? out : alt);
@@ -238,8 +251,9 @@ struct PassArgs {
 
 // ------------------------------------------------------------------ K4 ----
 template <typename K>
-__global__ void k_final_copy(const Ctrl* __restrict__ ctrl, const K* in, const K* alt, K* out,
-                             const uint32_t* vin, const uint32_t* valt, uint32_t* vout, size_t n) {
+__device__ __forceinline__ void final_copy_body(const Ctrl* __restrict__ ctrl, const K* in, const K* alt, K* out,
+                                                const uint32_t* vin, const uint32_t* valt, uint32_t* vout,
+                                                size_t n) {
     const int fc = ctrl->final_copy;
     if (fc == 0) return;
     const K* s = fc == 1 ? in : alt;
@@ -257,6 +271,12 @@ __global__ void k_final_copy(const Ctrl* __restrict__ ctrl, const K* in, const K
             reinterpret_cast<uint4*>(vout)[i] = reinterpret_cast<const uint4*>(vs)[i];
         for (size_t i = nv4 * 4 + g; i < n; i += stride) vout[i] = vs[i];
     }
+}
+
+template <typename K>
+__global__ void k_final_copy(const Ctrl* __restrict__ ctrl, const K* in, const K* alt, K* out,
+                             const uint32_t* vin, const uint32_t* valt, uint32_t* vout, size_t n) {
+    final_copy_body<K>(ctrl, in, alt, out, vin, valt, vout, n);
 }
 
 }  // namespace rs

@@ -47,6 +47,8 @@ struct Options {
     int match_every = 0;          // design 2, u32 keys: every k-th key ranked by match.any (0 = none)
     bool hist_shared = false;     // K1: 1 = one histogram copy per 4 warps (previous default)
     int small_tiles = 0;          // design 5 small-input tiles: 0 auto (< 2 large tiles per SM), 1 never, 2 always
+    int small_fused = 0;          // 1: small-tile full sorts as one cooperative launch (onesweep_fused.cuh);
+                                  // measured no faster (2^20: 70.8 vs 73.4 us direct, 69 vs 55 us as a graph)
     int pass_design = 5;          // 5 atomic ranks (if the lane-order probe passes, else 2);
                                   // 0 classic single sweep; early counts + prefetch with 1 a look-back
                                   // warp, 2 look-back after ranking; 3 counter-ranked nibble sub-passes;

@@ -10,6 +10,8 @@ import torch  # noqa: E402
 import inputs  # noqa: E402
 import paper_1808_10292_b200 as rs  # noqa: E402
 
+if os.environ.get("RS_SMALL_FUSED"):
+    rs.lib().rs_set_option(b"small_fused", int(os.environ["RS_SMALL_FUSED"]))
 for log2n in [int(x) for x in sys.argv[1:]] or [20, 22, 24]:
     n = 1 << log2n
     src = torch.from_numpy(inputs.gen_u32(n, 1).view(np.int32)).cuda()

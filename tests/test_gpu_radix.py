@@ -86,11 +86,14 @@ EDGE_N = sorted({1, 2, 3, 31, 32, 33, 1000, TILE64 - 1, TILE64, TILE64 + 1, TILE
                  TILE32 - 1, TILE32, TILE32 + 1, 2 * TILE32 + 3, 7 * TILE32 + 4095})
 
 
-@pytest.mark.parametrize("tiles", [1, 2])
-def test_edge_sizes_large_and_small_tiles(option, tiles):
+@pytest.mark.parametrize("tiles,fused", [(1, 0), (2, 0), (2, 1)])
+def test_edge_sizes_large_and_small_tiles(option, tiles, fused):
     """Both design-5 tile sizes (large: the size-dependent default above ~6.7 M
-    u32 keys; small: below) at every edge size, u32 keys, u64 keys and pairs."""
+    u32 keys; small: below) at every edge size, u32 keys, u64 keys and pairs; the
+    small tiles also as the single cooperative launch (onesweep_fused.cuh) and as
+    separate kernels."""
     option("small_tiles", tiles)
+    option("small_fused", fused)
     for n in EDGE_N:
         a = inputs.gen_u32(n, 125 + n)
         assert (_sort_u32(a, 8) == oracle.sr(a, 8)).all(), n
