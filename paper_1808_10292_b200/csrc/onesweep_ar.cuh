@@ -40,6 +40,10 @@
 #endif
 // per-warp digit counters as 16-bit halves of shared words (digits 2w, 2w+1
 // share word w): 128 words per warp instead of 256, so fewer bank conflicts
+// look-back window of the small-tile configuration (all tiles in flight at once)
+#ifndef RS_AR_LB_SMALL
+#define RS_AR_LB_SMALL 8
+#endif
 #ifndef RS_AR_EARLY_NEXT
 #define RS_AR_EARLY_NEXT 0
 #endif
@@ -90,7 +94,7 @@ struct OnesweepArCfg {
 //   2  as 1, but the keys are not kept: the scatter loads them again (from L2),
 //      which frees the registers for larger tiles
 template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, bool KREG_, int KSRC = 0,
-          int RANK2 = 0>
+          int RANK2 = 0, int LB = 8>
 __device__ __forceinline__ void onesweep_ar_body(const PassArgs& a) {
     static_assert(KSRC != 1 || !HAS_VAL, "register tiles are for keys-only sorts");
     constexpr bool LDGK = KSRC != 0;
@@ -391,7 +395,6 @@ __device__ __forceinline__ void onesweep_ar_body(const PassArgs& a) {
             if (tile != 0 && (RS_AR_ABLATE & 1)) {
                 st_relaxed_gpu(status + (size_t)tile * R + tid, ST::kFlagP | (S)s_tcnt[tid]);
             } else if (tile != 0) {
-                constexpr int LB = 8;
                 const S* sp = status + (size_t)(tile - 1) * R + tid;
                 int64_t left = (int64_t)tile;
                 bool done = false;
@@ -495,9 +498,9 @@ __device__ __forceinline__ void onesweep_ar_body(const PassArgs& a) {
 
 // the pass as its own launch (the fused small-n sort runs the same body in a loop)
 template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, bool KREG_, int KSRC = 0,
-          int RANK2 = 0>
+          int RANK2 = 0, int LB = 8>
 __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
-    onesweep_ar_body<K, HAS_VAL, RT, KPT, MINB, S, KREG_, KSRC, RANK2>(a);
+    onesweep_ar_body<K, HAS_VAL, RT, KPT, MINB, S, KREG_, KSRC, RANK2, LB>(a);
 }
 
 // Startup probe of the lane-order property design 5 relies on: every warp ranks

@@ -48,7 +48,7 @@ __global__ void __launch_bounds__(RT, MINB) k_sort_fused(FusedArgs f) {
         a.shift = 8 * t;
         a.status_cur = static_cast<char*>(f.status) + (size_t)(t & 1) * f.status_bytes;
         a.status_next = static_cast<char*>(f.status) + (size_t)((t + 1) & 1) * f.status_bytes;
-        onesweep_ar_body<K, V, RT, KPT, MINB, uint32_t, KREG_, KSRC, RANK2>(a);
+        onesweep_ar_body<K, V, RT, KPT, MINB, uint32_t, KREG_, KSRC, RANK2, RS_AR_LB_SMALL>(a);
         grid.sync();
     }
     final_copy_body<K>(a.ctrl, keys_in, static_cast<const K*>(a.keys_alt), static_cast<K*>(a.keys_out), a.vals_in,

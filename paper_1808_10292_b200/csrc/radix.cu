@@ -380,8 +380,11 @@ static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st) 
     constexpr int KSRC = V ? RS_AR_KSRC_PAIRS : (sizeof(K) == 8 ? RS_AR_KSRC_U64 : RS_AR_KSRC_U32);
     constexpr int RANK2 = V ? RS_AR_RANK2_PAIRS : (sizeof(K) == 4 ? RS_AR_RANK2_U32 : RS_AR_RANK2_U64);
     using C = OnesweepArCfg<K, V, TN::THREADS, TN::KPT, KSRC>;
+    // look-back window: small inputs run all tiles at once, so a tile's walk
+    // crosses many predecessors that have only published aggregates
+    constexpr int LB = SMALL ? RS_AR_LB_SMALL : 8;
     auto kern = k_onesweep_ar<K, V, TN::THREADS, TN::KPT, TN::MINB, S, (RS_AR_KREG == 1 || (RS_AR_KREG == 2 && V)), KSRC,
-                              RANK2>;
+                              RANK2, LB>;
     static int grid_cap = 0;
     if (!grid_cap) {
         RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::smem_bytes));
