@@ -451,11 +451,25 @@ static rs_status_t launch_split(int key_bytes, const void* X, size_t N, int rank
 // (default) or a stable radix re-sort of the concatenation (option gsd_merge=1);
 // both give the identical result (reading R17)
 static rs_status_t merge_runs(int key_bytes, void* runs, uint32_t* vruns, const std::vector<uint64_t>& roff, int b,
-                              void* out, uint32_t* vout, const GsdLayout& L, cudaStream_t st) {
+                              void* out, uint32_t* vout, const GsdLayout& L, size_t cap, cudaStream_t st) {
     const size_t total = roff.back();
     if (total == 0) return RS_OK;
     if (options().gsd_merge == 1)
         return local_sort(key_bytes, runs, vruns, total, b, key_bytes * 8, out, vout, L.local_ws, L.local_ws_bytes, st);
+    const int p = (int)roff.size() - 1;
+    std::vector<uint64_t> len(p);
+    for (int k = 0; k < p; ++k) len[k] = roff[k + 1] - roff[k];
+    if (options().gsd_merge == 3 && pway_applicable(p, len) &&
+        pway_scratch_bytes(key_bytes, total, p) <= cap * (size_t)key_bytes) {
+        // the received runs merged in one p-way pass (the all-to-all fallback of the pull merge)
+        std::vector<const void*> rk(p);
+        std::vector<const uint32_t*> rv(vruns ? p : 0);
+        for (int k = 0; k < p; ++k) {
+            rk[k] = static_cast<const char*>(runs) + roff[k] * key_bytes;
+            if (vruns) rv[k] = vruns + roff[k];
+        }
+        return merge_pway(key_bytes, rk, rv, len, L.merge_keys, cap * (size_t)key_bytes, out, vout, st);
+    }
     return merge_runs_tree(key_bytes, runs, vruns, roff, L.merge_keys, L.merge_vals, out, vout, L.merge_split, st);
 }
 
@@ -694,7 +708,7 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
         if (total && (sst = local_sort(key_bytes, L.recv_keys, L.recv_vals, total, b, key_bytes * 8, out, vout,
                                        L.local_ws, L.local_ws_bytes, st)) != RS_OK)
             return sst;
-    } else if ((sst = merge_runs(key_bytes, L.recv_keys, L.recv_vals, roff, b, out, vout, L, st)) != RS_OK) {
+    } else if ((sst = merge_runs(key_bytes, L.recv_keys, L.recv_vals, roff, b, out, vout, L, out_cap, st)) != RS_OK) {
         return sst;
     }
     if (n_out) *n_out = total;
@@ -953,7 +967,7 @@ static rs_status_t emulate(int mode, int key_bytes, int p, int r, size_t ger_s, 
                                          st)) != RS_OK)
                 return sst;
         } else if ((sst = merge_runs(key_bytes, L.recv_keys, L.recv_vals, roff, digit_bits, out_keys[j],
-                                     hv ? out_vals[j] : nullptr, L, st)) != RS_OK) {
+                                     hv ? out_vals[j] : nullptr, L, out_cap, st)) != RS_OK) {
             return sst;
         }
     }
