@@ -305,6 +305,9 @@ rs_status_t rs_ipc_close_all(void);
  *                    0 = NCCL all-to-all into a receive buffer, then the tree of
  *                    stable 2-way merge-path merges; 1 = all-to-all, then a
  *                    stable radix re-sort.
+ *   "gsd_pull"       1 (default) = modes 2 and 3 pull over NVLink; 0 = they take
+ *                    the all-to-all path (the fallback taken when a mapping
+ *                    fails), merging the received runs the same way.
  *   "compact"        1 = default pass with 16-bit per-warp counters (smaller
  *                    shared-memory footprint; ballots only).
  *   "small_tiles"    design-5 tiles: 0 = small tiles when the input makes fewer

@@ -622,7 +622,7 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
     // tree's first level reads the peers' X_{k,j} in place over NVLink through
     // CUDA IPC mappings exchanged now (falls back to the all-to-all on every
     // rank if any rank cannot export its block, e.g. VMM memory)
-    if (options().gsd_merge >= 2 && !gvr && p > 1) {
+    if (options().gsd_merge >= 2 && options().gsd_pull && !gvr && p > 1) {
         uint64_t* rec = h;
         std::memset(rec, 0, kIpcWords * 8);
         bool ok = ipc_export(keys, rec, &rec[8]) == RS_OK;
@@ -923,7 +923,7 @@ static rs_status_t emulate(int mode, int key_bytes, int p, int r, size_t ger_s, 
             n_out[j] = tot;
         }
     }
-    if (mode != 2 && options().gsd_merge >= 2 && p > 1) {  // pull merge: the blocks are read in place
+    if (mode != 2 && options().gsd_merge >= 2 && options().gsd_pull && p > 1) {  // pull merge: blocks read in place
         for (int j = 0; j < p; ++j) {
             std::vector<const void*> rk(p);
             std::vector<const uint32_t*> rv(hv ? p : 0);

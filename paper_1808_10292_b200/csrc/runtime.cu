@@ -139,6 +139,7 @@ rs_status_t rs_set_option(const char* name, long long value) {
     else if (n == "hist_shared" && value <= 1) options().hist_shared = value != 0;
     else if (n == "small_tiles" && value <= 2) options().small_tiles = (int)value;
     else if (n == "small_fused" && value <= 1) options().small_fused = (int)value;
+    else if (n == "gsd_pull" && value <= 1) options().gsd_pull = (int)value;
     else if (n == "match_every" && (value == 0 || value == 4 || value == 6 || value == 8))
         options().match_every = (int)value;
     else if (n == "pass_design" && value <= 6) options().pass_design = (int)value;
@@ -158,6 +159,7 @@ rs_status_t rs_get_option(const char* name, long long* value) {
     else if (n == "hist_shared") *value = o.hist_shared;
     else if (n == "small_tiles") *value = o.small_tiles;
     else if (n == "small_fused") *value = o.small_fused;
+    else if (n == "gsd_pull") *value = o.gsd_pull;
     else if (n == "match_every") *value = o.match_every;
     else if (n == "pass_design") *value = o.pass_design;
     else if (n == "rank_variant") *value = o.rank_variant;

@@ -42,6 +42,7 @@ struct Options {
     int rank_variant = 3;         // 0 ballot peers, 1 match.any, 2 atomic-OR peers, 3 hybrid pairs
     int gsd_merge = 3;            // GSD step 5: 0 merge tree, 1 stable radix re-sort, 2 pull merge (tree),
                                   // 3 pull merge as one p-way pass (pwmerge.cu; tree when p > 32)
+    int gsd_pull = 1;             // 0: exchange by all-to-all even with gsd_merge 2/3 (tests the fallback)
                                   // (the tree reads the source blocks in place: peers over NVLink)
     bool compact = false;         // design 2: 16-bit per-warp counters, ballots only (4 CTAs/SM)
     int match_every = 0;          // design 2, u32 keys: every k-th key ranked by match.any (0 = none)

@@ -247,6 +247,24 @@ def test_pway_merge_many_runs(option, p, dist):
     _check([a[i * N:(i + 1) * N] for i in range(p)], r=8, b=8)
 
 
+@pytest.mark.parametrize("merge", [2, 3])
+def test_exchange_fallback_with_pull_merges(option, merge):
+    """With pulling disabled (the path taken when a peer block cannot be mapped)
+    the all-to-all runs and the received runs are merged by the tree (2) or the
+    one-pass p-way merge (3): identical Y_j, pairs stable."""
+    option("gsd_merge", merge)
+    option("gsd_pull", 0)
+    p, N = 8, 30011
+    k = inputs.gen_u64(p * N, 430, "mod1024")
+    v = inputs.iota_u32(p * N)
+    got = _check([k[i * N:(i + 1) * N] for i in range(p)], r=8, b=8, vals_np=[v[i * N:(i + 1) * N] for i in range(p)])
+    K = np.concatenate([host(y, np.uint64) for y in got["Y"]])
+    V = np.concatenate([host(y, np.uint32) for y in got["Yv"]])
+    assert oracle.pairs_stable(K, V)
+    a = inputs.gen_u32(5 * 40000, 431, "gauss")
+    _check([a[i * 40000:(i + 1) * 40000] for i in range(5)], r=8, b=8)
+
+
 def test_pway_merge_pairs_uneven_tiny_and_empty_blocks(option):
     """p-way merge: stable pairs over uneven blocks, including blocks shorter than
     one sample stride and empty ones (runs with no samples)."""
