@@ -37,7 +37,11 @@ namespace {
 #define RS_PW_C 0  // 0: 32 samples per chunk for 4-byte keys without values, else 16
 #endif
 #ifndef RS_PW_IT
-#define RS_PW_IT 16
+// outputs per thread per merge round; odd, so neighbouring threads' merge-path
+// positions fall in different banks without padding (u32 at 2^31, p = 8,
+// k_pw_merge ms: padded 16 -> 1.68, unpadded 16 / 15 / 17 / 19 / 23 -> 2.41 /
+// 1.48 / 1.37 / 1.34 / 1.38)
+#define RS_PW_IT 19
 #endif
 constexpr int kPwM = RS_PW_M;  // sample stride m
 constexpr int kPwCMax = 32;     // samples per chunk c (PwRuns::c) at most
@@ -118,7 +122,10 @@ __global__ void k_pw_bounds(PwRuns R, const K* __restrict__ smk, const uint32_t*
     }
 }
 
-__device__ __forceinline__ int pw_pad(int i) { return i + (i >> 5); }
+#ifndef RS_PW_PAD
+#define RS_PW_PAD 0  // 1: one pad word per 32 in the shared tiles
+#endif
+__device__ __forceinline__ int pw_pad(int i) { return RS_PW_PAD ? i + (i >> 5) : i; }
 
 template <typename K, bool V>
 __global__ void __launch_bounds__(kPwT) k_pw_merge(PwRuns R, const uint32_t* __restrict__ cnt, int cap,
