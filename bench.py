@@ -151,17 +151,23 @@ def oracle_baseline(kind, seed, dist, b, target_s=10.0):
         a = inputs.gen_u64(n, seed, dist)
         vals = inputs.iota_u32(n)
     done, t_total = 0, 0.0
-    while t_total < target_s:
-        t0 = time.perf_counter()
-        if vals is None:
-            oracle.sr(a, b)
-        else:
-            oracle.sr(a, b, vals=vals)
-        t_total += time.perf_counter() - t0
-        done += n
-    return {"value": done / t_total / 1e9, "unit": "Gkeys/s", "cores": 1, "kind": "oracle",
+    prev = os.sched_getaffinity(0)
+    core = min(prev)
+    os.sched_setaffinity(0, {core})  # the serial oracle pinned to one host core
+    try:
+        while t_total < target_s:
+            t0 = time.perf_counter()
+            if vals is None:
+                oracle.sr(a, b)
+            else:
+                oracle.sr(a, b, vals=vals)
+            t_total += time.perf_counter() - t0
+            done += n
+    finally:
+        os.sched_setaffinity(0, prev)
+    return {"value": done / t_total / 1e9, "unit": "Gkeys/s", "cores": 1, "kind": "oracle", "core": core,
             "sample": f"first 2^25 keys of the workload stream (seed {seed}, {dist}), serial SR-{b} oracle "
-                      f"(oracle/sr.c, gcc -O2), {done // n} repetition(s), {t_total:.1f} s"}
+                      f"(oracle/sr.c, gcc -O2), pinned to core {core}, {done // n} repetition(s), {t_total:.1f} s"}
 
 
 def run_reference(args):
@@ -175,6 +181,8 @@ def run_reference(args):
     n = 1 << 25 if kind == "u32" else 1 << 24
     a = inputs.gen_u32(n, seed, dist) if kind == "u32" else inputs.gen_u64(n, seed, dist)
     vals = inputs.iota_u32(n) if kind == "pairs" else None
+    core = min(os.sched_getaffinity(0))
+    os.sched_setaffinity(0, {core})  # one host core, as the "cores" field says
     times = []
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
@@ -184,7 +192,7 @@ def run_reference(args):
             times.append(dt)
     t = sum(times) / len(times)
     v = n / t / 1e9
-    sample = f"first 2^{n.bit_length() - 1} keys of the workload stream per step, serial SR-{b} oracle, 1 core"
+    sample = f"first 2^{n.bit_length() - 1} keys of the workload stream per step, serial SR-{b} oracle, pinned to core {core}"
     print(json.dumps({
         "impl": "reference", "metric": "sorted keys/sec", "value": round(v, 6), "unit": "Gkeys/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
