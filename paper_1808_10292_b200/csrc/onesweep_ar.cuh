@@ -44,6 +44,10 @@
 #ifndef RS_AR_LB_SMALL
 #define RS_AR_LB_SMALL 8
 #endif
+// key loads through the read-only path: bit 0 [rank], bit 1 [scatter] (timing experiments)
+#ifndef RS_AR_LDG
+#define RS_AR_LDG 0
+#endif
 // [store] with the evict-first (streaming) cache hint: -1 u32 keys only (2^27 pass
 // 0.335 -> 0.328 ms, 2^31 4.874 -> 4.858, DRAM bytes unchanged; u64 / pairs flat), 0 / 1
 #ifndef RS_AR_STCS
@@ -266,7 +270,7 @@ __device__ __forceinline__ void onesweep_ar_body(const PassArgs& a) {
 #pragma unroll
                 for (int i = 0; i < G; ++i)
                     kk[i] = KSRC == 1   ? kr[KREG ? g + i : 0]
-                            : KSRC == 2 ? ((uint32_t)((g + i) * 32) < lim ? gk[(g + i) * 32] : ~K(0))
+                            : KSRC == 2 ? ((uint32_t)((g + i) * 32) < lim ? (RS_AR_LDG & 1 ? __ldg(gk + (g + i) * 32) : gk[(g + i) * 32]) : ~K(0))
                                         : in[(g + i) * 32];
 #pragma unroll
                 for (int i = 0; i < G; ++i) {
@@ -362,7 +366,7 @@ __device__ __forceinline__ void onesweep_ar_body(const PassArgs& a) {
 #pragma unroll
                 for (int i = 0; i < G; ++i)
                     kk[i] = KREG        ? kr[KREG ? g + i : 0]
-                            : KSRC == 2 ? ((uint32_t)((g + i) * 32) < lim ? __ldcs(gk + (g + i) * 32) : ~K(0))
+                            : KSRC == 2 ? ((uint32_t)((g + i) * 32) < lim ? (RS_AR_LDG & 2 ? __ldg(gk + (g + i) * 32) : __ldcs(gk + (g + i) * 32)) : ~K(0))
                                         : s_in[ibase + (g + i) * 32];
                 if (RTM) tmem_wait_ld();
 #pragma unroll
