@@ -10,9 +10,10 @@
 //     merge reads the partner's current block in place over NVLink and writes only
 //     the rank's own N outputs (merge.cu merge_range: positions [0, N) for the
 //     rank that keeps the smaller keys, [N, 2N) for the other) into its other
-//     buffer — no copy of the partner's block is ever staged, and each pair moves
-//     N keys across NVLink per side per stage (the paper's 4Ng per round: two
-//     inputs and one output through HBM, one block over the link);
+//     buffer — no copy of the partner's block is ever staged; a rank reads only the
+//     part of the partner's block its half needs (about N/2 keys on random data,
+//     up to N), against the paper's whole-block exchange (4Ng per round: two inputs
+//     and one output through HBM, one block over the link);
 //   4 a one-word all-reduce orders the stages (nobody overwrites a block a peer
 //     may still be reading); the last stage writes the caller's output directly.
 //
