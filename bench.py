@@ -34,6 +34,7 @@ CONFIGS = {
     "c4": ("u32", 1 << 31, 4, "uniform", 8, "BASELINE configs[3]: 2^31 u32 uniform seed 4, radix-256, GSD r=8 over N GPUs"),
     "c3": ("u32", 1 << 27, 3, "uniform", 8, "BASELINE configs[2] (uniform): 2^27 u32 seed 3, radix-256"),
     "c2": ("u32", 1 << 24, 2, "half", 8, "BASELINE configs[1]: 2^24 u32 in [0,2^31) seed 2, radix-256"),
+    "c1": ("u32", 1 << 20, 1, "uniform", 8, "BASELINE configs[0]: 2^20 u32 uniform seed 1, radix-256"),
     "c2b16": ("u32", 1 << 24, 2, "half", 16, "BASELINE configs[1]: 2^24 u32 in [0,2^31) seed 2, radix-65536"),
     "c5": ("pairs", 1 << 30, 5, "uniform", 8, "BASELINE configs[4]: 2^30 (u64 key, u32 index) pairs seed 5, radix-256"),
 }
