@@ -444,8 +444,8 @@ def main():
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get(f"{args.config}:p{p}")
     design, probe = ctypes.c_longlong(), ctypes.c_longlong()
-    L.rs_get_option(b"pass_design", ctypes.byref(design))
-    L.rs_get_option(b"rank_probe", ctypes.byref(probe))
+    L.rs_dev_get_option(b"pass_design", ctypes.byref(design))
+    L.rs_dev_get_option(b"rank_probe", ctypes.byref(probe))
     kname = ("k_onesweep_ar (design 5: atomic ranks)" if design.value == 5 and probe.value == 1
              else f"k_onesweep_* (design {design.value if design.value != 5 else 2})")
     if b == 16:

@@ -121,13 +121,18 @@ rs_status_t rs_digit_histogram(int key_bytes, const void* keys, size_t n, int di
 
 /* NCCL bootstrap: rank 0 calls rs_get_unique_id, the caller broadcasts the
  * 128 bytes (e.g. torch.distributed.broadcast_object_list), then every rank
- * calls rs_comm_create on its own device.  The comm owns an NCCL communicator
- * and a small pinned host buffer.  Blocking, collective. */
+ * calls rs_comm_create on its own device.  The comm owns an NCCL communicator,
+ * a small pinned host buffer and ~200 KB of device scratch, and the CUDA IPC
+ * mappings of peer buffers it opens (a mapping is released as soon as a call no
+ * longer uses it; all of them at rs_comm_destroy).  Blocking, collective.
+ * (One GPU, several ranks as threads: rs_comm_create_local, rsort_dev.h.) */
 rs_status_t rs_get_unique_id(void* uid128);
 rs_status_t rs_comm_create(const void* uid128, int nranks, int rank, int cuda_device, void** comm);
 rs_status_t rs_comm_destroy(void* comm);
 /* GSD oversampling factor r (s = r·p samples per rank; default 8, BASELINE
- * config 4 "oversampling factor 8·p").  Must match on every rank. */
+ * config 4 "oversampling factor 8·p", or the largest r with r·p² <= 8192 below
+ * 8).  COLLECTIVE and blocking: every rank calls it with the same r (checked:
+ * RS_EINVAL on every rank otherwise, or if r·p² > 8192). */
 rs_status_t rs_comm_set_oversampling(void* comm, int r);
 /* Sample selection of the sample sort (§3.3): mode 0 = GSD's regular
  * oversampling (default; r from rs_comm_set_oversampling); mode 1 = GER
@@ -145,18 +150,15 @@ rs_status_t rs_comm_set_oversampling(void* comm, int r);
  * The output capacity (rs_output_capacity) then follows Lemma Sampling1 with
  * ρ = 1: exceeding it has probability ≤ 1/n and returns RS_ECAPACITY. */
 rs_status_t rs_comm_set_sampling(void* comm, int mode, size_t s, uint64_t seed);
+/* (rs_comm_set_sampling is COLLECTIVE and blocking like rs_comm_set_oversampling;
+ * GER / GVR need p <= 256.) */
 /* mode 3 (not a sample sort) = the paper's PR4 across GPUs:
  * per 8-bit digit, a local count-sort round, an all-gather of the p×256 counts,
  * and each rank pulling from every peer (CUDA IPC over NVLink) the keys whose
  * global rank (SPEC.md:206 formula) falls in its range; rank j ends with exactly
  * its input count of the sorted order (balanced).  digit_bits 8 only; every rank
  * must be able to map its peers' memory (else RS_ECUDA on every rank).
- * rs_pr_emulate runs all ranks on one GPU (ws: rs_pr_emulate_ws_bytes). */
-size_t rs_pr_emulate_ws_bytes(int key_bytes, int val_bytes, int p, size_t n_max);
-rs_status_t rs_pr_emulate(int key_bytes, int p, void* const* keys, uint32_t* const* vals, const size_t* n,
-                          void* const* out_keys, uint32_t* const* out_vals, void* ws, size_t ws_bytes,
-                          void* stream);
-/* modes 4 and 5 (network sorts; costs PAPER.md:717-763):
+ * modes 4 and 5 (network sorts; costs PAPER.md:717-763):
  * every rank sorts its block locally (the SR-b above), then the ranks run the
  * p-processor merge-split network over their sorted blocks — mode 4 BTN, the
  * lg p (lg p + 1)/2-stage bitonic network (p must be a power of two), mode 5
@@ -171,176 +173,27 @@ rs_status_t rs_pr_emulate(int key_bytes, int p, void* const* keys, uint32_t* con
  * ends with positions [j·n, (j+1)·n) of the sorted order, so out_cap ≥ n.  Ties
  * merge the lower-indexed block first: OET keeps pairs stable, BTN only moves
  * each value with its key.  The workspace must be one cudaMalloc'd allocation
- * region (it is exported whole); rs_ws_bytes sizes it.
- * rs_net_stages: the number of stages (BTN) / rounds (OET) for p ranks, −1 if
- * p is invalid for the mode.  rs_net_emulate runs all p ranks on this GPU:
- * keys[k] / vals[k] (N each, vals NULL or u32 values of every block; read only),
- * out_keys[j] / out_vals[j] (N each), ws of rs_net_emulate_ws_bytes (device,
- * 16-byte aligned), stream-ordered, no sync. */
-int rs_net_stages(int mode, int p);
-/* The exchange of `rank` in stage `stage` (0-based) of the mode's network, host
- * only: *partner = the other rank of its merge-split (−1: idle this stage),
- * *keep_low = 1 if it keeps the smaller half.  Returns 0, or −1 on a bad argument. */
-int rs_net_schedule(int mode, int p, int stage, int rank, int* partner, int* keep_low);
-size_t rs_net_emulate_ws_bytes(int key_bytes, int val_bytes, int p, int digit_bits, size_t N);
-rs_status_t rs_net_emulate(int mode, int key_bytes, int p, int digit_bits, void* const* keys,
-                           const uint32_t* const* vals, size_t N, void* const* out_keys,
-                           uint32_t* const* out_vals, void* ws, size_t ws_bytes, void* stream);
-/* GER's default s for n keys in all, and the Lemma-Sampling1 capacity for a
- * largest block of n_local_max keys over p ranks (s = 0: the default s). */
-size_t rs_ger_default_s(uint64_t n_total);
-size_t rs_ger_capacity(size_t n_local_max, int p, size_t s);
-/* The p×p count matrix |X_{k,j}| (row k = sender) of the last sample sort on
- * this communicator, into host u64[p*p]; RS_EINVAL before the first sort.
- * (bench.py derives the all-to-all bytes from it.) */
-rs_status_t rs_comm_last_counts(void* comm, uint64_t* counts);
+ * region (it is exported whole). */
 int rs_comm_rank(void* comm);
 int rs_comm_size(void* comm);
 
 /* With comm != NULL, rs_sort_* is the GSD collective: every rank calls it with
- * the same key/value types, digit_bits and r (checked: RS_EINVAL on all ranks
- * on a mismatch).  n may differ per rank.  Rank j receives Y_j, the j-th
- * contiguous slice of the global sorted order, in out[0 .. *n_out).  `keys`
- * (and vals) are used as scratch (they hold X_j, the locally sorted block, on
- * return).  The call blocks the host twice (the header exchange and the p×p
- * count exchange); *n_out is valid on return.  Receive capacity: out_cap <
- * |Y_j| on any rank → RS_ECAPACITY on every rank.  Argument errors on any rank
- * (bad pointers, digit width, workspace too small, mismatched settings) are
- * agreed on in the header exchange: every rank returns RS_EINVAL, none hangs. */
-
-/* rs_gsd_exchange_plan: the host-side plan of GSD's all-to-all (PAPER.md:797-803,
- * "Processor k sends to processor j sequence X_{k,j}") from the all-gathered
- * count matrix counts[k*p + j] = |X_{k,j}| (host, p×p).  For `rank`:
- *   send_off[0..p]: X_{rank,j} = sorted block [send_off[j], send_off[j+1])
- *   recv_off[0..p]: X_{k,rank} lands at [recv_off[k], recv_off[k+1]) of the
- *                   receive buffer, runs in source-rank order (reading R16)
- *   *total = |Y_rank|.
- * caps (host, p entries, may be NULL): every rank's output capacity; any
- * |Y_j| > caps[j] returns RS_ECAPACITY, identically on every rank.
- * Pure host function (no device access); used by the GSD call itself. */
-rs_status_t rs_gsd_exchange_plan(int p, int rank, const uint64_t* counts, const uint64_t* caps,
-                                 uint64_t* send_off, uint64_t* recv_off, uint64_t* total);
-
-/* ---------------------------------------------------------- GSD emulation -- */
-/* rs_gsd_emulate: GSD over p ranks whose blocks all live on THIS GPU, run rank
- * by rank in one stream (no NCCL, nothing waits on another rank): the same
- * kernels and host plan as the multi-GPU path, with device copies standing in
- * for the all-gathers and the all-to-all.  Used to test the multi-GPU path's
- * kernels on one GPU.
- *   keys[k], vals[k] (vals NULL for keys-only), n[k]: the p blocks (scratch).
- *   out_keys[j], out_vals[j], out_cap: per-rank outputs; n_out[j] = |Y_j|.
- *   splitters: NULL or host u64[3*(p-1)] receiving (key, rank, pos) of S_i.
- *   counts:    NULL or host u64[p*p] receiving |X_{k,j}| at [k*p + j].
- *   ws: rs_gsd_emulate_ws_bytes(key_bytes, val_bytes, p, r, digit_bits,
- *       max_k n[k], out_cap) bytes.
- * Blocks the host once (the count exchange), like the multi-GPU call. */
-size_t rs_gsd_emulate_ws_bytes(int key_bytes, int val_bytes, int p, int r, int digit_bits, size_t n_max,
-                               size_t out_cap);
-rs_status_t rs_gsd_emulate(int key_bytes, int p, int r, int digit_bits,
-                           void* const* keys, uint32_t* const* vals, const size_t* n,
-                           void* const* out_keys, uint32_t* const* out_vals, size_t out_cap,
-                           size_t* n_out, uint64_t* splitters, uint64_t* counts,
-                           void* ws, size_t ws_bytes, void* stream);
-
-/* rs_ger_emulate: GER (see rs_comm_set_sampling) over p ranks on this GPU, with
- * the same arguments as rs_gsd_emulate except s and seed in place of r
- * (the draws of every rank go into one array, standing in for the all-reduce).
- *   ws: rs_ger_emulate_ws_bytes(key_bytes, val_bytes, p, s, digit_bits,
- *       max_k n[k], out_cap) bytes (s = 0: sized for n = p·max_k n[k]). */
-size_t rs_ger_emulate_ws_bytes(int key_bytes, int val_bytes, int p, size_t s, int digit_bits, size_t n_max,
-                               size_t out_cap);
-rs_status_t rs_ger_emulate(int key_bytes, int p, size_t s, uint64_t seed, int digit_bits,
-                           void* const* keys, uint32_t* const* vals, const size_t* n,
-                           void* const* out_keys, uint32_t* const* out_vals, size_t out_cap,
-                           size_t* n_out, uint64_t* splitters, uint64_t* counts,
-                           void* ws, size_t ws_bytes, void* stream);
-
-/* rs_gvr_emulate: GVR over p ranks on this GPU, arguments as rs_ger_emulate
- * (the blocks are partitioned by destination in place). */
-size_t rs_gvr_emulate_ws_bytes(int key_bytes, int val_bytes, int p, size_t s, int digit_bits, size_t n_max,
-                               size_t out_cap);
-rs_status_t rs_gvr_emulate(int key_bytes, int p, size_t s, uint64_t seed, int digit_bits,
-                           void* const* keys, uint32_t* const* vals, const size_t* n,
-                           void* const* out_keys, uint32_t* const* out_vals, size_t out_cap,
-                           size_t* n_out, uint64_t* splitters, uint64_t* counts,
-                           void* ws, size_t ws_bytes, void* stream);
-
-/* ------------------------------------------------------------ CUDA IPC -- */
-/* Device-buffer mappings used by the GSD pull merge (gsd_merge = 2, 3): export
- * the IPC handle (64 bytes) of the cudaMalloc allocation containing `ptr` and
- * ptr's byte offset in it; open a peer's (handle, offset) as a local pointer
- * (each handle is opened once per device and cached; rs_ipc_close_all unmaps).
- * Export fails with RS_ECUDA for memory that has no IPC handle (VMM / cuMem
- * allocations); the pull merge then falls back to the all-to-all. */
-rs_status_t rs_ipc_export(const void* ptr, void* handle64, uint64_t* offset);
-rs_status_t rs_ipc_open(const void* handle64, uint64_t offset, void** ptr);
-rs_status_t rs_ipc_close_all(void);
-
-/* --------------------------------------------------------------- options -- */
-/* Process-wide tuning / test knobs (not needed for normal use):
- *   "wide_status"    1 = use 64-bit look-back status words at any n (they are
- *                    used automatically when n > 2^31, where a 31-bit
- *                    inclusive prefix could overflow); lets the tests run that
- *                    path on small n.
- *   "rank_variant"   in-tile ranking: 3 = pairs of keys, one by 8 ballots and one
- *                    by a shared-memory atomic-OR peer mask (default); 0 = ballots;
- *                    2 = atomic-OR masks; 1 = match.any (classic design only).
- *   "pass_design"    radix-256 pass kernel: 5 = atomic ranks (default; used when
- *                    the lane-order probe passes on this device, otherwise 2);
- *                    2 = early counts + tile prefetch, ballot ranks,
- *                    look-back after ranking; 1 = early counts + tile
- *                    prefetch with a dedicated look-back warp; 0 = classic single
- *                    sweep (rank, look-back, reorder, store).
- *   "match_every"    0, 4, 6 or 8: in the default pass (u32 keys) every k-th key is
- *                    ranked with match.any (ADU pipe) instead of ballots (ALU pipe).
- *   "gsd_merge"      GSD step 5 (all give the same Y_j): 3 = pull merge in one
- *                    p-way pass (default): no all-to-all; every peer's X_{k,j}
- *                    is read in place over NVLink through CUDA IPC mappings
- *                    (see below; emulation: the blocks in place), cut into
- *                    chunks by a regular sample of the runs and merged chunk by
- *                    chunk in shared memory, Y_j written once (2 ≤ p ≤ 32, else
- *                    as 2); 2 = pull merge as a tree of 2-way merges whose first
- *                    level reads the peers' blocks; if any rank cannot export or
- *                    map a block, every rank falls back to 0 for that call.
- *                    0 = NCCL all-to-all into a receive buffer, then the tree of
- *                    stable 2-way merge-path merges; 1 = all-to-all, then a
- *                    stable radix re-sort.
- *   "gsd_pull"       1 (default) = modes 2 and 3 pull over NVLink; 0 = they take
- *                    the all-to-all path (the fallback taken when a mapping
- *                    fails), merging the received runs the same way.
- *   "compact"        1 = default pass with 16-bit per-warp counters (smaller
- *                    shared-memory footprint; ballots only).
- *   "small_tiles"    design-5 tiles: 0 = small tiles when the input makes fewer
- *                    than three large tiles per SM (default), 1 = always large,
- *                    2 = always small.
- *   "small_fused"    1 = small-tile full sorts as one cooperative launch (all
- *                    phases separated by grid barriers); 0 = separate kernels
- *                    (default: the fused form measured no faster).
- *   "hist_shared"    1 = digit-histogram kernel with one shared histogram per
- *                    4 warps (0, default: lane-private copies, conflict-free).
- *   "debug_skip"     timing ablations, OUTPUT INVALID: bit 0 no look-back,
- *                    bit 1 no ranking, bit 2 no global store, bit 3 no reorder.
- * Returns RS_EINVAL for an unknown name or a negative value. */
-rs_status_t rs_set_option(const char* name, long long value);
-/* Current value of an rs_set_option knob, or a read-only value: "rank_probe",
- * the result of the design-5 lane-order probe on the current device (-1 not run
- * yet, 0 failed -> design 2 is used, 1 passed); "tile_u32", "tile_u64",
- * "tile_pairs", the radix-256 tile (keys per look-back row) of the selected
- * pass design.  RS_EINVAL for unknown names. */
-rs_status_t rs_get_option(const char* name, long long* value);
-
-/* ---------------------------------------------------------------- timing -- */
-/* Per-kernel device timing for measurement (bench.py): when enabled, every
- * kernel the library launches is bracketed by CUDA events on its own stream.
- * rs_timing_query sums the elapsed ms and launch count of kernels whose name
- * starts with `prefix` (e.g. "onesweep", "hist", "" = all) since the last
- * rs_timing_reset; it synchronises the recorded events. */
-void rs_timing_enable(int on);
-void rs_timing_reset(void);
-rs_status_t rs_timing_query(const char* prefix, double* total_ms, int* launches);
-/* kernel launches issued by the library since the last rs_timing_reset
- * (counted whether or not timing is enabled) */
-long long rs_launch_count(void);
+ * the same key/value types and digit_bits (checked: RS_EINVAL on all ranks on a
+ * mismatch).  n may differ per rank.  Rank j receives Y_j, the j-th contiguous
+ * slice of the global sorted order, in out[0 .. *n_out).  `keys` (and vals) are
+ * used as scratch: they hold X_j, the locally sorted block, on return, also when
+ * the call fails because of ANOTHER rank's arguments.  `out` must not overlap
+ * `keys` (nor out_vals vals) when p > 1.  GSD (mode 0) blocks the host ONCE per
+ * call, on the all-gather of every rank's header and count record; GER / GVR
+ * exchange the headers first (twice); *n_out is valid on return.  Receive
+ * capacity: out_cap < |Y_j| on any rank → RS_ECAPACITY on every rank.  Argument
+ * errors on any rank (bad pointers, digit width, workspace too small, mismatched
+ * types or settings) are agreed on from the all-gathered headers: every rank
+ * returns RS_EINVAL, none hangs (a rank that fails its own checks still takes
+ * part in every exchange with an empty block).  A peer that dies, or an NCCL
+ * asynchronous error, turns a blocking wait into RS_ENCCL after the comm's
+ * timeout (rsort_dev.h rs_comm_set_timeout, default 600 s); the comm is then
+ * unusable and must be destroyed. */
 
 #if defined(__GNUC__)
 #pragma GCC visibility pop

@@ -16,8 +16,8 @@ import torch
 from . import _abi
 from ._abi import RSortError, check, lib
 
-__all__ = ["sort", "sort_pairs", "sort_bits", "digit_histogram", "workspace_bytes", "Comm", "gsd_emulate",
-           "ger_emulate", "gvr_emulate", "pr_emulate", "net_emulate", "net_stages",
+__all__ = ["sort", "sort_pairs", "sort_bits", "digit_histogram", "workspace_bytes", "Comm", "LocalGroup",
+           "sort_ranks", "net_stages", "set_option", "get_option",
            "RSortError", "lib", "rs_sort_u32", "rs_sort_u64", "rs_sort_pairs_u64_u32"]
 
 _KEY_BYTES = {torch.uint32: 4, torch.int32: 4, torch.uint64: 8, torch.int64: 8}
@@ -81,7 +81,9 @@ def sort(keys: torch.Tensor, digit_bits: int = 8, comm: "Comm | None" = None, ou
             out = keys
         cap = out.numel()
     if ws is None:
-        ws = _workspace(lib().rs_workspace_bytes(kb, 0, comm.ws_n(n) if comm else n, digit_bits, h), keys.device)
+        # with a comm: sized for the largest block, and for out_cap if the caller's is larger
+        wn = max(comm.ws_n(n), cap) if comm else n
+        ws = _workspace(lib().rs_workspace_bytes(kb, 0, wn, digit_bits, h), keys.device)
     n_out = ctypes.c_size_t(0)
     fn = lib().rs_sort_u32 if kb == 4 else lib().rs_sort_u64
     check(fn(keys.data_ptr(), n, digit_bits, h, out.data_ptr(), cap, ctypes.byref(n_out), ws.data_ptr(), ws.numel(),
@@ -109,7 +111,8 @@ def sort_pairs(keys: torch.Tensor, vals: torch.Tensor, digit_bits: int = 8, comm
         out_vals = vals if out_vals is None else out_vals
         cap = out_keys.numel()
     if ws is None:
-        ws = _workspace(lib().rs_workspace_bytes(8, 4, comm.ws_n(n) if comm else n, digit_bits, h), keys.device)
+        wn = max(comm.ws_n(n), cap) if comm else n
+        ws = _workspace(lib().rs_workspace_bytes(8, 4, wn, digit_bits, h), keys.device)
     n_out = ctypes.c_size_t(0)
     check(lib().rs_sort_pairs_u64_u32(keys.data_ptr(), vals.data_ptr(), n, digit_bits, h, out_keys.data_ptr(),
                                       out_vals.data_ptr(), cap, ctypes.byref(n_out), ws.data_ptr(), ws.numel(),
@@ -178,41 +181,61 @@ def exchange_plan(counts, rank: int, caps=None):
 
 
 class Comm:
-    """GSD communicator: an NCCL comm owned by librsort, bootstrapped over a
-    torch.distributed process group (only the 128-byte unique id travels)."""
+    """Collective-sort communicator.  Default: an NCCL comm owned by librsort,
+    bootstrapped over a torch.distributed process group (only the 128-byte
+    unique id travels).  Comm.local(group, rank) instead joins an in-process
+    LocalGroup (p threads on one GPU, include/rsort_dev.h)."""
 
-    def __init__(self, group=None, device: int | None = None, oversampling: int = 8):
-        import torch.distributed as dist
-        self.rank = dist.get_rank(group)
-        self.size = dist.get_world_size(group)
-        self.device = torch.cuda.current_device() if device is None else device
-        uid = (ctypes.c_char * 128)()
-        if self.rank == 0:
-            check(lib().rs_get_unique_id(uid), "rs_get_unique_id")
-        obj = [bytes(uid)]
-        src = dist.get_global_rank(group, 0) if group is not None else 0
-        dist.broadcast_object_list(obj, src=src, group=group)
-        uid = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+    def __init__(self, group=None, device: int | None = None, oversampling: int = 8, *, _handle=None,
+                 _rank=None, _size=None, _local=None):
+        if _handle is not None:  # Comm.local
+            self.handle, self.rank, self.size, self._local, self._group = _handle, _rank, _size, _local, None
+            self.device = torch.cuda.current_device()
+        else:
+            import torch.distributed as dist
+            self.rank = dist.get_rank(group)
+            self.size = dist.get_world_size(group)
+            self.device = torch.cuda.current_device() if device is None else device
+            uid = (ctypes.c_char * 128)()
+            if self.rank == 0:
+                check(lib().rs_get_unique_id(uid), "rs_get_unique_id")
+            obj = [bytes(uid)]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(obj, src=src, group=group)
+            uid = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+            h = ctypes.c_void_p()
+            check(lib().rs_comm_create(uid, self.size, self.rank, self.device, ctypes.byref(h)), "rs_comm_create")
+            self.handle = h
+            self._group = group
+            self._local = None
+        self.sampling = "gsd"
+        if oversampling is not None:
+            self.set_oversampling(min(oversampling, max(1, 8192 // (self.size * self.size))))
+
+    @classmethod
+    def local(cls, group: "LocalGroup", rank: int, oversampling: int = 8) -> "Comm":
+        """Rank `rank` of an in-process group; call from that rank's thread (collective)."""
         h = ctypes.c_void_p()
-        check(lib().rs_comm_create(uid, self.size, self.rank, self.device, ctypes.byref(h)), "rs_comm_create")
-        self.handle = h
-        self.set_oversampling(oversampling)
-        # largest local n over ranks, for workspace / capacity sizing
-        self._group = group
+        check(lib().rs_comm_create_local(group.handle, rank, ctypes.byref(h)), "rs_comm_create_local")
+        return cls(oversampling=oversampling, _handle=h, _rank=rank, _size=group.p, _local=group)
 
     def set_oversampling(self, r: int):
+        """Collective: every rank with the same r."""
         check(lib().rs_comm_set_oversampling(self.handle, r), "rs_comm_set_oversampling")
         self.r = r
 
     def set_sampling(self, mode: str = "gsd", s: int = 0, seed: int = 0):
-        """"gsd" (regular oversampling, default), "ger" (random oversampling
-        with s samples per rank, s = 0 the paper's choice, SplitMix64 seed),
-        "gvr" (the same sample, split before sorting), "pr4" (PR4 routing across
-        GPUs), "btn" / "oet" (the bitonic / odd-even transposition merge-split
-        networks over equal sorted blocks)."""
+        """Collective.  "gsd" (regular oversampling, default), "ger" (random
+        oversampling with s samples per rank, s = 0 the paper's choice, SplitMix64
+        seed), "gvr" (the same sample, split before sorting), "pr4" (PR4 routing
+        across GPUs), "btn" / "oet" (the bitonic / odd-even transposition
+        merge-split networks over equal sorted blocks)."""
         m = {"gsd": 0, "ger": 1, "gvr": 2, "pr4": 3, "btn": 4, "oet": 5}[mode]
         check(lib().rs_comm_set_sampling(self.handle, m, s, seed), "rs_comm_set_sampling")
         self.sampling = mode
+
+    def set_timeout(self, ms: int):
+        check(lib().rs_comm_set_timeout(self.handle, ms), "rs_comm_set_timeout")
 
     def last_counts(self):
         """(p, p) uint64 count matrix |X_{k,j}| of the last sort on this communicator."""
@@ -222,10 +245,23 @@ class Comm:
               "rs_comm_last_counts")
         return c
 
+    def last_splitters(self):
+        """(p-1, 3) uint64 (key, rank, pos) splitters of the last sample sort."""
+        import numpy as np
+        sp = np.zeros((max(self.size - 1, 1), 3), dtype=np.uint64)
+        check(lib().rs_comm_last_splitters(self.handle, sp.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))),
+              "rs_comm_last_splitters")
+        return sp[: self.size - 1]
+
+    def last_host_syncs(self) -> int:
+        return lib().rs_comm_last_host_syncs(self.handle)
+
     def capacity(self, n_local: int) -> int:
         return lib().rs_output_capacity(self.ws_n(n_local), self.handle)
 
     def ws_n(self, n_local: int) -> int:
+        if self._local is not None:
+            return self._local.allreduce_max(self.rank, n_local)
         return max_over_ranks(n_local, self._group)
 
     def close(self):
@@ -240,39 +276,122 @@ class Comm:
             pass
 
 
-def gsd_emulate(blocks: list[torch.Tensor], r: int = 8, digit_bits: int = 8, vals: list[torch.Tensor] | None = None,
-                out_cap: int | None = None, stream=None):
-    """GSD over p = len(blocks) ranks held on this GPU (see include/rsort.h):
-    returns dict(Y, Yv, n_out, splitters (p-1,3) uint64, counts (p,p) uint64)."""
-    return _emulate(0, blocks, r, 0, 0, digit_bits, vals, out_cap, stream)
+class LocalGroup:
+    """p ranks as p threads of this process on the current GPU: the multi-GPU
+    collective (rs_sort_* with a comm) run through host barriers and device
+    copies (include/rsort_dev.h).  run(fn) calls fn(comm) on p threads, each with
+    its own CUDA stream and Comm.local, and returns the p results."""
+
+    def __init__(self, p: int):
+        import threading
+        self.p = p
+        h = ctypes.c_void_p()
+        check(lib().rs_local_group_create(p, ctypes.byref(h)), "rs_local_group_create")
+        self.handle = h
+        self._bar = threading.Barrier(p)
+        self._vals = [0] * p
+
+    def allreduce_max(self, rank: int, value: int) -> int:
+        self._vals[rank] = value
+        self._bar.wait()
+        m = max(self._vals)
+        self._bar.wait()
+        return m
+
+    def run(self, fn, oversampling: int = 8, timeout_ms: int | None = None):
+        import threading
+        torch.cuda.synchronize()
+        dev = torch.cuda.current_device()
+        res, err = [None] * self.p, [None] * self.p
+
+        def body(k):
+            try:
+                torch.cuda.set_device(dev)
+                st = torch.cuda.Stream()
+                with torch.cuda.stream(st):
+                    c = Comm.local(self, k, oversampling)
+                    if timeout_ms is not None:
+                        c.set_timeout(timeout_ms)
+                    try:
+                        res[k] = fn(c)
+                    finally:
+                        st.synchronize()
+                        c.close()
+            except BaseException as e:  # re-raised on the caller's thread
+                err[k] = e
+                try:
+                    self._bar.abort()
+                except Exception:
+                    pass
+
+        th = [threading.Thread(target=body, args=(k,)) for k in range(self.p)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join()
+        for e in err:
+            if e is not None:
+                raise e
+        return res
+
+    def close(self):
+        if self.handle:
+            lib().rs_local_group_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
-def ger_emulate(blocks: list[torch.Tensor], s: int = 0, seed: int = 0, digit_bits: int = 8,
-                vals: list[torch.Tensor] | None = None, out_cap: int | None = None, stream=None):
-    """GER (random oversampling) over p = len(blocks) ranks on
-    this GPU; s = 0 selects the paper's s.  Same result dict as gsd_emulate."""
-    return _emulate(1, blocks, 1, s, seed, digit_bits, vals, out_cap, stream)
+_MODES = ("gsd", "ger", "gvr", "pr4", "btn", "oet")
 
 
-def pr_emulate(blocks: list[torch.Tensor], vals: list[torch.Tensor] | None = None, stream=None):
-    """PR4 across p = len(blocks) ranks held on this GPU (per-digit local round,
-    count exchange, pull of each rank's global-rank range): returns dict(Y, Yv)
-    with |Y_j| = |blocks[j]|.  The blocks are scratch."""
+def sort_ranks(blocks: list[torch.Tensor], mode: str = "gsd", digit_bits: int = 8,
+               vals: list[torch.Tensor] | None = None, r: int = 8, s: int = 0, seed: int = 0,
+               out_cap: int | None = None, out_caps: list[int] | None = None):
+    """The collective sort over p = len(blocks) in-process ranks on this GPU
+    (LocalGroup): rank k calls rs_sort_* with block k (used as scratch) through
+    its own Comm.  Returns dict(Y, Yv, n_out, counts (p,p), splitters (p-1,3),
+    host_syncs, capacity) — the same call a multi-GPU job makes on each rank."""
+    import numpy as np
     p = len(blocks)
+    g = LocalGroup(p)
     kb = _KEY_BYTES[blocks[0].dtype]
-    n = [b.numel() for b in blocks]
-    dev = blocks[0].device
-    outs = [torch.empty(max(x, 1), dtype=blocks[0].dtype, device=dev) for x in n]
-    vouts = [torch.empty(max(x, 1), dtype=torch.int32, device=dev) for x in n] if vals is not None else None
-    ws = _workspace(lib().rs_pr_emulate_ws_bytes(kb, 4 if vals is not None else 0, p, max(n) if n else 0), dev)
-    arr = ctypes.c_void_p * p
-    check(lib().rs_pr_emulate(kb, p, arr(*[b.data_ptr() for b in blocks]),
-                              arr(*[v.data_ptr() for v in vals]) if vals is not None else None,
-                              (ctypes.c_size_t * p)(*n), arr(*[o.data_ptr() for o in outs]),
-                              arr(*[o.data_ptr() for o in vouts]) if vals is not None else None,
-                              ws.data_ptr(), ws.numel(), _stream(stream)), "rs_pr_emulate")
-    return dict(Y=[outs[j][: n[j]] for j in range(p)],
-                Yv=[vouts[j][: n[j]] for j in range(p)] if vals is not None else None)
+
+    def rank_fn(c: Comm):
+        k = c.rank
+        if mode != "gsd":
+            c.set_sampling(mode, s, seed)
+        x = blocks[k]
+        v = vals[k] if vals is not None else None
+        cap = out_caps[k] if out_caps is not None else (out_cap if out_cap is not None else c.capacity(x.numel()))
+        if v is None:
+            y = sort(x, digit_bits, comm=c, out_cap=cap)
+            yv = None
+        else:
+            y, yv = sort_pairs(x, v, digit_bits, comm=c, out_cap=cap)
+        torch.cuda.current_stream().synchronize()
+        info = dict(Y=y, Yv=yv, host_syncs=c.last_host_syncs(), capacity=cap)
+        if mode in ("gsd", "ger", "gvr"):
+            info["counts"] = c.last_counts()
+            info["splitters"] = c.last_splitters()
+        return info
+
+    try:
+        out = g.run(rank_fn, oversampling=min(r, max(1, 8192 // (p * p))))
+    finally:
+        g.close()
+    res = dict(Y=[o["Y"] for o in out], Yv=[o["Yv"] for o in out] if vals is not None else None,
+               n_out=[int(o["Y"].numel()) for o in out], host_syncs=[o["host_syncs"] for o in out],
+               capacity=[o["capacity"] for o in out])
+    if mode in ("gsd", "ger", "gvr"):
+        res["counts"] = out[0]["counts"]
+        res["splitters"] = out[0]["splitters"]
+    del kb
+    return res
 
 
 def net_stages(mode: str, p: int) -> int:
@@ -283,71 +402,11 @@ def net_stages(mode: str, p: int) -> int:
     return st
 
 
-def net_emulate(mode: str, blocks: list[torch.Tensor], digit_bits: int = 8,
-                vals: list[torch.Tensor] | None = None, stream=None):
-    """BTN ("btn") or OET ("oet") over p = len(blocks) ranks held on this GPU:
-    local radix sort of every block, then the merge-split network.
-    Blocks must have equal sizes; they are read only.  Returns dict(Y, Yv)."""
-    p = len(blocks)
-    kb = _KEY_BYTES[blocks[0].dtype]
-    N = blocks[0].numel()
-    if any(b.numel() != N for b in blocks):
-        raise ValueError("BTN/OET need equal block sizes")
-    dev = blocks[0].device
-    outs = [torch.empty(max(N, 1), dtype=blocks[0].dtype, device=dev) for _ in range(p)]
-    vouts = [torch.empty(max(N, 1), dtype=torch.int32, device=dev) for _ in range(p)] if vals is not None else None
-    vb = 4 if vals is not None else 0
-    ws = _workspace(lib().rs_net_emulate_ws_bytes(kb, vb, p, digit_bits, N), dev)
-    arr = ctypes.c_void_p * p
-    check(lib().rs_net_emulate({"btn": 4, "oet": 5}[mode], kb, p, digit_bits, arr(*[b.data_ptr() for b in blocks]),
-                               arr(*[v.data_ptr() for v in vals]) if vals is not None else None, N,
-                               arr(*[o.data_ptr() for o in outs]),
-                               arr(*[o.data_ptr() for o in vouts]) if vals is not None else None,
-                               ws.data_ptr(), ws.numel(), _stream(stream)), "rs_net_emulate")
-    return dict(Y=[o[:N] for o in outs], Yv=[o[:N] for o in vouts] if vals is not None else None)
+def set_option(name: str, value: int):
+    check(lib().rs_dev_set_option(name.encode(), value), "rs_dev_set_option")
 
 
-def gvr_emulate(blocks: list[torch.Tensor], s: int = 0, seed: int = 0, digit_bits: int = 8,
-                vals: list[torch.Tensor] | None = None, out_cap: int | None = None, stream=None):
-    """GVR (split, exchange, then sort) over p = len(blocks)
-    ranks on this GPU; the blocks are used as scratch.  Same result dict."""
-    return _emulate(2, blocks, 1, s, seed, digit_bits, vals, out_cap, stream)
-
-
-def _emulate(mode, blocks, r, s, seed, digit_bits, vals, out_cap, stream):
-    import numpy as np
-    p = len(blocks)
-    kb = _KEY_BYTES[blocks[0].dtype]
-    n = [b.numel() for b in blocks]
-    nmax = max(n) if n else 0
-    if out_cap is not None:
-        cap = out_cap
-    elif mode == 0:
-        cap = nmax + nmax // r + p
-    else:
-        cap = lib().rs_ger_capacity(nmax, p, s)
-    dev = blocks[0].device
-    outs = [torch.empty(max(cap, 1), dtype=blocks[0].dtype, device=dev) for _ in range(p)]
-    vouts = [torch.empty(max(cap, 1), dtype=torch.int32, device=dev) for _ in range(p)] if vals is not None else None
-    vb = 4 if vals is not None else 0
-    wsb = (lib().rs_gsd_emulate_ws_bytes(kb, vb, p, r, digit_bits, nmax, cap) if mode == 0
-           else (lib().rs_ger_emulate_ws_bytes if mode == 1 else lib().rs_gvr_emulate_ws_bytes)(
-               kb, vb, p, s, digit_bits, nmax, cap))
-    ws = _workspace(wsb, dev)
-    arr = ctypes.c_void_p * p
-    n_arr = (ctypes.c_size_t * p)(*n)
-    n_out = (ctypes.c_size_t * p)()
-    spl = np.zeros((max(p - 1, 1), 3), dtype=np.uint64)
-    counts = np.zeros((p, p), dtype=np.uint64)
-    head = (kb, p, r) if mode == 0 else (kb, p, s, seed)
-    fn = [lib().rs_gsd_emulate, lib().rs_ger_emulate, lib().rs_gvr_emulate][mode]
-    check(fn(*head, digit_bits, arr(*[b.data_ptr() for b in blocks]),
-             arr(*[v.data_ptr() for v in vals]) if vals is not None else None, n_arr,
-             arr(*[o.data_ptr() for o in outs]),
-             arr(*[o.data_ptr() for o in vouts]) if vals is not None else None, cap, n_out,
-             spl.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)),
-             counts.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), ws.data_ptr(), ws.numel(),
-             _stream(stream)), ["rs_gsd_emulate", "rs_ger_emulate", "rs_gvr_emulate"][mode])
-    return dict(Y=[outs[j][: n_out[j]] for j in range(p)],
-                Yv=[vouts[j][: n_out[j]] for j in range(p)] if vals is not None else None,
-                n_out=list(n_out), splitters=spl[: p - 1], counts=counts)
+def get_option(name: str) -> int:
+    v = ctypes.c_longlong()
+    check(lib().rs_dev_get_option(name.encode(), ctypes.byref(v)), "rs_dev_get_option")
+    return int(v.value)

@@ -9,7 +9,7 @@ import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("RS_LIB_PATH", os.path.join(HERE, "librsort.so"))
-HEADER = os.path.join(os.path.dirname(HERE), "include", "rsort.h")
+HEADERS = [os.path.join(os.path.dirname(HERE), "include", h) for h in ("rsort.h", "rsort_dev.h")]
 
 RS_OK, RS_EINVAL, RS_ECUDA, RS_ENCCL, RS_ENOMEM, RS_ECAPACITY = range(6)
 
@@ -19,6 +19,7 @@ _vpp = ctypes.POINTER(ctypes.c_void_p)
 
 # name -> (restype, argtypes)
 SIGNATURES = {
+    # include/rsort.h
     "rs_status_string": (ctypes.c_char_p, [_i32]),
     "rs_last_error": (ctypes.c_char_p, []),
     "rs_version": (ctypes.c_char_p, []),
@@ -34,46 +35,44 @@ SIGNATURES = {
     "rs_comm_destroy": (_i32, [_vp]),
     "rs_comm_set_oversampling": (_i32, [_vp, _i32]),
     "rs_comm_set_sampling": (_i32, [_vp, _i32, _sz, ctypes.c_uint64]),
+    "rs_comm_rank": (_i32, [_vp]),
+    "rs_comm_size": (_i32, [_vp]),
+    # include/rsort_dev.h
+    "rs_local_group_create": (_i32, [_i32, _vpp]),
+    "rs_local_group_destroy": (_i32, [_vp]),
+    "rs_comm_create_local": (_i32, [_vp, _i32, _vpp]),
     "rs_comm_last_counts": (_i32, [_vp, _u64p]),
+    "rs_comm_last_splitters": (_i32, [_vp, _u64p]),
+    "rs_comm_last_host_syncs": (_i32, [_vp]),
+    "rs_comm_set_timeout": (_i32, [_vp, _i32]),
+    "rs_gsd_exchange_plan": (_i32, [_i32, _i32, _u64p, _u64p, _u64p, _u64p, _u64p]),
+    "rs_net_stages": (_i32, [_i32, _i32]),
+    "rs_net_schedule": (_i32, [_i32, _i32, _i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
+    "rs_ger_default_s": (_sz, [ctypes.c_uint64]),
+    "rs_ger_capacity": (_sz, [_sz, _i32, _sz]),
     "rs_ipc_export": (_i32, [_vp, _vp, _u64p]),
     "rs_ipc_open": (_i32, [_vp, ctypes.c_uint64, _vpp]),
     "rs_ipc_close_all": (_i32, []),
-    "rs_pr_emulate_ws_bytes": (_sz, [_i32, _i32, _i32, _sz]),
-    "rs_pr_emulate": (_i32, [_i32, _i32, _vpp, _vpp, _szp, _vpp, _vpp, _vp, _sz, _vp]),
-    "rs_net_stages": (_i32, [_i32, _i32]),
-    "rs_net_schedule": (_i32, [_i32, _i32, _i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
-    "rs_net_emulate_ws_bytes": (_sz, [_i32, _i32, _i32, _i32, _sz]),
-    "rs_net_emulate": (_i32, [_i32, _i32, _i32, _i32, _vpp, _vpp, _sz, _vpp, _vpp, _vp, _sz, _vp]),
-    "rs_ger_default_s": (_sz, [ctypes.c_uint64]),
-    "rs_ger_capacity": (_sz, [_sz, _i32, _sz]),
-    "rs_ger_emulate_ws_bytes": (_sz, [_i32, _i32, _i32, _sz, _i32, _sz, _sz]),
-    "rs_gvr_emulate_ws_bytes": (_sz, [_i32, _i32, _i32, _sz, _i32, _sz, _sz]),
-    "rs_comm_rank": (_i32, [_vp]),
-    "rs_comm_size": (_i32, [_vp]),
-    "rs_gsd_exchange_plan": (_i32, [_i32, _i32, _u64p, _u64p, _u64p, _u64p, _u64p]),
-    "rs_gsd_emulate_ws_bytes": (_sz, [_i32, _i32, _i32, _i32, _i32, _sz, _sz]),
-    "rs_gsd_emulate": (_i32, [_i32, _i32, _i32, _i32, _vpp, _vpp, _szp, _vpp, _vpp, _sz, _szp, _u64p, _u64p,
-                              _vp, _sz, _vp]),
-    "rs_ger_emulate": (_i32, [_i32, _i32, _sz, ctypes.c_uint64, _i32, _vpp, _vpp, _szp, _vpp, _vpp, _sz, _szp,
-                              _u64p, _u64p, _vp, _sz, _vp]),
-    "rs_gvr_emulate": (_i32, [_i32, _i32, _sz, ctypes.c_uint64, _i32, _vpp, _vpp, _szp, _vpp, _vpp, _sz, _szp,
-                              _u64p, _u64p, _vp, _sz, _vp]),
+    "rs_dev_set_option": (_i32, [ctypes.c_char_p, ctypes.c_longlong]),
+    "rs_dev_get_option": (_i32, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_longlong)]),
     "rs_timing_enable": (None, [_i32]),
     "rs_timing_reset": (None, []),
     "rs_timing_query": (_i32, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i32)]),
     "rs_launch_count": (ctypes.c_longlong, []),
-    "rs_set_option": (_i32, [ctypes.c_char_p, ctypes.c_longlong]),
-    "rs_get_option": (_i32, [ctypes.c_char_p, ctypes.POINTER(ctypes.c_longlong)]),
 }
 
 _lib = None
 
 
-def header_symbols() -> list[str]:
-    """Every function name include/rsort.h declares."""
-    src = open(HEADER).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(rs_[a-z0-9_]+)\s*\(", src)))
+def header_symbols(which: str | None = None) -> list[str]:
+    """Every function name include/rsort.h and include/rsort_dev.h declare (or one of them)."""
+    names = set()
+    for path in HEADERS:
+        if which is not None and os.path.basename(path) != which:
+            continue
+        src = re.sub(r"/\*.*?\*/", "", open(path).read(), flags=re.S)
+        names |= set(re.findall(r"\b(rs_[a-z0-9_]+)\s*\(", src))
+    return sorted(names)
 
 
 def lib() -> ctypes.CDLL:

@@ -35,7 +35,7 @@ def _sources():
 
 def _deps():
     return _sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) + \
-        [os.path.join(ROOT, "include", "rsort.h"), __file__]
+        [os.path.join(ROOT, "include", "rsort.h"), os.path.join(ROOT, "include", "rsort_dev.h"), __file__]
 
 
 def up_to_date() -> bool:

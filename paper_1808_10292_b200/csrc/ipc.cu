@@ -3,8 +3,10 @@
 //
 // A buffer is exported as the IPC handle of its cudaMalloc allocation plus the
 // byte offset of the pointer inside it (torch tensors are sub-allocations of
-// larger segments); an importer opens each distinct handle once
-// (cudaIpcMemLazyEnablePeerAccess) and caches the mapping per device.
+// larger segments).  Opening is reference counted per (device, handle): a handle
+// is mapped once however many communicators use it, and unmapped when the last
+// user releases it (the NCCL transport releases a mapping as soon as a collective
+// call no longer uses it, and all of them when the comm is destroyed).
 #include <cuda.h>
 
 #include <cstring>
@@ -32,8 +34,12 @@ GetRange get_range_fn() {
     return fn;
 }
 
+struct Mapping {
+    void* base;
+    int refs;
+};
 std::mutex g_mu;
-std::map<std::pair<int, std::string>, void*> g_open;  // (device, handle bytes) -> mapped base
+std::map<std::pair<int, std::string>, Mapping> g_open;  // (device, handle bytes) -> mapping
 
 }  // namespace
 
@@ -43,7 +49,7 @@ rs_status_t ipc_export(const void* ptr, void* handle64, uint64_t* offset) {
     CUdeviceptr base = 0;
     size_t size = 0;
     if (fn(&base, &size, reinterpret_cast<CUdeviceptr>(ptr)) != CUDA_SUCCESS)
-        return fail(RS_EINVAL, "rs_ipc_export: pointer is not device memory");
+        return fail(RS_EINVAL, "ipc export: pointer is not device memory");
     cudaIpcMemHandle_t h;
     cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
     if (e != cudaSuccess) return cuda_fail(e, "cudaIpcGetMemHandle (VMM / non-cudaMalloc memory?)");
@@ -53,7 +59,8 @@ rs_status_t ipc_export(const void* ptr, void* handle64, uint64_t* offset) {
     return RS_OK;
 }
 
-rs_status_t ipc_open(const void* handle64, uint64_t offset, void** ptr) {
+// map (or reference again) the allocation of handle64; *base = its mapped start
+rs_status_t ipc_open_ref(const void* handle64, void** base) {
     int dev = 0;
     RS_CUDA_TRY(cudaGetDevice(&dev));
     const std::pair<int, std::string> key(dev, std::string(static_cast<const char*>(handle64), 64));
@@ -62,12 +69,37 @@ rs_status_t ipc_open(const void* handle64, uint64_t offset, void** ptr) {
     if (it == g_open.end()) {
         cudaIpcMemHandle_t h;
         std::memcpy(&h, handle64, sizeof(h));
-        void* base = nullptr;
-        RS_CUDA_TRY(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
-        it = g_open.emplace(key, base).first;
+        void* b = nullptr;
+        RS_CUDA_TRY(cudaIpcOpenMemHandle(&b, h, cudaIpcMemLazyEnablePeerAccess));
+        it = g_open.emplace(key, Mapping{b, 0}).first;
     }
-    *ptr = static_cast<char*>(it->second) + offset;
+    ++it->second.refs;
+    *base = it->second.base;
     return RS_OK;
+}
+
+// drop one reference to the mapping at `base`; unmapped at zero
+void ipc_release(void* base) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    for (auto it = g_open.begin(); it != g_open.end(); ++it)
+        if (it->second.base == base) {
+            if (--it->second.refs <= 0) {
+                int cur = 0;
+                cudaGetDevice(&cur);
+                cudaSetDevice(it->first.first);
+                cudaIpcCloseMemHandle(base);
+                cudaSetDevice(cur);
+                g_open.erase(it);
+            }
+            return;
+        }
+}
+
+rs_status_t ipc_open(const void* handle64, uint64_t offset, void** ptr) {
+    void* base = nullptr;
+    rs_status_t s = ipc_open_ref(handle64, &base);
+    if (s == RS_OK) *ptr = static_cast<char*>(base) + offset;
+    return s;
 }
 
 rs_status_t ipc_close_all() {
@@ -77,7 +109,7 @@ rs_status_t ipc_close_all() {
         int cur = 0;
         cudaGetDevice(&cur);
         cudaSetDevice(kv.first.first);
-        if (cudaIpcCloseMemHandle(kv.second) != cudaSuccess) s = RS_ECUDA;
+        if (cudaIpcCloseMemHandle(kv.second.base) != cudaSuccess) s = RS_ECUDA;
         cudaSetDevice(cur);
     }
     g_open.clear();

@@ -165,11 +165,8 @@ static rs_status_t merge2_range(const K* A, const uint32_t* VA, size_t na, const
     }
     {
         const size_t smem = (size_t)kMTilePad * (sizeof(K) + (V ? 4 : 0));
-        static bool attr = false;
-        if (!attr) {
-            RS_CUDA_TRY(cudaFuncSetAttribute(k_merge_tile<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
-        }
+        rs_status_t s = kernel_setup(reinterpret_cast<const void*>(k_merge_tile<K, V>), kMT, smem, nullptr);
+        if (s != RS_OK) return s;
         LaunchScope ls("merge_tile", st);
         k_merge_tile<K, V><<<(unsigned)ntiles, kMT, smem, st>>>(A, VA, na, B, VB, nb, split, lo, hi, out, vout);
     }

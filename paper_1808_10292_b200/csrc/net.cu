@@ -14,7 +14,7 @@
 //     part of the partner's block its half needs (about N/2 keys on random data,
 //     up to N), against the paper's whole-block exchange (4Ng per round: two inputs
 //     and one output through HBM, one block over the link);
-//   4 a one-word all-reduce orders the stages (nobody overwrites a block a peer
+//   4 a stage barrier of the transport orders the stages (nobody overwrites a block a peer
 //     may still be reading); the last stage writes the caller's output directly.
 //
 // Readings (R32-R34): standard bitonic network, OET round parity, equal
@@ -28,13 +28,6 @@
 
 namespace rs {
 namespace {
-
-#define RS_NCCL_TRY3(expr)                                                             \
-    do {                                                                               \
-        ncclResult_t r_ = (expr);                                                      \
-        if (r_ != ncclSuccess)                                                         \
-            return fail(RS_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
-    } while (0)
 
 struct NetLayout {
     void* local_ws;
@@ -135,39 +128,21 @@ rs_status_t net_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
     rs_status_t s = local_sort(key_bytes, keys, vals, n, b, key_bytes * 8, L.X[0], L.V[0], L.local_ws,
                                L.local_ws_bytes, st);
     if (s != RS_OK) return s;
-    // map every peer's workspace; the all-gather also orders all local sorts before any read
-    uint64_t* h = c->h_pinned;
-    std::memset(h, 0, kIpcWords * 8);
-    h[18] = ipc_export(ws, h, &h[8]) == RS_OK ? 1 : 0;
-    RS_CUDA_TRY(cudaMemcpyAsync(c->d_ipc, h, kIpcWords * 8, cudaMemcpyHostToDevice, st));
-    RS_NCCL_TRY3(ncclAllGather(c->d_ipc, c->d_ipc + kIpcWords, kIpcWords, ncclUint64, c->nccl, st));
-    RS_CUDA_TRY(cudaMemcpyAsync(h, c->d_ipc + kIpcWords, (size_t)p * kIpcWords * 8, cudaMemcpyDeviceToHost, st));
-    RS_CUDA_TRY(cudaStreamSynchronize(st));
-    std::vector<char*> peer_ws(p, nullptr);
-    bool ok = true;
-    for (int k = 0; k < p; ++k) ok = ok && h[(size_t)k * kIpcWords + 18] == 1;
-    for (int k = 0; k < p && ok; ++k) {
-        void* base = ws;
-        if (k != rank) ok = ipc_open(h + (size_t)k * kIpcWords, h[(size_t)k * kIpcWords + 8], &base) == RS_OK;
-        peer_ws[k] = static_cast<char*>(base);
-    }
-    h[0] = ok ? 0 : 1;
-    RS_CUDA_TRY(cudaMemcpyAsync(c->d_ipc, h, 8, cudaMemcpyHostToDevice, st));
-    RS_NCCL_TRY3(ncclAllReduce(c->d_ipc, c->d_ipc, 1, ncclUint64, ncclMax, c->nccl, st));
-    RS_CUDA_TRY(cudaMemcpyAsync(h, c->d_ipc, 8, cudaMemcpyDeviceToHost, st));
-    RS_CUDA_TRY(cudaStreamSynchronize(st));
-    if (h[0]) return fail(RS_ECUDA, "BTN/OET across GPUs needs every rank to map every peer's workspace (CUDA IPC)");
+    // map every peer's workspace; the exchange also orders all local sorts before any read
+    const void* mine[1] = {ws};
+    std::vector<void*> peer_ws;
+    if ((s = map_peer_buffers(c, mine, 1, &peer_ws, st)) != RS_OK) return s;
     // the peer's copy of a layout pointer: same layout (equal n, b) at the peer's base
     auto at_peer = [&](int k, const void* local) -> const void* {
         if (!local) return nullptr;
-        return peer_ws[k] + (static_cast<const char*>(local) - static_cast<const char*>(ws));
+        return static_cast<char*>(peer_ws[k]) + (static_cast<const char*>(local) - static_cast<const char*>(ws));
     };
     const auto S = net_schedule(c->sampling, p);
     std::vector<int> cur(p, 0);
     bool in_out = false;
     {
         LaunchScope ls("net_stages", st, false);
-        for (size_t t = 0; t < S.size(); ++t) {
+        for (size_t t = 0; t < S.size() && s == RS_OK; ++t) {
             const NetExchange e = S[t][rank];
             const bool last = t + 1 == S.size();
             if (e.partner >= 0) {
@@ -176,67 +151,23 @@ rs_status_t net_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
                 uint32_t* vdst = hv ? (last ? vout : L.V[cur[rank] ^ 1]) : nullptr;
                 const void* Xq = at_peer(q, L.X[cur[q]]);
                 const uint32_t* Vq = hv ? static_cast<const uint32_t*>(at_peer(q, L.V[cur[q]])) : nullptr;
-                if ((s = merge_split_half(key_bytes, n, rank, q, e.keep_low, L.X[cur[rank]], hv ? L.V[cur[rank]] : nullptr,
-                                          Xq, Vq, dst, vdst, L.split, st)) != RS_OK)
-                    return s;
+                s = merge_split_half(key_bytes, n, rank, q, e.keep_low, L.X[cur[rank]], hv ? L.V[cur[rank]] : nullptr,
+                                     Xq, Vq, dst, vdst, L.split, st);
                 in_out = last;
             }
             for (int k = 0; k < p; ++k)
                 if (S[t][k].partner >= 0) cur[k] ^= 1;
             // stage barrier: no rank overwrites a block before its partner has read it
-            RS_NCCL_TRY3(ncclAllReduce(c->d_ipc, c->d_ipc, 1, ncclUint64, ncclMax, c->nccl, st));
+            const rs_status_t bs = c->tr->barrier(st);
+            if (s == RS_OK) s = bs;
         }
     }
+    c->tr->release_unused();
+    if (s != RS_OK) return s;
     if (!in_out) {  // idle in the last stage (OET end ranks)
         RS_CUDA_TRY(cudaMemcpyAsync(out, L.X[cur[rank]], n * key_bytes, cudaMemcpyDeviceToDevice, st));
         if (hv) RS_CUDA_TRY(cudaMemcpyAsync(vout, L.V[cur[rank]], n * 4, cudaMemcpyDeviceToDevice, st));
     }
-    RS_CUDA_TRY(cudaGetLastError());
-    return RS_OK;
-}
-
-// all p ranks on this GPU: keys[k] (N each, read) -> out_keys[j] (N each)
-rs_status_t net_emulate(int mode, int key_bytes, int p, int b, void* const* keys, const uint32_t* const* vals, size_t N,
-                        void* const* out_keys, uint32_t* const* out_vals, void* ws, size_t ws_bytes, cudaStream_t st) {
-    const bool hv = vals != nullptr;
-    const size_t per = net_layout(nullptr, key_bytes, hv, N, b).bytes;
-    if (!ws || ws_bytes < per * (size_t)p)
-        return fail(RS_EINVAL, "net emulate workspace too small: need " + std::to_string(per * p));
-    std::vector<NetLayout> L(p);
-    for (int k = 0; k < p; ++k) L[k] = net_layout(static_cast<char*>(ws) + per * k, key_bytes, hv, N, b);
-    if (N == 0) return RS_OK;
-    const auto S = net_schedule(mode, p);
-    for (int k = 0; k < p; ++k) {
-        void* dst = S.empty() ? out_keys[k] : L[k].X[0];
-        uint32_t* vdst = hv ? (S.empty() ? out_vals[k] : L[k].V[0]) : nullptr;
-        rs_status_t s = local_sort(key_bytes, keys[k], hv ? vals[k] : nullptr, N, b, key_bytes * 8, dst, vdst,
-                                   L[k].local_ws, L[k].local_ws_bytes, st);
-        if (s != RS_OK) return s;
-    }
-    if (S.empty()) return RS_OK;
-    std::vector<int> cur(p, 0);
-    std::vector<bool> in_out(p, false);
-    for (size_t t = 0; t < S.size(); ++t) {
-        const bool last = t + 1 == S.size();
-        for (int k = 0; k < p; ++k) {
-            const NetExchange e = S[t][k];
-            if (e.partner < 0) continue;
-            const int q = e.partner;
-            void* dst = last ? out_keys[k] : L[k].X[cur[k] ^ 1];
-            uint32_t* vdst = hv ? (last ? out_vals[k] : L[k].V[cur[k] ^ 1]) : nullptr;
-            rs_status_t s = merge_split_half(key_bytes, N, k, q, e.keep_low, L[k].X[cur[k]], hv ? L[k].V[cur[k]] : nullptr,
-                                             L[q].X[cur[q]], hv ? L[q].V[cur[q]] : nullptr, dst, vdst, L[k].split, st);
-            if (s != RS_OK) return s;
-            in_out[k] = last;
-        }
-        for (int k = 0; k < p; ++k)
-            if (S[t][k].partner >= 0) cur[k] ^= 1;
-    }
-    for (int k = 0; k < p; ++k)
-        if (!in_out[k]) {
-            RS_CUDA_TRY(cudaMemcpyAsync(out_keys[k], L[k].X[cur[k]], N * key_bytes, cudaMemcpyDeviceToDevice, st));
-            if (hv) RS_CUDA_TRY(cudaMemcpyAsync(out_vals[k], L[k].V[cur[k]], N * 4, cudaMemcpyDeviceToDevice, st));
-        }
     RS_CUDA_TRY(cudaGetLastError());
     return RS_OK;
 }
@@ -257,26 +188,6 @@ int rs_net_schedule(int mode, int p, int stage, int rank, int* partner, int* kee
     *partner = S[stage][rank].partner;
     *keep_low = S[stage][rank].keep_low ? 1 : 0;
     return 0;
-}
-
-size_t rs_net_emulate_ws_bytes(int key_bytes, int val_bytes, int p, int digit_bits, size_t N) {
-    if (p < 1 || (key_bytes != 4 && key_bytes != 8) || (digit_bits != 8 && digit_bits != 16)) return 0;
-    return rs::net_ws_bytes(key_bytes, val_bytes != 0, N, digit_bits) * (size_t)p;
-}
-
-rs_status_t rs_net_emulate(int mode, int key_bytes, int p, int digit_bits, void* const* keys, const uint32_t* const* vals,
-                           size_t N, void* const* out_keys, uint32_t* const* out_vals, void* ws, size_t ws_bytes,
-                           void* stream) {
-    if ((mode != 4 && mode != 5) || p < 1 || !keys || !out_keys || (key_bytes != 4 && key_bytes != 8) ||
-        (digit_bits != 8 && digit_bits != 16))
-        return rs::fail(RS_EINVAL, "bad BTN/OET emulate arguments");
-    if (mode == 4 && (p & (p - 1))) return rs::fail(RS_EINVAL, "BTN needs p a power of two");
-    if (N >= (1ull << 32)) return rs::fail(RS_EINVAL, "N >= 2^32");
-    for (int k = 0; k < p; ++k)
-        if (N && (!keys[k] || !out_keys[k] || (vals && (!vals[k] || !out_vals[k]))))
-            return rs::fail(RS_EINVAL, "NULL block");
-    return rs::net_emulate(mode, key_bytes, p, digit_bits, keys, vals, N, out_keys, out_vals, ws, ws_bytes,
-                           static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

@@ -133,84 +133,57 @@ size_t pr_ws_bytes(int key_bytes, bool hv, size_t n_local_max, int p) {
     return pr_layout(nullptr, key_bytes, hv, n_local_max, p).bytes;
 }
 
-#define RS_NCCL_TRY2(expr)                                                                    \
-    do {                                                                                      \
-        ncclResult_t r_ = (expr);                                                             \
-        if (r_ != ncclSuccess)                                                                \
-            return fail(RS_ENCCL, std::string(#expr) + ": " + ncclGetErrorString(r_));        \
-    } while (0)
-
 // the multi-GPU call (Comm::sampling = 3): header / validation exchanged by the
 // caller (gsd_sort), sizes n_all (per rank) known; every rank must be able to map
-// every peer's S block (checked collectively, else RS_ECUDA on every rank)
+// every peer's S block (agreed collectively, else RS_ECUDA on every rank)
 rs_status_t pr_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t n, void* out, uint32_t* vout,
                     size_t* n_out, void* ws, const std::vector<uint64_t>& n_all, cudaStream_t st) {
     const int p = c->nranks, rank = c->rank;
     const bool hv = vals != nullptr;
     const PrLayout L = pr_layout(ws, key_bytes, hv, n, p);
     const int P = key_bytes;  // radix-256 rounds
-    uint64_t* h = c->h_pinned;
     // map the peers' S blocks once per call
-    std::memset(h, 0, kIpcWords * 8);
-    bool ok = ipc_export(L.s_keys, h, &h[8]) == RS_OK;
-    if (ok && hv) ok = ipc_export(L.s_vals, &h[9], &h[17]) == RS_OK;
-    h[18] = ok ? 1 : 0;
-    RS_CUDA_TRY(cudaMemcpyAsync(c->d_ipc, h, kIpcWords * 8, cudaMemcpyHostToDevice, st));
-    RS_NCCL_TRY2(ncclAllGather(c->d_ipc, c->d_ipc + kIpcWords, kIpcWords, ncclUint64, c->nccl, st));
-    RS_CUDA_TRY(cudaMemcpyAsync(h, c->d_ipc + kIpcWords, (size_t)p * kIpcWords * 8, cudaMemcpyDeviceToHost, st));
-    RS_CUDA_TRY(cudaStreamSynchronize(st));
+    const void* mine[2] = {L.s_keys, L.s_vals};
+    const int nb = hv ? 2 : 1;
+    std::vector<void*> peers;
+    rs_status_t s = map_peer_buffers(c, mine, nb, &peers, st);
+    if (s != RS_OK) return s;
     std::vector<const void*> sk(p);
     std::vector<const uint32_t*> sv(hv ? p : 0);
-    bool all_ok = true;
     for (int k = 0; k < p; ++k) {
-        const uint64_t* rec = h + (size_t)k * kIpcWords;
-        if (rec[18] != 1) all_ok = false;
+        sk[k] = peers[(size_t)k * nb];
+        if (hv) sv[k] = static_cast<const uint32_t*>(peers[(size_t)k * nb + 1]);
     }
-    if (all_ok)
-        for (int k = 0; k < p && all_ok; ++k) {
-            const uint64_t* rec = h + (size_t)k * kIpcWords;
-            void* kb = L.s_keys;
-            void* vb = L.s_vals;
-            if (k != rank) {
-                all_ok = ipc_open(rec, rec[8], &kb) == RS_OK;
-                if (all_ok && hv) all_ok = ipc_open(&rec[9], rec[17], &vb) == RS_OK;
-            }
-            sk[k] = kb;
-            if (hv) sv[k] = static_cast<const uint32_t*>(vb);
-        }
-    h[0] = all_ok ? 0 : 1;
-    RS_CUDA_TRY(cudaMemcpyAsync(c->d_ipc, h, 8, cudaMemcpyHostToDevice, st));
-    RS_NCCL_TRY2(ncclAllReduce(c->d_ipc, c->d_ipc, 1, ncclUint64, ncclMax, c->nccl, st));
-    RS_CUDA_TRY(cudaMemcpyAsync(h, c->d_ipc, 8, cudaMemcpyDeviceToHost, st));
-    RS_CUDA_TRY(cudaStreamSynchronize(st));
-    if (h[0]) return fail(RS_ECUDA, "PR4 across GPUs needs every rank to map every peer's block (CUDA IPC)");
-
+    uint64_t* h_hist = c->h + comm_hin_offset();           // p·256 u32 counts
+    Piece* h_pieces = reinterpret_cast<Piece*>(h_hist + (size_t)p * 128);  // staged piece list
     void* A = keys;
     uint32_t* Av = vals;
     void* B = L.b_keys;
     uint32_t* Bv = L.b_vals;
     std::vector<uint64_t> cnt((size_t)p * 256);
-    for (int t = 0; t < P; ++t) {
-        rs_status_t s = local_sort_digit(key_bytes, A, Av, n, t, L.s_keys, L.s_vals, L.local_ws, st, L.hist_local);
-        if (s != RS_OK) return s;
+    for (int t = 0; t < P && s == RS_OK; ++t) {
+        if ((s = local_sort_digit(key_bytes, A, Av, n, t, L.s_keys, L.s_vals, L.local_ws, st, L.hist_local)) != RS_OK)
+            break;
         // the counter exchange; it also orders every rank's S before any pull
-        RS_NCCL_TRY2(ncclAllGather(L.hist_local, L.hist_all, 256, ncclUint32, c->nccl, st));
-        RS_CUDA_TRY(cudaMemcpyAsync(h, L.hist_all, (size_t)p * 256 * 4, cudaMemcpyDeviceToHost, st));
-        RS_CUDA_TRY(cudaStreamSynchronize(st));
-        const uint32_t* h32 = reinterpret_cast<const uint32_t*>(h);
+        if ((s = c->tr->allgather(L.hist_local, L.hist_all, 256 * 4, st)) != RS_OK) break;
+        RS_CUDA_TRY(cudaMemcpyAsync(h_hist, L.hist_all, (size_t)p * 256 * 4, cudaMemcpyDeviceToHost, st));
+        // (this wait also retires the previous round's pull, so the staged piece list is free)
+        if ((s = c->wait(st)) != RS_OK) break;
+        const uint32_t* h32 = reinterpret_cast<const uint32_t*>(h_hist);
         for (size_t i = 0; i < cnt.size(); ++i) cnt[i] = h32[i];
         const std::vector<Piece> pcs = plan_pieces(p, rank, cnt, n_all, sk, sv, key_bytes);
         if (!pcs.empty()) {
-            std::memcpy(h, pcs.data(), pcs.size() * sizeof(Piece));  // pinned, host-synced below
-            RS_CUDA_TRY(cudaMemcpyAsync(L.pieces, h, pcs.size() * sizeof(Piece), cudaMemcpyHostToDevice, st));
+            std::memcpy(h_pieces, pcs.data(), pcs.size() * sizeof(Piece));
+            RS_CUDA_TRY(cudaMemcpyAsync(L.pieces, h_pieces, pcs.size() * sizeof(Piece), cudaMemcpyHostToDevice, st));
         }
-        if ((s = launch_pull(key_bytes, L.pieces, (int)pcs.size(), n, B, Bv, st)) != RS_OK) return s;
+        if ((s = launch_pull(key_bytes, L.pieces, (int)pcs.size(), n, B, Bv, st)) != RS_OK) break;
         // nobody rewrites its S (next round) before every peer has pulled from it
-        RS_NCCL_TRY2(ncclAllReduce(c->d_ipc, c->d_ipc, 1, ncclUint64, ncclMax, c->nccl, st));
-        RS_CUDA_TRY(cudaStreamSynchronize(st));  // the pinned piece list is reused next round
+        if ((s = c->tr->barrier(st)) != RS_OK) break;
         std::swap(A, B);
         std::swap(Av, Bv);
     }
+    c->tr->release_unused();
+    if (s != RS_OK) return s;
     if (A != out && n) {
         RS_CUDA_TRY(cudaMemcpyAsync(out, A, n * key_bytes, cudaMemcpyDeviceToDevice, st));
         if (hv) RS_CUDA_TRY(cudaMemcpyAsync(vout, Av, n * 4, cudaMemcpyDeviceToDevice, st));
@@ -220,88 +193,4 @@ rs_status_t pr_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t n
     return RS_OK;
 }
 
-// all p ranks on this GPU: blocks[k] (scratch, n[k] keys each) -> out[j] (n[j] keys)
-rs_status_t pr_emulate(int key_bytes, int p, void* const* keys, uint32_t* const* vals, const size_t* n,
-                       void* const* out_keys, uint32_t* const* out_vals, void* ws, size_t ws_bytes, cudaStream_t st) {
-    const bool hv = vals != nullptr;
-    size_t n_max = 0;
-    std::vector<uint64_t> n_all(p);
-    for (int k = 0; k < p; ++k) {
-        n_max = std::max(n_max, n[k]);
-        n_all[k] = n[k];
-    }
-    const size_t per = pr_layout(nullptr, key_bytes, hv, n_max, p).bytes;
-    if (!ws || ws_bytes < per * (size_t)p) return fail(RS_EINVAL, "PR emulate workspace too small: need " +
-                                                                      std::to_string(per * p));
-    std::vector<PrLayout> L(p);
-    for (int k = 0; k < p; ++k) L[k] = pr_layout(static_cast<char*>(ws) + per * k, key_bytes, hv, n_max, p);
-    std::vector<void*> A(keys, keys + p), B(p);
-    std::vector<uint32_t*> Av(p, nullptr), Bv(p, nullptr);
-    for (int k = 0; k < p; ++k) {
-        B[k] = L[k].b_keys;
-        if (hv) {
-            Av[k] = vals[k];
-            Bv[k] = L[k].b_vals;
-        }
-    }
-    std::vector<const void*> sk(p);
-    std::vector<const uint32_t*> sv(hv ? p : 0);
-    for (int k = 0; k < p; ++k) {
-        sk[k] = L[k].s_keys;
-        if (hv) sv[k] = L[k].s_vals;
-    }
-    std::vector<uint64_t> cnt((size_t)p * 256);
-    std::vector<uint32_t> h32((size_t)p * 256);
-    for (int t = 0; t < key_bytes; ++t) {
-        for (int k = 0; k < p; ++k) {
-            rs_status_t s = local_sort_digit(key_bytes, A[k], Av[k], n[k], t, L[k].s_keys, L[k].s_vals, L[k].local_ws,
-                                             st, L[0].hist_all + (size_t)k * 256);
-            if (s != RS_OK) return s;
-        }
-        RS_CUDA_TRY(cudaMemcpyAsync(h32.data(), L[0].hist_all, h32.size() * 4, cudaMemcpyDeviceToHost, st));
-        RS_CUDA_TRY(cudaStreamSynchronize(st));
-        for (size_t i = 0; i < cnt.size(); ++i) cnt[i] = h32[i];
-        for (int j = 0; j < p; ++j) {
-            const std::vector<Piece> pcs = plan_pieces(p, j, cnt, n_all, sk, sv, key_bytes);
-            if (!pcs.empty())
-                RS_CUDA_TRY(cudaMemcpyAsync(L[j].pieces, pcs.data(), pcs.size() * sizeof(Piece),
-                                            cudaMemcpyHostToDevice, st));
-            rs_status_t s = launch_pull(key_bytes, L[j].pieces, (int)pcs.size(), n[j], B[j], Bv[j], st);
-            if (s != RS_OK) return s;
-            RS_CUDA_TRY(cudaStreamSynchronize(st));  // pcs (pageable) and the shared S blocks
-        }
-        std::swap(A, B);
-        std::swap(Av, Bv);
-    }
-    for (int j = 0; j < p; ++j)
-        if (n[j]) {
-            RS_CUDA_TRY(cudaMemcpyAsync(out_keys[j], A[j], n[j] * key_bytes, cudaMemcpyDeviceToDevice, st));
-            if (hv) RS_CUDA_TRY(cudaMemcpyAsync(out_vals[j], Av[j], n[j] * 4, cudaMemcpyDeviceToDevice, st));
-        }
-    RS_CUDA_TRY(cudaGetLastError());
-    return RS_OK;
-}
-
 }  // namespace rs
-
-extern "C" {
-
-size_t rs_pr_emulate_ws_bytes(int key_bytes, int val_bytes, int p, size_t n_max) {
-    if (p < 1 || (key_bytes != 4 && key_bytes != 8)) return 0;
-    return rs::pr_ws_bytes(key_bytes, val_bytes != 0, n_max, p) * (size_t)p;
-}
-
-rs_status_t rs_pr_emulate(int key_bytes, int p, void* const* keys, uint32_t* const* vals, const size_t* n,
-                          void* const* out_keys, uint32_t* const* out_vals, void* ws, size_t ws_bytes, void* stream) {
-    if (p < 1 || !keys || !n || !out_keys || (key_bytes != 4 && key_bytes != 8))
-        return rs::fail(RS_EINVAL, "bad PR emulate arguments");
-    for (int k = 0; k < p; ++k) {
-        if (n[k] >= (1ull << 32)) return rs::fail(RS_EINVAL, "n >= 2^32");
-        if (n[k] && (!keys[k] || !out_keys[k] || (vals && (!vals[k] || !out_vals[k]))))
-            return rs::fail(RS_EINVAL, "NULL block");
-    }
-    return rs::pr_emulate(key_bytes, p, keys, vals, n, out_keys, out_vals, ws, ws_bytes,
-                          static_cast<cudaStream_t>(stream));
-}
-
-}  // extern "C"

@@ -329,11 +329,10 @@ rs_status_t pway(const PwRuns& R, uint64_t M, void* scratch, K* out, uint32_t* v
     }
     const int cap = pw_cap_padded(p, R.c);
     const size_t smem = (size_t)cap * (2 * sizeof(K) + (V ? 8 : 0));
-    static bool attr = false;
-    if (!attr) {
-        RS_CUDA_TRY(cudaFuncSetAttribute(k_pw_merge<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)pw_cap_padded(kPwMaxP, kPwCMax) * (2 * (int)sizeof(K) + (V ? 8 : 0))));
-        attr = true;
+    {
+        rs_status_t s = kernel_setup(reinterpret_cast<const void*>(k_pw_merge<K, V>), kPwT,
+                                     (size_t)pw_cap_padded(kPwMaxP, kPwCMax) * (2 * sizeof(K) + (V ? 8 : 0)), nullptr);
+        if (s != RS_OK) return s;
     }
     {
         LaunchScope ls("pw_merge", st);

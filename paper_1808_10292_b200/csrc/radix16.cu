@@ -419,13 +419,12 @@ static rs_status_t sort16(const K* in, const uint32_t* vin, size_t n, int end_bi
     const Layout16 L = layout16(ws, sizeof(K), V, n);
     const int P = (end_bit + 15) / 16;
     using S = Scatter16Smem<K, V>;
-    static bool attr = false;
-    if (!attr) {
-        RS_CUDA_TRY(cudaFuncSetAttribute(k16_count<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, kR16 / 2 * 4));
-        RS_CUDA_TRY(cudaFuncSetAttribute(k16_scatter<K, V>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes));
-        RS_CUDA_TRY(cudaFuncSetAttribute(k16_scatter_fast, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)Scatter16FastSmem::bytes));
-        attr = true;
+    {
+        rs_status_t s = kernel_setup(reinterpret_cast<const void*>(k16_count<K>), kC16Threads, kR16 / 2 * 4, nullptr);
+        if (s == RS_OK) s = kernel_setup(reinterpret_cast<const void*>(k16_scatter<K, V>), kS16Threads, S::bytes, nullptr);
+        if (s == RS_OK)
+            s = kernel_setup(reinterpret_cast<const void*>(k16_scatter_fast), kS16Threads, Scatter16FastSmem::bytes, nullptr);
+        if (s != RS_OK) return s;
     }
     K* alt = static_cast<K*>(L.alt_keys);
     // static ping-pong: the last pass writes `out`; an in-place odd count ends in alt + copy

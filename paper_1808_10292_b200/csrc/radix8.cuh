@@ -1,13 +1,13 @@
 // Radix-256 LSD pass machinery (the paper's PR4/SR4 count-sort round,
 // PAPER.md:653-709) re-designed for sm_100a as a single-sweep pass:
 //
-//   K1 k_digit_hist   one HBM read of all keys -> every pass's 256-bin histogram
+//   K1 k_digit_hist_lp one HBM read of all keys -> every pass's 256-bin histogram
 //                     ("initial counting process", all rounds at once)
 //   K2 k_plan         exclusive prefix of the histograms -> bucket bases per pass
 //                     and portion, plus the ping-pong plan
 //                     (which passes are non-trivial, src/dst of each)
-//   K3 k_onesweep     one stable count-sort round: TMA bulk
-//                     tile load -> in-tile stable rank with warp match ->
+//   K3 k_onesweep_ar  one stable count-sort round: tile
+//                     loads -> in-tile stable rank by shared atomics ->
 //                     decoupled look-back across tiles for the per-digit tile
 //                     offsets (the single-GPU form of PR's p×r counter matrix,
 //                     PAPER.md:690-694) -> shared-memory reorder ->
@@ -52,54 +52,7 @@ struct Ctrl {
 };
 
 // ------------------------------------------------------------------ K1 ----
-// hist[t][d] for pass t < P.
-// Shared-memory histograms, one copy per group of 4 warps, merged into global
-// with one atomicAdd per nonzero bin per CTA.  Also zeroes `zero_words` words
-// at `zero_ptr` (the look-back status region of the first pass).
-template <typename K, int THREADS>
-__global__ void __launch_bounds__(THREADS) k_digit_hist(const K* __restrict__ keys, size_t n, int P, int b,
-                                                       uint32_t* __restrict__ hist,
-                                                       uint32_t* __restrict__ zero_ptr,
-                                                       size_t zero_words) {
-    constexpr int COPIES = THREADS / 128;  // one histogram copy per 4 warps
-    const int R = 1 << b;                  // b == 8 here
-    extern __shared__ __align__(16) uint32_t s_hist[];  // [COPIES][P][256]
-    const int tid = threadIdx.x;
-    const size_t gtid = (size_t)blockIdx.x * THREADS + tid;
-    const size_t gstride = (size_t)gridDim.x * THREADS;
-
-    for (size_t i = gtid; i < zero_words; i += gstride) zero_ptr[i] = 0;
-
-    uint32_t* my = s_hist + (tid / 128) * P * 256;
-    const uint32_t mask = (uint32_t)R - 1;
-    for (int i = tid; i < COPIES * P * 256; i += THREADS) s_hist[i] = 0;
-    __syncthreads();
-    constexpr int VEC = 16 / sizeof(K);
-    const size_t nvec = n / VEC;
-    const uint4* vbase = reinterpret_cast<const uint4*>(keys);
-    for (size_t v = gtid; v < nvec; v += gstride) {
-        uint4 x = __ldg(vbase + v);
-        const K* ks = reinterpret_cast<const K*>(&x);
-#pragma unroll
-        for (int e = 0; e < VEC; ++e) {
-            K k = ks[e];
-            for (int t = 0; t < P; ++t) atomicAdd(&my[t * 256 + digit_of<K>(k, t * b, mask)], 1u);
-        }
-    }
-    for (size_t i = nvec * VEC + gtid; i < n; i += gstride) {
-        K k = keys[i];
-        for (int t = 0; t < P; ++t) atomicAdd(&my[t * 256 + digit_of<K>(k, t * b, mask)], 1u);
-    }
-    __syncthreads();
-    for (int i = tid; i < P * 256; i += THREADS) {
-        uint32_t s = 0;
-#pragma unroll
-        for (int c = 0; c < COPIES; ++c) s += s_hist[c * P * 256 + i];
-        if (s) atomicAdd(&hist[i], s);
-    }
-}
-
-// K1, lane-private layout (default): the CTA keeps C copies of every pass's
+// K1, lane-private layout: the CTA keeps C copies of every pass's
 // histogram and lane l adds to copy l % C, with copy c of digit d at word
 // d*C + c, so the 32 lanes of an atomic touch 32/C words per bank at most:
 // C = 32 (u32 keys, 4 passes: 128 KB) makes every warp-wide atomic a single
@@ -246,7 +199,6 @@ struct PassArgs {
     const uint32_t* bases;  // [P][256]
     void* status_cur;       // [T][256] status words, zero on entry
     void* status_next;      // [T][256], cleared here for the next pass
-    uint32_t debug_skip;    // timing ablations only (rs_set_option "debug_skip"); 0 in normal use
 };
 
 // ------------------------------------------------------------------ K4 ----

@@ -1,4 +1,6 @@
 // Host runtime: error strings, launch counting / event timing, device queries.
+#include <algorithm>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -61,6 +63,25 @@ void timing_after(int slot, cudaStream_t stream) {
 Options& options() {
     static Options o;
     return o;
+}
+
+static std::mutex g_kmu;
+static std::map<std::pair<const void*, int>, int> g_kgrid;  // (kernel, device) -> persistent grid
+
+rs_status_t kernel_setup(const void* kern, int threads, size_t smem, int* grid_cap) {
+    int dev = 0;
+    RS_CUDA_TRY(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_kmu);
+    auto it = g_kgrid.find({kern, dev});
+    if (it == g_kgrid.end()) {
+        RS_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        int per_sm = 0, sms = 0;
+        RS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem));
+        RS_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        it = g_kgrid.emplace(std::make_pair(kern, dev), std::max(1, per_sm) * std::max(1, sms)).first;
+    }
+    if (grid_cap) *grid_cap = it->second;
+    return RS_OK;
 }
 
 int sm_count() {
@@ -129,45 +150,35 @@ rs_status_t rs_timing_query(const char* prefix, double* total_ms, int* launches)
 
 long long rs_launch_count(void) { return g_launches.load(); }
 
-rs_status_t rs_set_option(const char* name, long long value) {
-    if (!name || value < 0) return fail(RS_EINVAL, "rs_set_option: bad name / negative value");
+rs_status_t rs_dev_set_option(const char* name, long long value) {
+    if (!name || value < 0) return fail(RS_EINVAL, "rs_dev_set_option: bad name / negative value");
     const std::string n(name);
-    if (n == "wide_status" && value <= 1) options().wide_status = value != 0;
-    else if (n == "debug_skip" && value <= 31) options().debug_skip = (unsigned)value;
-    else if (n == "gsd_merge" && value <= 3) options().gsd_merge = (int)value;
-    else if (n == "compact" && value <= 1) options().compact = value != 0;
-    else if (n == "hist_shared" && value <= 1) options().hist_shared = value != 0;
-    else if (n == "small_tiles" && value <= 2) options().small_tiles = (int)value;
-    else if (n == "small_fused" && value <= 1) options().small_fused = (int)value;
-    else if (n == "gsd_pull" && value <= 1) options().gsd_pull = (int)value;
-    else if (n == "match_every" && (value == 0 || value == 4 || value == 6 || value == 8))
-        options().match_every = (int)value;
-    else if (n == "pass_design" && value <= 6) options().pass_design = (int)value;
-    else if (n == "rank_variant" && value <= 4) options().rank_variant = (int)value;
-    else return fail(RS_EINVAL, "rs_set_option: unknown option or value: " + n);
+    Options& o = options();
+    if (n == "wide_status" && value <= 1) o.wide_status = (int)value;
+    else if (n == "gsd_merge" && value <= 3) o.gsd_merge = (int)value;
+    else if (n == "gsd_pull" && value <= 1) o.gsd_pull = (int)value;
+    else if (n == "small_tiles" && value <= 2) o.small_tiles = (int)value;
+    else if (n == "pass_design" && (value == 2 || value == 5)) o.pass_design = (int)value;
+    else if (n == "self_check" && value <= 1) o.self_check = (int)value;
+    else return fail(RS_EINVAL, "rs_dev_set_option: unknown option or value: " + n);
     return RS_OK;
 }
 
-rs_status_t rs_get_option(const char* name, long long* value) {
-    if (!name || !value) return fail(RS_EINVAL, "rs_get_option: null argument");
+rs_status_t rs_dev_get_option(const char* name, long long* value) {
+    if (!name || !value) return fail(RS_EINVAL, "rs_dev_get_option: null argument");
     const std::string n(name);
     const Options& o = options();
     if (n == "wide_status") *value = o.wide_status;
-    else if (n == "debug_skip") *value = o.debug_skip;
     else if (n == "gsd_merge") *value = o.gsd_merge;
-    else if (n == "compact") *value = o.compact;
-    else if (n == "hist_shared") *value = o.hist_shared;
-    else if (n == "small_tiles") *value = o.small_tiles;
-    else if (n == "small_fused") *value = o.small_fused;
     else if (n == "gsd_pull") *value = o.gsd_pull;
-    else if (n == "match_every") *value = o.match_every;
+    else if (n == "small_tiles") *value = o.small_tiles;
     else if (n == "pass_design") *value = o.pass_design;
-    else if (n == "rank_variant") *value = o.rank_variant;
+    else if (n == "self_check") *value = o.self_check;
     else if (n == "rank_probe") *value = rank_probe_state();
     else if (n == "tile_u32") *value = tile_keys_for(4, false);
     else if (n == "tile_u64") *value = tile_keys_for(8, false);
     else if (n == "tile_pairs") *value = tile_keys_for(8, true);
-    else return fail(RS_EINVAL, "rs_get_option: unknown option: " + n);
+    else return fail(RS_EINVAL, "rs_dev_get_option: unknown option: " + n);
     return RS_OK;
 }
 

@@ -3,11 +3,13 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <string>
 
 #include "../../include/rsort.h"
+#include "../../include/rsort_dev.h"
 
 namespace rs {
 
@@ -35,26 +37,20 @@ struct LaunchScope {
 
 int sm_count();
 
-// process-wide tuning / test knobs (rs_set_option)
+// process-wide test / tuning knobs (include/rsort_dev.h rs_dev_set_option); read
+// once per call, written only between calls
 struct Options {
-    bool wide_status = false;     // force 64-bit look-back status words (tests)
-    unsigned debug_skip = 0;      // timing ablations (invalid output): 1 look-back, 2 rank, 4 store, 8 reorder
-    int rank_variant = 3;         // 0 ballot peers, 1 match.any, 2 atomic-OR peers, 3 hybrid pairs
-    int gsd_merge = 3;            // GSD step 5: 0 merge tree, 1 stable radix re-sort, 2 pull merge (tree),
-                                  // 3 pull merge as one p-way pass (pwmerge.cu; tree when p > 32)
-    int gsd_pull = 1;             // 0: exchange by all-to-all even with gsd_merge 2/3 (tests the fallback)
-                                  // (the tree reads the source blocks in place: peers over NVLink)
-    bool compact = false;         // design 2: 16-bit per-warp counters, ballots only (4 CTAs/SM)
-    int match_every = 0;          // design 2, u32 keys: every k-th key ranked by match.any (0 = none)
-    bool hist_shared = false;     // K1: 1 = one histogram copy per 4 warps (previous default)
-    int small_tiles = 0;          // design 5 small-input tiles: 0 auto (< 2 large tiles per SM), 1 never, 2 always
-    int small_fused = 0;          // 1: small-tile full sorts as one cooperative launch (onesweep_fused.cuh);
-                                  // measured no faster (2^20: 70.8 vs 73.4 us direct, 69 vs 55 us as a graph)
-    int pass_design = 5;          // 5 atomic ranks (if the lane-order probe passes, else 2);
-                                  // 0 classic single sweep; early counts + prefetch with 1 a look-back
-                                  // warp, 2 look-back after ranking; 3 counter-ranked nibble sub-passes;
-                                  // 4 register nibble counters
+    std::atomic<int> wide_status{0};   // force 64-bit look-back status words (tests)
+    std::atomic<int> gsd_merge{3};     // GSD step 5: 0 all-to-all + merge tree, 1 all-to-all + stable radix
+                                       // re-sort, 2 pull merge (tree), 3 pull merge as one p-way pass
+    std::atomic<int> gsd_pull{1};      // 0: exchange by all-to-all even with gsd_merge 2/3 (the fallback)
+    std::atomic<int> small_tiles{0};   // design 5 small-input tiles: 0 auto, 1 never, 2 always
+    std::atomic<int> pass_design{5};   // 5 atomic ranks (if the lane-order probe passes, else 2); 2 ballots
+    std::atomic<int> self_check{0};    // 1: verify every local sort's output on the device (debug)
 };
+// per (kernel, device): set the kernel's dynamic shared-memory limit to `smem` once
+// and return its persistent grid (resident CTAs per SM at `threads` x SMs)
+rs_status_t kernel_setup(const void* kern, int threads, size_t smem, int* grid_cap);
 // design 5 precondition (radix.cu): -1 not probed yet on this device, 0 failed, 1 passed
 int rank_probe_state();
 // CUDA IPC mappings (ipc.cu)

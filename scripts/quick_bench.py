@@ -15,9 +15,9 @@ import paper_1808_10292_b200 as rs  # noqa: E402
 L = rs.lib()
 PEAK = 6545.6
 ONE_PASS = os.environ.get("RS_ONE_PASS") == "1"
-for _opt in ("rank_variant", "debug_skip", "wide_status", "pass_design", "match_every", "compact", "hist_shared", "small_tiles", "small_fused"):
+for _opt in ("wide_status", "pass_design", "small_tiles"):
     if os.environ.get("RS_" + _opt.upper()):
-        L.rs_set_option(_opt.encode(), int(os.environ["RS_" + _opt.upper()]))
+        L.rs_dev_set_option(_opt.encode(), int(os.environ["RS_" + _opt.upper()]))
 
 
 def q(prefix):

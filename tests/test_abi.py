@@ -1,6 +1,6 @@
 """C-ABI boundary checks that need no GPU: librsort.so loads, exports every
-symbol include/rsort.h declares (and nothing else), and rejects bad arguments
-before touching the device."""
+symbol include/rsort.h and include/rsort_dev.h declare (and nothing else), and
+rejects bad arguments before touching the device."""
 import ctypes
 import subprocess
 
@@ -20,7 +20,7 @@ def L():
 
 def test_exports_every_declared_symbol(L):
     declared = _abi.header_symbols()
-    assert len(declared) >= 20
+    assert len(declared) >= 30
     for name in declared:
         assert hasattr(L, name), name
         assert name in _abi.SIGNATURES, f"binding lacks {name}"
@@ -82,14 +82,43 @@ def test_comm_argument_validation(L):
     assert L.rs_comm_set_oversampling(None, 8) == RS_EINVAL
 
 
-def test_emulate_validation(L):
-    assert L.rs_gsd_emulate_ws_bytes(4, 0, 4, 8, 8, 1000, 1200) > 0
-    assert L.rs_gsd_emulate_ws_bytes(4, 0, 0, 8, 8, 1000, 1200) == 0
-    n_out = (ctypes.c_size_t * 2)()
-    n = (ctypes.c_size_t * 2)(10, 10)
-    arr = (ctypes.c_void_p * 2)(0x10000, 0x10000)
-    assert L.rs_gsd_emulate(4, 2, 8, 12, arr, None, n, arr, None, 100, n_out, None, None, 0x10000, 1 << 30,
-                            None) == RS_EINVAL
+def test_product_header_is_the_scope_table(L):
+    """include/rsort.h carries exactly SURVEY §8(b)'s calls and the comm helpers;
+    test / tuning surface lives in include/rsort_dev.h."""
+    prod = set(_abi.header_symbols("rsort.h"))
+    assert prod == {"rs_status_string", "rs_last_error", "rs_version", "rs_workspace_bytes", "rs_output_capacity",
+                    "rs_sort_u32", "rs_sort_u64", "rs_sort_pairs_u64_u32", "rs_sort_bits", "rs_digit_histogram",
+                    "rs_get_unique_id", "rs_comm_create", "rs_comm_destroy", "rs_comm_set_oversampling",
+                    "rs_comm_set_sampling", "rs_comm_rank", "rs_comm_size"}
+    dev = set(_abi.header_symbols("rsort_dev.h"))
+    assert not prod & dev
+    assert {"rs_local_group_create", "rs_comm_create_local", "rs_dev_set_option", "rs_ipc_open"} <= dev
+
+
+def test_local_group_validation(L):
+    g = ctypes.c_void_p()
+    assert L.rs_local_group_create(0, ctypes.byref(g)) == RS_EINVAL
+    assert L.rs_local_group_create(65, ctypes.byref(g)) == RS_EINVAL
+    assert L.rs_local_group_create(2, None) == RS_EINVAL
+    assert L.rs_local_group_create(2, ctypes.byref(g)) == RS_OK
+    c = ctypes.c_void_p()
+    assert L.rs_comm_create_local(g, 2, ctypes.byref(c)) == RS_EINVAL      # rank out of range
+    assert L.rs_comm_create_local(g, -1, ctypes.byref(c)) == RS_EINVAL
+    assert L.rs_comm_create_local(None, 0, ctypes.byref(c)) == RS_EINVAL
+    assert L.rs_local_group_destroy(g) == RS_OK
+    assert L.rs_comm_last_host_syncs(None) == -1
+    assert L.rs_comm_set_timeout(None, 10) == RS_EINVAL
+
+
+def test_dev_options_validation(L):
+    v = ctypes.c_longlong()
+    assert L.rs_dev_get_option(b"pass_design", ctypes.byref(v)) == RS_OK and v.value == 5
+    assert L.rs_dev_set_option(b"pass_design", 3) == RS_EINVAL               # designs 5 and 2 only
+    assert L.rs_dev_set_option(b"rank_variant", 1) == RS_EINVAL              # removed knobs
+    assert L.rs_dev_set_option(b"gsd_merge", 4) == RS_EINVAL
+    assert L.rs_dev_set_option(b"self_check", 1) == RS_OK
+    assert L.rs_dev_set_option(b"self_check", 0) == RS_OK
+    assert L.rs_dev_get_option(b"nope", ctypes.byref(v)) == RS_EINVAL
 
 
 def test_net_host_logic(L):
@@ -99,12 +128,9 @@ def test_net_host_logic(L):
         assert L.rs_net_stages(4, 1 << m) == m * (m + 1) // 2
     assert L.rs_net_stages(4, 12) == -1 and L.rs_net_stages(6, 4) == -1
     assert [L.rs_net_stages(5, p) for p in (1, 2, 9)] == [1, 2, 9]
-    assert L.rs_net_emulate_ws_bytes(4, 0, 4, 8, 1000) > 0
-    assert L.rs_net_emulate_ws_bytes(4, 0, 4, 12, 1000) == 0
-    arr = (ctypes.c_void_p * 3)(0x10000, 0x10000, 0x10000)
-    assert L.rs_net_emulate(4, 4, 3, 8, arr, None, 10, arr, None, 0x10000, 1 << 30, None) == RS_EINVAL  # p=3
-    assert L.rs_net_emulate(5, 4, 3, 12, arr, None, 10, arr, None, 0x10000, 1 << 30, None) == RS_EINVAL
-    assert L.rs_net_emulate(5, 4, 3, 8, arr, None, 1 << 32, arr, None, 0x10000, 1 << 30, None) == RS_EINVAL
+    q, kl = ctypes.c_int(), ctypes.c_int()
+    assert L.rs_net_schedule(4, 3, 0, 0, ctypes.byref(q), ctypes.byref(kl)) == -1   # BTN needs a power of 2
+    assert L.rs_net_schedule(5, 3, 0, 3, ctypes.byref(q), ctypes.byref(kl)) == -1   # rank out of range
 
 
 def test_timing_api_without_gpu(L):

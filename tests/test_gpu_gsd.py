@@ -1,9 +1,10 @@
-"""GPU parity of the GSD kernels and host plan (rs_gsd_emulate: every rank's
-steps on this GPU, device copies in place of NCCL) against the CPU GSD
-simulator (oracle/gsd.c): splitters, the p×p count matrix
-and every Y_j bit-exact."""
-import ctypes
-
+"""GPU parity of the collective sort itself — rs_sort_u32 / rs_sort_u64 /
+rs_sort_pairs_u64_u32 with a comm, one call per rank, the ranks being p threads
+on this GPU (LocalGroup, include/rsort_dev.h: the multi-GPU orchestration over
+the in-process transport) — against the CPU simulators (oracle/gsd.c,
+PAPER.md:775-805 GSD, 965-986 GER, 988-1016 GVR, 685-709 PR4): splitters, the
+p×p count matrix and every Y_j bit-exact, on the pull merge and on the
+all-to-all fallback; errors come back identically on every rank."""
 import numpy as np
 import pytest
 
@@ -19,8 +20,8 @@ def _check(blocks_np, r, b, vals_np=None):
     p = len(blocks_np)
     dt = blocks_np[0].dtype
     want = oracle.gsd(blocks_np, r=r, b=b, vals=vals_np)
-    got = rs.gsd_emulate([dev(x) for x in blocks_np], r=r, digit_bits=b,
-                         vals=[dev(v) for v in vals_np] if vals_np is not None else None)
+    got = rs.sort_ranks([dev(x) for x in blocks_np], "gsd", r=r, digit_bits=b,
+                        vals=[dev(v) for v in vals_np] if vals_np is not None else None)
     assert got["counts"].tolist() == want["counts"].tolist()
     assert got["splitters"].tolist() == want["splitters"].tolist()
     for j in range(p):
@@ -30,6 +31,7 @@ def _check(blocks_np, r, b, vals_np=None):
     nmax = max(x.size for x in blocks_np)
     if min(x.size for x in blocks_np) >= r * p:
         assert max(got["n_out"]) <= nmax + nmax // r          # balance bound (R18)
+    assert got["host_syncs"] == [1] * p                       # one blocking wait per call, every rank
     return got
 
 
@@ -76,7 +78,7 @@ def test_gsd_config4_shape_reduced():
     a = inputs.gen_u32(n, 4)
     N = n // p
     blocks = [a[k * N:(k + 1) * N] for k in range(p)]
-    got = rs.gsd_emulate([dev(x) for x in blocks], r=8, digit_bits=8)
+    got = rs.sort_ranks([dev(x) for x in blocks], "gsd", r=8, digit_bits=8)
     Y = np.concatenate([host(y, np.uint32) for y in got["Y"]])
     assert (Y == oracle.sr(a, 8)).all()
     assert max(got["n_out"]) <= N + N // 8
@@ -87,13 +89,11 @@ def option():
     saved = {}
 
     def _set(name, value):
-        v = ctypes.c_longlong()
-        assert rs.lib().rs_get_option(name.encode(), ctypes.byref(v)) == 0
-        saved.setdefault(name, v.value)
-        assert rs.lib().rs_set_option(name.encode(), value) == 0
+        saved.setdefault(name, rs.get_option(name))
+        rs.set_option(name, value)
     yield _set
     for name, value in saved.items():
-        rs.lib().rs_set_option(name.encode(), value)
+        rs.set_option(name, value)
 
 
 @pytest.mark.parametrize("merge", [0, 1, 2, 3])
@@ -129,8 +129,8 @@ def _check_ger(blocks_np, s, seed, b=8, vals_np=None):
     dt = blocks_np[0].dtype
     want = oracle.ger(blocks_np, s=s if s else _default_s(sum(x.size for x in blocks_np)), seed=seed, b=b,
                       vals=vals_np)
-    got = rs.ger_emulate([dev(x) for x in blocks_np], s=s, seed=seed, digit_bits=b,
-                         vals=[dev(v) for v in vals_np] if vals_np is not None else None)
+    got = rs.sort_ranks([dev(x) for x in blocks_np], "ger", s=s, seed=seed, digit_bits=b,
+                        vals=[dev(v) for v in vals_np] if vals_np is not None else None)
     assert got["counts"].tolist() == want["counts"].tolist()
     assert got["splitters"].tolist() == want["splitters"].tolist()
     for j in range(p):
@@ -182,8 +182,8 @@ def _check_gvr(blocks_np, s, seed, b=8, vals_np=None):
     dt = blocks_np[0].dtype
     want = oracle.gvr(blocks_np, s=s if s else _default_s(sum(x.size for x in blocks_np)), seed=seed, b=b,
                       vals=vals_np)
-    got = rs.gvr_emulate([dev(x) for x in blocks_np], s=s, seed=seed, digit_bits=b,
-                         vals=[dev(v) for v in vals_np] if vals_np is not None else None)
+    got = rs.sort_ranks([dev(x) for x in blocks_np], "gvr", s=s, seed=seed, digit_bits=b,
+                        vals=[dev(v) for v in vals_np] if vals_np is not None else None)
     assert got["counts"].tolist() == want["counts"].tolist()
     assert got["splitters"].tolist() == want["splitters"].tolist()
     for j in range(p):
@@ -285,14 +285,14 @@ def test_pway_merge_pairs_uneven_tiny_and_empty_blocks(option):
 @pytest.mark.parametrize("p", [1, 2, 3, 8])
 @pytest.mark.parametrize("dist", ["uniform", "mod16", "equal", "sorted"])
 def test_pr4_across_ranks_matches_the_sort(p, dist):
-    """PR4 routing (PAPER.md:685-709, SPEC.md:206 rank formula; rs_pr_emulate):
+    """PR4 routing (PAPER.md:685-709, SPEC.md:206 rank formula), rank by rank:
     after the four rounds rank j holds exactly positions [off_j, off_j + n_j) of
     the stable sorted order — the oracle's SR4 result sliced by the input sizes."""
     sizes = [7000 + 1311 * k for k in range(p)]
     a = inputs.gen_u32(sum(sizes), 150 + p, dist)
     cuts = np.concatenate([[0], np.cumsum(sizes)])
     blocks = [a[cuts[k]:cuts[k + 1]] for k in range(p)]
-    got = rs.pr_emulate([dev(x) for x in blocks])
+    got = rs.sort_ranks([dev(x) for x in blocks], "pr4")
     want = oracle.sr(a, 8)
     for j in range(p):
         assert (host(got["Y"][j], np.uint32) == want[cuts[j]:cuts[j + 1]]).all(), j
@@ -303,9 +303,116 @@ def test_pr4_pairs_stability_u64_uneven_and_empty_blocks():
     k = inputs.gen_u64(sum(sizes), 151, "mod1024")
     v = inputs.iota_u32(k.size)
     cuts = np.concatenate([[0], np.cumsum(sizes)])
-    got = rs.pr_emulate([dev(k[cuts[i]:cuts[i + 1]]) for i in range(5)],
+    got = rs.sort_ranks([dev(k[cuts[i]:cuts[i + 1]]) for i in range(5)], "pr4",
                         vals=[dev(v[cuts[i]:cuts[i + 1]]) for i in range(5)])
     wk, wv = oracle.sr(k, 8, vals=v)
     for j in range(5):
         assert (host(got["Y"][j], np.uint64) == wk[cuts[j]:cuts[j + 1]]).all(), j
         assert (host(got["Yv"][j], np.uint32) == wv[cuts[j]:cuts[j + 1]]).all(), j
+
+
+# ------------------------------------------------- collective error agreement ----
+def _statuses(p, fn):
+    """run fn(comm) on p in-process ranks; each rank's RSortError status (0 = ok)"""
+    g = rs.LocalGroup(p)
+
+    def body(c):
+        try:
+            fn(c)
+            return 0
+        except rs.RSortError as e:
+            return e.status
+    try:
+        return g.run(body, timeout_ms=60000)
+    finally:
+        g.close()
+
+
+def test_capacity_error_identical_on_every_rank():
+    """One rank's out_cap below its |Y_j| -> RS_ECAPACITY on EVERY rank (the
+    capacities travel with the headers; every rank checks every rank)."""
+    p, N = 4, 20000
+    a = inputs.gen_u32(p * N, 501)
+    blocks = [dev(a[k * N:(k + 1) * N]) for k in range(p)]
+
+    def fn(c):
+        cap = c.capacity(N)  # (collective: every rank takes part in the size agreement)
+        rs.sort(blocks[c.rank], comm=c, out_cap=N // 2 if c.rank == 2 else cap)
+    assert _statuses(p, fn) == [5] * p  # RS_ECAPACITY
+
+
+def test_header_mismatch_identical_on_every_rank():
+    """Rank 1 sorts u64 keys while the others sort u32: RS_EINVAL on every rank,
+    no hang (the header rides on the sample all-gather)."""
+    p, N = 3, 5000
+    a32 = inputs.gen_u32(p * N, 502)
+    a64 = inputs.gen_u64(N, 503)
+
+    def fn(c):
+        x = dev(a64) if c.rank == 1 else dev(a32[c.rank * N:(c.rank + 1) * N])
+        rs.sort(x, comm=c, out_cap=4 * N)
+    assert _statuses(p, fn) == [1] * p  # RS_EINVAL
+
+
+def test_local_argument_error_identical_on_every_rank():
+    """Rank 0 passes a workspace that is too small: it never touches its buffers,
+    takes part in both all-gathers with an empty block, and every rank returns
+    RS_EINVAL; then the same group sorts correctly."""
+    import torch
+    p, N = 4, 8000
+    a = inputs.gen_u32(p * N, 504)
+
+    def fn(c):
+        x = dev(a[c.rank * N:(c.rank + 1) * N])
+        ws = torch.empty(1024 if c.rank == 0 else
+                         rs.workspace_bytes(4, 0, 2 * N, 8, c), dtype=torch.uint8, device="cuda")
+        rs.sort(x, comm=c, ws=ws, out_cap=2 * N)
+    assert _statuses(p, fn) == [1] * p
+
+
+def test_out_aliasing_keys_rejected_with_comm():
+    """out overlapping keys is rejected (the pull merge reads every peer's block
+    while each rank writes Y_j): RS_EINVAL on every rank."""
+    p, N = 2, 4000
+    a = inputs.gen_u32(p * N, 505)
+
+    def fn(c):
+        x = dev(np.concatenate([a[c.rank * N:(c.rank + 1) * N], np.zeros(N, np.uint32)]))
+        rs.sort(x[:N], comm=c, out=x, out_cap=2 * N)
+    assert _statuses(p, fn) == [1] * p
+
+
+@pytest.mark.parametrize("pull", [1, 0])
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+def test_gsd_pull_and_alltoall_paths(option, pull, p):
+    """rs_sort_pairs_u64_u32 / rs_sort_u32 with a comm at p = 2, 3, 4, 8 on one
+    GPU, both data paths — the pull merge (peers' blocks read in place) and the
+    all-to-all fallback — bit-exact against oracle.gsd: counts, splitters, Y_j."""
+    option("gsd_pull", pull)
+    N = 12000 + 101 * p
+    k = inputs.gen_u64(p * N, 510 + p, "mod1024")
+    v = inputs.iota_u32(p * N)
+    _check([k[i * N:(i + 1) * N] for i in range(p)], r=8, b=8, vals_np=[v[i * N:(i + 1) * N] for i in range(p)])
+    a = inputs.gen_u32(p * N + 7, 520 + p)
+    cuts = np.linspace(0, a.size, p + 1).astype(int)
+    _check([a[cuts[i]:cuts[i + 1]] for i in range(p)], r=8, b=8)
+
+
+def test_repeated_calls_same_comm():
+    """Several collective calls on the same comms (mapping cache, header reuse)."""
+    p, N = 4, 10000
+    g = rs.LocalGroup(p)
+    arrays = [inputs.gen_u32(p * N, 530 + t) for t in range(3)]
+
+    def fn(c):
+        outs = []
+        for a in arrays:
+            y = rs.sort(dev(a[c.rank * N:(c.rank + 1) * N]), comm=c)
+            outs.append(host(y, np.uint32))
+        return outs
+    try:
+        res = g.run(fn)
+    finally:
+        g.close()
+    for t, a in enumerate(arrays):
+        assert (np.concatenate([res[k][t] for k in range(p)]) == np.sort(a)).all()

@@ -1,7 +1,8 @@
-"""BASELINE configs[3] and [4] at their full sizes on the multi-GPU path, all p = 8
-ranks emulated on this GPU (rs_gsd_emulate runs every rank's kernels — local
-sort, sample, splitters, split, and the default one-pass p-way pull merge — with
-device copies in place of NCCL).  Too large for the serial GSD simulator in a
+"""BASELINE configs[3] and [4] at their full sizes on the multi-GPU path: p = 8
+ranks as threads on this GPU, each calling rs_sort_u32 / rs_sort_pairs_u64_u32
+with its comm (LocalGroup: the multi-GPU orchestration — local sort, sample,
+splitters, split, the one host sync, and the default one-pass p-way pull merge
+reading the peers' blocks in place — over the in-process transport).  Too large for the serial GSD simulator in a
 test: the concatenation Y_0‖…‖Y_7 is checked for order, for the input multiset
 (hash + count), for 64 sampled order statistics against the unsorted input, and
 every |Y_j| against the balance bound ⌊(1 + 1/r)·N⌋ + p (R18); pairs
@@ -26,7 +27,7 @@ def test_config4_gsd_p8_full_size():
     a = inputs.gen_u32(n, 4)
     h_in = oracle.multiset_hash(a)
     blocks = [torch.from_numpy(a[k * N:(k + 1) * N].view(np.int32)).cuda() for k in range(p)]
-    got = rs.gsd_emulate(blocks, r=r, digit_bits=8)
+    got = rs.sort_ranks(blocks, "gsd", r=r, digit_bits=8)
     del blocks
     ys = [host(y, np.uint32) for y in got["Y"]]
     del got["Y"]
@@ -52,7 +53,7 @@ def test_config5_gsd_p8_full_size():
     kb = [torch.from_numpy(k[i * N:(i + 1) * N].view(np.int64)).cuda() for i in range(p)]
     vb = [torch.from_numpy(v[i * N:(i + 1) * N].view(np.int32)).cuda() for i in range(p)]
     del k, v
-    got = rs.gsd_emulate(kb, r=r, digit_bits=8, vals=vb)
+    got = rs.sort_ranks(kb, "gsd", r=r, digit_bits=8, vals=vb)
     del kb, vb
     yk = [host(t, np.uint64) for t in got["Y"]]
     yv = [host(t, np.uint32) for t in got["Yv"]]

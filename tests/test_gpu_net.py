@@ -1,8 +1,10 @@
-"""GPU parity of BTN and OET (rs_net_emulate: every rank's local
-sort and merge-split halves on this GPU, the same schedule and merge-range
-kernels the multi-GPU path runs over NVLink) against the CPU oracle
-(oracle/net.c): every block bit-exact, values included (both sides merge ties
-lower-indexed block first, so BTN's non-stable value order is also determined)."""
+"""GPU parity of BTN and OET: rs_sort_* with a comm in BTN / OET
+mode (rs_comm_set_sampling 4 / 5), one call per rank, the ranks being threads on
+this GPU (LocalGroup: the multi-GPU orchestration over the in-process transport;
+each rank computes its merge-split half reading its partner's block in place)
+against the CPU oracle (oracle/net.c): every block bit-exact, values included
+(both sides merge ties lower-indexed block first, so BTN's non-stable value order
+is also determined)."""
 import numpy as np
 import pytest
 import torch
@@ -18,8 +20,8 @@ pytestmark = pytest.mark.gpu
 def _check(mode, blocks_np, b=8, vals_np=None):
     dt = blocks_np[0].dtype
     want = getattr(oracle, mode)(blocks_np, b=b, vals=vals_np)
-    got = rs.net_emulate(mode, [dev(x) for x in blocks_np], digit_bits=b,
-                         vals=[dev(v) for v in vals_np] if vals_np is not None else None)
+    got = rs.sort_ranks([dev(x) for x in blocks_np], mode, digit_bits=b,
+                        vals=[dev(v) for v in vals_np] if vals_np is not None else None)
     for j in range(len(blocks_np)):
         assert (host(got["Y"][j], dt) == want["Y"][j]).all(), j
         if vals_np is not None:
@@ -73,10 +75,10 @@ def test_stage_counts_and_errors():
     assert [rs.net_stages("oet", p) for p in (1, 2, 3, 7)] == [1, 2, 3, 7]
     with pytest.raises(ValueError):
         rs.net_stages("btn", 6)
-    with pytest.raises(rs.RSortError):
-        rs.net_emulate("btn", [dev(np.zeros(4, np.uint32)) for _ in range(3)])
-    with pytest.raises(ValueError):
-        rs.net_emulate("oet", [dev(np.zeros(4, np.uint32)), dev(np.zeros(5, np.uint32))])
+    with pytest.raises(rs.RSortError):  # BTN over 3 ranks: RS_EINVAL on every rank
+        rs.sort_ranks([dev(np.zeros(4, np.uint32)) for _ in range(3)], "btn")
+    with pytest.raises(rs.RSortError):  # unequal blocks
+        rs.sort_ranks([dev(np.zeros(4, np.uint32)), dev(np.zeros(5, np.uint32))], "oet")
 
 
 @pytest.mark.parametrize("mode", ["btn", "oet"])
@@ -85,7 +87,7 @@ def test_large_blocks_property(mode):
     property that holds at any size; the oracle runs the element-wise cases)."""
     p, N = 8, 1 << 22
     a = torch.randint(0, 1 << 32, (p * N,), dtype=torch.int64, device="cuda").to(torch.int32)
-    got = rs.net_emulate(mode, [a[k * N:(k + 1) * N] for k in range(p)])
+    got = rs.sort_ranks([a[k * N:(k + 1) * N].clone() for k in range(p)], mode)
     y = torch.cat(got["Y"]).to(torch.int64) & 0xFFFFFFFF
     want = torch.sort(a.to(torch.int64) & 0xFFFFFFFF).values
     assert torch.equal(y, want)
