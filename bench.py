@@ -139,11 +139,70 @@ def bind_gpu_local_cpus(device_index: int):
     return None
 
 
+# ------------------------------------------------------- device-side verification
+_GOLD = 0x9E3779B97F4A7C15
+
+
+def _s64(c):  # unsigned 64-bit constant as a signed int64 (torch wraps on overflow)
+    return c - (1 << 64) if c >= 1 << 63 else c
+
+
+def _mix(x):
+    """SplitMix64 finaliser on an int64 tensor (wrapping arithmetic, logical shifts)."""
+    import torch
+    def shr(v, k):
+        return (v >> k) & ((1 << (64 - k)) - 1)
+    x = x ^ shr(x, 30)
+    x = x * _s64(0xBF58476D1CE4E5B9)
+    x = x ^ shr(x, 27)
+    x = x * _s64(0x94D049BB133111EB)
+    return x ^ shr(x, 31)
+
+
+def _as_u64(t):
+    """keys as int64 carrying the unsigned value's bits (u32 zero-extended)"""
+    import torch
+    return t.to(torch.int64) & 0xFFFFFFFF if t.dtype == torch.int32 else t
+
+
+def multiset_hash(keys, vals=None, chunk=1 << 26):
+    """(count, Σ mix(x), Σ mix(x + φ)) mod 2^64 over the (key[, value]) multiset."""
+    import torch
+    h1 = torch.zeros((), dtype=torch.int64, device=keys.device)
+    h2 = torch.zeros_like(h1)
+    for i in range(0, keys.numel(), chunk):
+        x = _as_u64(keys[i:i + chunk])
+        if vals is not None:
+            x = x ^ _mix(vals[i:i + chunk].to(torch.int64) & 0xFFFFFFFF)
+        h1 += _mix(x).sum()
+        h2 += _mix(x + _s64(_GOLD)).sum()
+    return [keys.numel(), int(h1), int(h2)]
+
+
+def order_violations(keys, vals=None, chunk=1 << 26):
+    """# adjacent inversions (unsigned order); with vals (= global index), also
+    # equal-key pairs whose values do not increase (stability)"""
+    import torch
+    bad = 0
+    n = keys.numel()
+    for i in range(0, max(n - 1, 0), chunk):
+        x = _as_u64(keys[i:min(i + chunk + 1, n)])
+        if keys.dtype == torch.int64:
+            x = x ^ _s64(1 << 63)  # unsigned order as signed order
+        bad += int((x[1:] < x[:-1]).sum())
+        if vals is not None:
+            v = vals[i:min(i + chunk + 1, n)].to(torch.int64) & 0xFFFFFFFF
+            bad += int(((x[1:] == x[:-1]) & (v[1:] <= v[:-1])).sum())
+    return bad
+
+
 def oracle_baseline(kind, seed, dist, b, target_s=10.0):
-    """The serial C oracle (SR-b) as it stands, on a bounded
-    sample of the workload's stream, one host core, until >= target_s elapsed."""
+    """The serial C oracle (SR-b) as it stands, built with gcc
+    -O3 -march=native on this host, on a bounded sample of the workload's stream,
+    one host core, until >= target_s elapsed."""
     import inputs
     import oracle
+    flags = oracle.use_native()
     n = 1 << 25
     if kind == "u32":
         a = inputs.gen_u32(n, seed, dist)
@@ -167,8 +226,9 @@ def oracle_baseline(kind, seed, dist, b, target_s=10.0):
     finally:
         os.sched_setaffinity(0, prev)
     return {"value": done / t_total / 1e9, "unit": "Gkeys/s", "cores": 1, "kind": "oracle", "core": core,
+            "flags": f"gcc {flags}",
             "sample": f"first 2^25 keys of the workload stream (seed {seed}, {dist}), serial SR-{b} oracle "
-                      f"(oracle/sr.c, gcc -O2), pinned to core {core}, {done // n} repetition(s), {t_total:.1f} s"}
+                      f"(oracle/sr.c, gcc {flags}), pinned to core {core}, {done // n} repetition(s), {t_total:.1f} s"}
 
 
 def run_reference(args):
@@ -179,6 +239,7 @@ def run_reference(args):
     kind, n_total, seed, dist, b, desc = CONFIGS[args.config]
     import inputs
     import oracle
+    flags = oracle.use_native()
     n = 1 << 25 if kind == "u32" else 1 << 24
     a = inputs.gen_u32(n, seed, dist) if kind == "u32" else inputs.gen_u64(n, seed, dist)
     vals = inputs.iota_u32(n) if kind == "pairs" else None
@@ -193,13 +254,15 @@ def run_reference(args):
             times.append(dt)
     t = sum(times) / len(times)
     v = n / t / 1e9
-    sample = f"first 2^{n.bit_length() - 1} keys of the workload stream per step, serial SR-{b} oracle, pinned to core {core}"
+    sample = (f"first 2^{n.bit_length() - 1} keys of the workload stream per step, serial SR-{b} oracle "
+              f"(gcc {flags}), pinned to core {core}")
     print(json.dumps({
         "impl": "reference", "metric": "sorted keys/sec", "value": round(v, 6), "unit": "Gkeys/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32" if kind == "u32" else "u64+u32",
         "data": "synthetic", "config": {"workload": args.config, "description": desc, "sample_keys": n},
-        "cpu_baseline": {"value": round(v, 6), "unit": "Gkeys/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": round(v, 6), "unit": "Gkeys/s", "cores": 1, "kind": "oracle", "sample": sample,
+                         "flags": f"gcc {flags}"},
         "e2e": {"value": round(v, 6), "unit": "Gkeys/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "host": host_info()}))
 
@@ -276,11 +339,17 @@ def main():
 
     out_cap = out.numel()
 
+    comm_n_out = [n]
+
     def one_sort():
         if kind == "u32":
-            return rs.sort(work, digit_bits=b, comm=comm, out=out, ws=ws, out_cap=out_cap)
-        return rs.sort_pairs(work, vals_work, digit_bits=b, comm=comm, out_keys=out, out_vals=vout, ws=ws,
-                             out_cap=out_cap)
+            r = rs.sort(work, digit_bits=b, comm=comm, out=out, ws=ws, out_cap=out_cap)
+            comm_n_out[0] = r.numel()
+            return r
+        r = rs.sort_pairs(work, vals_work, digit_bits=b, comm=comm, out_keys=out, out_vals=vout, ws=ws,
+                          out_cap=out_cap)
+        comm_n_out[0] = r[0].numel()
+        return r
 
     def barrier():
         if p > 1:
@@ -326,6 +395,40 @@ def main():
             step_ms.append(e0.elapsed_time(e1))
     L.rs_timing_enable(0)
     clocks = clk.summary()
+
+    # ---- the last timed step's output, checked on the device against the pristine
+    # input: nondecreasing (pairs: stable), same multiset (count + two SplitMix64
+    # sums), and across ranks the boundary last(Y_j) <= first(Y_{j+1})
+    res_k = out if comm is None else out[: comm_n_out[0]]
+    res_v = (vout if comm is None else vout[: comm_n_out[0]]) if kind == "pairs" else None
+    torch.cuda.synchronize()
+    h_in = multiset_hash(pristine, vals_pristine)
+    h_out = multiset_hash(res_k, res_v)
+    viol = order_violations(res_k, res_v)
+    edges = [None, None]
+    if res_k.numel():
+        edges = [int(_as_u64(res_k[:1])[0]), int(_as_u64(res_k[-1:])[0])]
+    if p > 1:
+        t = torch.tensor([h_in[1], h_in[2], h_out[1], h_out[2], h_out[0], viol], dtype=torch.int64, device=dev)
+        dist.all_reduce(t)  # wrapping sums of the per-rank hashes and counts
+        h_in = [n_total, int(t[0]), int(t[1])]
+        h_out = [int(t[4]), int(t[2]), int(t[3])]
+        viol = int(t[5])
+        allg = [None] * p
+        dist.all_gather_object(allg, edges)
+        last = None
+        for fe, le in allg:  # ranks in order; empty Y_j skipped
+            if fe is None:
+                continue
+            ufe = fe & ((1 << 64) - 1)
+            if last is not None and (ufe ^ (1 << 63) if kind == "pairs" else ufe) < last:
+                viol += 1
+            ule = le & ((1 << 64) - 1)
+            last = ule ^ (1 << 63) if kind == "pairs" else ule
+    verified = viol == 0 and h_in == h_out
+    verify = {"method": "device: adjacent order" + (" + stability (value = global index)" if kind == "pairs" else "") +
+                        (" + rank boundaries" if p > 1 else "") + "; multiset (count, two SplitMix64 sums) vs the "
+                        "pristine input", "violations": viol, "multiset_equal": h_in == h_out}
     ms_q, cnt_q = ctypes.c_double(), ctypes.c_int()
     L.rs_timing_query(b"onesweep", ctypes.byref(ms_q), ctypes.byref(cnt_q))
     pass_ms = ms_q.value / max(cnt_q.value, 1)
@@ -474,6 +577,7 @@ def main():
                    "l2": ("L2 flushed before every step (2x L2 write)" if flush is not None
                           else "inputs larger than L2 (no flush)"), "l2_bytes": l2_bytes,
                    "inputs": "resident in HBM, reset outside timed region"},
+        "verified": verified, "verify": verify,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         **({"nvlink_roofline": xchg} if xchg else {}),
         "clocks": clocks, "kernel_ms_per_step": round(all_kernels_ms / args.steps, 4),

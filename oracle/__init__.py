@@ -24,25 +24,40 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRCS = [os.path.join(_HERE, f) for f in ("sr.c", "gsd.c", "net.c", "verify.c")]
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
+# bench.py's CPU baseline: the same sources built on the timing host with
+# -O3 -march=native; tests use the generic build
+_NATIVE_PATH = os.path.join("/tmp", f"liboracle_native_{os.getuid()}_{os.getpid()}.so")
+_FLAGS = {"generic": ["-O2"], "native": ["-O3", "-march=native"]}
 _lib = None
+_flavor = "generic"
 
 
-def build(force: bool = False) -> str:
-    """gcc -O2 (generic x86-64, so the .so also runs on the GPU box's host)."""
+def build(force: bool = False, flavor: str = "generic") -> str:
+    """gcc -O2 generic x86-64 (the test build, also runs on the GPU box's host), or
+    flavor "native": gcc -O3 -march=native for this host (bench CPU baseline)."""
+    path = _LIB_PATH if flavor == "generic" else _NATIVE_PATH
     newest = max(os.path.getmtime(p) for p in _SRCS + [os.path.join(_HERE, "oracle.h")])
-    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < newest:
-        tmp = _LIB_PATH + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-fopenmp",
-                               "-o", tmp] + _SRCS)
-        os.replace(tmp, _LIB_PATH)
-    return _LIB_PATH
+    if force or not os.path.exists(path) or os.path.getmtime(path) < newest:
+        tmp = path + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc"] + _FLAGS[flavor] + ["-std=c99", "-fPIC", "-shared", "-o", tmp] + _SRCS)
+        os.replace(tmp, path)
+    return path
+
+
+def use_native() -> str:
+    """Load the -O3 -march=native build instead (before the first oracle call of
+    the process); returns the compiler flags used."""
+    global _flavor
+    if _lib is not None and _flavor != "native":
+        raise RuntimeError("oracle already loaded with the generic build")
+    _flavor = "native"
+    return " ".join(_FLAGS["native"])
 
 
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = ctypes.CDLL(_LIB_PATH)
+        L = ctypes.CDLL(build(flavor=_flavor))
         vp, sz, i32, u64 = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_uint64
         for name in ("or_sr_u32", "or_sr_u64"):
             getattr(L, name).argtypes = [vp, sz, i32, i32]

@@ -31,7 +31,7 @@ rs_status_t sort_entry(int key_bytes, void* keys, uint32_t* vals, bool want_vals
     // collective: a rank whose arguments fail still takes part in the header
     // exchange, so every rank returns RS_EINVAL instead of the others hanging
     if (comm)
-        return gsd_sort(static_cast<Comm*>(comm), key_bytes, keys, want_vals ? vals : nullptr, n, b, out,
+        return gsd_sort(static_cast<Comm*>(comm), key_bytes, keys, want_vals ? vals : nullptr, want_vals, n, b, out,
                         want_vals ? vout : nullptr, out_cap, n_out, ws, ws_bytes, st, s);
     if (s != RS_OK) return s;
     if (out_cap < n) return fail(RS_ECAPACITY, "out_cap < n");

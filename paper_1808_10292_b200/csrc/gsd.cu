@@ -496,7 +496,8 @@ constexpr uint64_t kMagic = 0x52534F5254ull;  // "RSORT"
 struct CallArgs {
     int key_bytes;
     void* keys;
-    uint32_t* vals;
+    uint32_t* vals;   // NULL for keys-only; may be NULL with n = 0 in a pair sort (hv says which)
+    bool hv;          // a pair sort (rs_sort_pairs_*), whatever this rank's n
     size_t n;
     int b;
     void* out;
@@ -512,7 +513,7 @@ static void fill_header(const Comm* c, const CallArgs& a, bool local_err, uint64
     std::memset(h, 0, kHdrWords * 8);
     h[kHMagic] = kMagic;
     h[kHKeyBytes] = (uint64_t)a.key_bytes;
-    h[kHHasVal] = a.vals != nullptr;
+    h[kHHasVal] = a.hv;
     h[kHBits] = (uint64_t)a.b;
     h[kHSampling] = (uint64_t)c->sampling;
     h[kHR] = (uint64_t)c->r;
@@ -551,7 +552,7 @@ static rs_status_t check_headers(const Comm* c, const uint64_t* all, const uint6
 // this rank's own argument checks, before anything is enqueued
 static std::string validate_local(Comm* c, const CallArgs& a, rs_status_t local_status) {
     if (local_status != RS_OK) return rs_last_error();
-    const bool hv = a.vals != nullptr;
+    const bool hv = a.hv;
     if (a.out_cap && (!a.out || (hv && !a.vout))) return "NULL output with out_cap > 0";
     if (!a.ws || !aligned16(a.ws)) return "collective workspace NULL or misaligned";
     if (c->nranks > 1 && c->sampling <= 2 && a.n && a.out_cap) {
@@ -576,7 +577,7 @@ static rs_status_t exchange_and_merge(Comm* c, const CallArgs& a, const GsdLayou
                                       const uint64_t* recs, size_t wc, bool gvr, uint64_t* total_out,
                                       cudaStream_t st) {
     const int p = c->nranks, rank = c->rank, kb = a.key_bytes;
-    const bool hv = a.vals != nullptr;
+    const bool hv = a.hv;
     std::vector<uint64_t> cnt((size_t)p * p);
     bool all_exported = true;
     for (int k = 0; k < p; ++k) {
@@ -590,7 +591,10 @@ static rs_status_t exchange_and_merge(Comm* c, const CallArgs& a, const GsdLayou
     const uint64_t total = roff[p];
     *total_out = total;
     rs_status_t s = RS_OK;
-    if (p == 1) {  // Y_0 = X_0
+    if (p == 1) {  // Y_0 = X_0 (GVR: its one local sort)
+        if (gvr)
+            return total ? local_sort(kb, X, XV, total, a.b, kb * 8, a.out, a.vout, L.local_ws, L.local_ws_bytes, st)
+                         : RS_OK;
         if (total && X != a.out) {
             RS_CUDA_TRY(cudaMemcpyAsync(a.out, X, total * kb, cudaMemcpyDeviceToDevice, st));
             if (hv) RS_CUDA_TRY(cudaMemcpyAsync(a.vout, XV, total * 4, cudaMemcpyDeviceToDevice, st));
@@ -652,7 +656,7 @@ static rs_status_t stage_peer_records(Comm* c, const CallArgs& a, const void* X,
     uint64_t* rec = c->h + 16;  // staging words [16, 16 + 2·kPeerRecWords + 2)
     std::memset(rec, 0, (2 * kPeerRecWords + 2) * 8);
     bool ok = want && c->tr->export_buffer(X, rec);
-    if (ok && a.vals) ok = c->tr->export_buffer(XV, rec + kPeerRecWords);
+    if (ok && a.hv) ok = c->tr->export_buffer(XV, rec + kPeerRecWords);
     rec[2 * kPeerRecWords] = ok ? 1 : 0;
     RS_CUDA_TRY(cudaMemcpyAsync(cnt_send + p, rec, (2 * kPeerRecWords + 2) * 8, cudaMemcpyHostToDevice, st));
     return RS_OK;
@@ -664,7 +668,7 @@ static rs_status_t gsd_regular(Comm* c, const CallArgs& a, const std::string& lo
     const int p = c->nranks, rank = c->rank, kb = a.key_bytes;
     const int s = c->r * p;
     const bool valid = local_err.empty();
-    const bool hv = a.vals != nullptr;
+    const bool hv = a.hv;
     const CommRegions R = comm_regions(c);
     const size_t Bs = 128 + 16 * (size_t)s;  // record: header + s composites
     unsigned char* samp_send = R.samp;
@@ -732,7 +736,7 @@ static rs_status_t gsd_regular(Comm* c, const CallArgs& a, const std::string& lo
 static rs_status_t gsd_random(Comm* c, const CallArgs& a, const std::vector<uint64_t>& n_all,
                               const std::vector<uint64_t>& caps, size_t* n_out, cudaStream_t st) {
     const int p = c->nranks, rank = c->rank, kb = a.key_bytes;
-    const bool hv = a.vals != nullptr, gvr = c->sampling == 2;
+    const bool hv = a.hv, gvr = c->sampling == 2;
     const CommRegions R = comm_regions(c);
     uint64_t* cnt_send = R.cnt;
     uint64_t* cnt_all = R.cnt + R.wc;
@@ -807,19 +811,19 @@ static rs_status_t gsd_random(Comm* c, const CallArgs& a, const std::vector<uint
     return RS_OK;
 }
 
-rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t n, int b, void* out, uint32_t* vout,
-                     size_t out_cap, size_t* n_out, void* ws, size_t ws_bytes, cudaStream_t st,
+rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, bool has_val, size_t n, int b, void* out,
+                     uint32_t* vout, size_t out_cap, size_t* n_out, void* ws, size_t ws_bytes, cudaStream_t st,
                      rs_status_t local_status) {
     c->last_host_syncs = 0;
     if (c->broken) return fail(RS_ENCCL, "communicator is broken by an earlier failure; destroy it");
     const int p = c->nranks;
-    CallArgs a{key_bytes, keys, vals, n, b, out, vout, out_cap, ws, ws_bytes, options().gsd_merge,
+    CallArgs a{key_bytes, keys, vals, has_val, n, b, out, vout, out_cap, ws, ws_bytes, options().gsd_merge,
                options().gsd_pull != 0};
     std::string local_err = validate_local(c, a, local_status);
     if (local_err.empty() && c->sampling == 0 && (size_t)c->r * p * p > (size_t)kMaxSample)
         local_err = "r·p² exceeds the one-CTA sample sort limit of 8192";
     if (local_err.empty()) {
-        const size_t need = ws_need(c, key_bytes, vals != nullptr, n, out_cap, b, 0);
+        const size_t need = ws_need(c, key_bytes, has_val, n, out_cap, b, 0);
         if (c->sampling != 1 && c->sampling != 2 && ws_bytes < need)
             local_err = "collective workspace too small: need " + std::to_string(need) + " bytes";
     }
@@ -836,11 +840,11 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
     if (c->sampling == 3) {  // PR4 across GPUs: sizes, digit width and capacity agreed here
         if (b != 8) return fail(RS_EINVAL, "PR4 routing across GPUs is radix 256 (digit_bits 8)");
         for (int k = 0; k < p; ++k) {
-            if (all[(size_t)k * kHdrWords + kHWs] < pr_ws_bytes(key_bytes, vals, n_all[k], p))
+            if (all[(size_t)k * kHdrWords + kHWs] < pr_ws_bytes(key_bytes, has_val, n_all[k], p))
                 return fail(RS_EINVAL, "PR workspace of rank " + std::to_string(k) + " too small");
             if (caps[k] < n_all[k]) return fail(RS_ECAPACITY, "PR: out_cap < n on rank " + std::to_string(k));
         }
-        return pr_sort(c, key_bytes, keys, vals, n, out, vout, n_out, ws, n_all, st);
+        return pr_sort(c, key_bytes, keys, vals, has_val, n, out, vout, n_out, ws, n_all, st);
     }
     if (c->sampling >= 4) {  // BTN / OET: equal blocks (reading R34), agreed here
         if (c->sampling == 4 && (p & (p - 1))) return fail(RS_EINVAL, "BTN needs a power-of-two number of ranks");
@@ -849,13 +853,13 @@ rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t 
                 return fail(RS_EINVAL, "BTN/OET need the same n on every rank (rank " + std::to_string(k) + ")");
             if (caps[k] < n_all[k]) return fail(RS_ECAPACITY, "BTN/OET: out_cap < n on rank " + std::to_string(k));
         }
-        return net_sort(c, key_bytes, keys, vals, n, b, out, vout, n_out, ws, st);
+        return net_sort(c, key_bytes, keys, vals, has_val, n, b, out, vout, n_out, ws, st);
     }
     // GER / GVR: every rank checks every rank's workspace (sizes from the headers)
     uint64_t n_total = 0;
     for (int k = 0; k < p; ++k) n_total += n_all[k];
     for (int k = 0; k < p; ++k) {
-        const size_t need = ws_need(c, key_bytes, vals != nullptr, n_all[k], caps[k], b, n_total);
+        const size_t need = ws_need(c, key_bytes, has_val, n_all[k], caps[k], b, n_total);
         if (all[(size_t)k * kHdrWords + kHWs] < need)
             return fail(RS_EINVAL, "workspace of rank " + std::to_string(k) + " too small: need " +
                                        std::to_string(need) + " (size it with the largest local n)");

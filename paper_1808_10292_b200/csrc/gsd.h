@@ -123,13 +123,13 @@ size_t ger_default_s(uint64_t n_total);
 
 // PR4 across GPUs (pr.cu; Comm::sampling = 3)
 size_t pr_ws_bytes(int key_bytes, bool hv, size_t n_local_max, int p);
-rs_status_t pr_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t n, void* out, uint32_t* vout,
+rs_status_t pr_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, bool hv, size_t n, void* out, uint32_t* vout,
                     size_t* n_out, void* ws, const std::vector<uint64_t>& n_all, cudaStream_t st);
 
 // BTN / OET across GPUs (net.cu; Comm::sampling = 4 / 5)
 size_t net_ws_bytes(int key_bytes, bool hv, size_t n_local, int b);
-rs_status_t net_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t n, int b, void* out, uint32_t* vout,
-                     size_t* n_out, void* ws, cudaStream_t st);
+rs_status_t net_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, bool hv, size_t n, int b, void* out,
+                     uint32_t* vout, size_t* n_out, void* ws, cudaStream_t st);
 int net_stage_count(int mode, int p);
 
 // map every peer's buffers (nb per rank): peers[k·nb + i] = rank k's ptrs[i]
@@ -141,7 +141,8 @@ size_t gsd_capacity(Comm* c, size_t n_local_max);
 size_t gsd_ws_bytes(Comm* c, int key_bytes, bool has_val, size_t n_local_max, int b);
 // local_status: the caller's validation of this rank's arguments; a failure on
 // any rank makes every rank return RS_EINVAL (no hang)
-rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t n, int b, void* out,
+// has_val: a pair sort (vals may be NULL on a rank with n = 0)
+rs_status_t gsd_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, bool has_val, size_t n, int b, void* out,
                      uint32_t* vout, size_t out_cap, size_t* n_out, void* ws, size_t ws_bytes, cudaStream_t st,
                      rs_status_t local_status = RS_OK);
 

@@ -110,10 +110,9 @@ static rs_status_t merge_split_half(int key_bytes, size_t N, int self, int partn
 
 // the multi-GPU call: header / validation done by gsd_sort (equal n on every rank,
 // out_cap >= n, workspaces sized, BTN p a power of 2)
-rs_status_t net_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, size_t n, int b, void* out, uint32_t* vout,
-                     size_t* n_out, void* ws, cudaStream_t st) {
+rs_status_t net_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, bool hv, size_t n, int b, void* out,
+                     uint32_t* vout, size_t* n_out, void* ws, cudaStream_t st) {
     const int p = c->nranks, rank = c->rank;
-    const bool hv = vals != nullptr;
     if (n_out) *n_out = n;
     if (p == 1 || n == 0) {
         rs_status_t s = RS_OK;

@@ -95,11 +95,18 @@ public:
             if (spin > 2000) std::this_thread::sleep_for(std::chrono::microseconds(20));
         }
     }
+    // a NULL buffer (a rank with n = 0) travels as the all-zero record: never read
     bool export_buffer(const void* p, uint64_t* rec) override {
         std::memset(rec, 0, kPeerRecWords * 8);
-        return ipc_export(p, rec, &rec[8]) == RS_OK;
+        return !p || ipc_export(p, rec, &rec[8]) == RS_OK;
     }
     rs_status_t open_peer(int k, const uint64_t* rec, void** p) override {
+        bool null_rec = true;
+        for (int i = 0; i < kPeerRecWords; ++i) null_rec = null_rec && rec[i] == 0;
+        if (null_rec) {
+            *p = nullptr;
+            return RS_OK;
+        }
         const std::pair<int, std::string> key(k, std::string(reinterpret_cast<const char*>(rec), 64));
         auto it = maps_.find(key);
         if (it == maps_.end()) {

@@ -50,6 +50,20 @@ def test_gsd_hand_trace_spec290():
     assert [host(y, np.uint32).tolist() for y in got["Y"]] == [list(range(1, 9)), list(range(9, 17))]
 
 
+def test_gsd_hand_trace_p3_r2():
+    """The hand-derived p = 3, r = 2 trace (tests/golden/gsd_hand_trace_p3_r2.json)
+    through rs_sort_u32 with a comm on three in-process ranks: the literal
+    splitters, count matrix and Y_j."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "gsd_hand_trace_p3_r2.json")))
+    blocks = [np.array(b, dtype=np.uint32) for b in g["blocks"]]
+    got = _check(blocks, r=g["r"], b=8)
+    assert got["splitters"].tolist() == g["splitters"]
+    assert got["counts"].tolist() == g["counts"]
+    assert [host(y, np.uint32).tolist() for y in got["Y"]] == g["Y"]
+
+
 @pytest.mark.parametrize("b", [8, 16])
 def test_gsd_pairs_global_stability(b):
     p, N = 4, 30000

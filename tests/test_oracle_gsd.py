@@ -23,6 +23,27 @@ def test_hand_trace_spec290():
     assert res["counts"].tolist() == [[4, 4], [4, 4]]
 
 
+def test_hand_trace_p3_r2_duplicates():
+    """A hand-derived trace beyond SPEC.md:290 (tests/golden/gsd_hand_trace_p3_r2.json):
+    p = 3, r = 2, duplicates within and across ranks, every intermediate written
+    out by hand (X_k, T_k, T, S_i with their rank and position, the composite cuts,
+    X_{k,j}, Y_j).  A wrong sample index (R10), splitter index (R12) or tie
+    direction at a splitter (R14) changes the counts or the splitters."""
+    g = json.load(open(os.path.join(GOLD, "gsd_hand_trace_p3_r2.json")))
+    shards = [np.array(b, dtype=np.uint32) for b in g["blocks"]]
+    res = oracle.gsd(shards, r=g["r"])
+    assert res["splitters"].tolist() == g["splitters"]
+    assert res["counts"].tolist() == g["counts"]
+    assert [y.tolist() for y in res["Y"]] == g["Y"]
+    assert max(len(y) for y in g["Y"]) <= g["balance_bound"]
+    # the hand-written intermediates agree with each other (slices of X_k by counts)
+    for k in range(g["p"]):
+        assert sum(g["X_kj"][k], []) == g["X_k"][k] == sorted(g["blocks"][k])
+        assert [len(x) for x in g["X_kj"][k]] == g["counts"][k]
+    for j in range(g["p"]):
+        assert sorted(sum((g["X_kj"][k][j] for k in range(g["p"])), [])) == g["Y"][j]
+
+
 def _shards(total, p, seed, dist="uniform"):
     a = inputs.gen_u32(total, seed, dist)
     N = total // p
