@@ -32,6 +32,17 @@
 
 #include "onesweep_ec.cuh"
 
+// LPC (count-then-rank passes): [rank] counts into LANE-PRIVATE byte counters laid
+// over the (then unused) sorted-tile buffer — warp w, lane l, digit d at byte d % 4
+// of word w·2048 + (d / 4)·32 + l, so every lane's RED hits its own bank (one
+// shared-memory wavefront per warp instruction instead of ~3.8 for 32 random
+// digits on shared counters); each warp then sums its 32 lanes' bytes into its
+// 16-bit digit counters (staggered 16-byte loads, two words added byte-wise
+// before the 16-bit split: a byte holds <= KPT <= 127 keys).
+#ifndef RS_AR_LPC
+#define RS_AR_LPC 0
+#endif
+
 namespace rs {
 
 template <typename K, bool HAS_VAL, int RT, int KPT>
@@ -90,6 +101,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         vdst = pick<uint32_t>(ds, const_cast<uint32_t*>(a.vals_in), a.vals_out, a.vals_alt);
     }
     const int shift = a.shift;
+    constexpr bool LPC = RS_AR_LPC && R2A && KPT <= 127 && (size_t)W * 2048 * 4 <= (size_t)TILE * sizeof(K);
 
     auto prefetch = [&](uint32_t t) {  // thread 0 only: the tile into L2 by the TMA engine
         const size_t base = (size_t)t * TILE;
@@ -121,7 +133,41 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         const uint32_t lim = valid - min(valid, (uint32_t)(warp * WK + lane));
 
         // ---- [rank] one shared atomic per key: per-warp histogram (+ ranks)
-        {
+        if (LPC) {
+            uint32_t* lp = reinterpret_cast<uint32_t*>(smem + C::out_off) + warp * 2048;
+#pragma unroll
+            for (int q = 0; q < 16; ++q) reinterpret_cast<uint4*>(lp)[q * 32 + lane] = make_uint4(0u, 0u, 0u, 0u);
+            __syncwarp();
+#pragma unroll
+            for (int g = 0; g < KPT; g += G) {
+                K kk[G];
+#pragma unroll
+                for (int i = 0; i < G; ++i) kk[i] = (uint32_t)((g + i) * 32) < lim ? gk[(g + i) * 32] : ~K(0);
+#pragma unroll
+                for (int i = 0; i < G; ++i) {
+                    const uint32_t d = digit8<K>(kk[i], shift);
+                    atomicAdd(&lp[(d >> 2) * 32 + lane], 1u << ((d & 3u) << 3));
+                }
+            }
+            __syncwarp();
+            // lane l sums rows l and l + 32 (digits 4·row .. 4·row + 3) over the 32 lanes
+            uint32_t* wc = s_wc + warp * (WCW / W);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int row = lane + 32 * h;
+                const uint4* rp = reinterpret_cast<const uint4*>(lp + row * 32);
+                uint32_t lo = 0, hi = 0;  // 16-bit lanes: lo = digits 4r, 4r+2; hi = 4r+1, 4r+3
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const uint4 v = rp[(q + lane) & 7];  // staggered: 8 lanes cover the 32 banks
+                    const uint32_t s0 = v.x + v.y, s1 = v.z + v.w;  // bytes <= 2·KPT < 256
+                    lo += (s0 & 0x00FF00FFu) + (s1 & 0x00FF00FFu);
+                    hi += ((s0 >> 8) & 0x00FF00FFu) + ((s1 >> 8) & 0x00FF00FFu);
+                }
+                wc[2 * row] = (lo & 0xFFFFu) | (hi << 16);
+                wc[2 * row + 1] = (lo >> 16) | (hi & 0xFFFF0000u);
+            }
+        } else {
             uint32_t* wc = s_wc + warp * (WCW / W);
             // groups of G keys: G loads, then G atomics, then the packing of their
             // results, so G shared-memory round trips overlap
