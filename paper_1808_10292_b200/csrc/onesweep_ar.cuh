@@ -2,46 +2,52 @@
 // stable count-sort round of radix 256:
 //
 //   [load]    each warp reads its rows of the tile straight from global memory
-//             (the tile was prefetched into L2 by the TMA engine at [next])
-//   [rank]    warp w, row j (32 consecutive keys, lane order = input order):
-//             an atomicAdd on the warp's shared-memory counter of the key's digit
-//             d.  RANK2 = 0 keeps the returned old values: they ARE the stable
-//             ranks of the keys among the warp's keys of digit d (earlier rows
-//             were counted by earlier instructions, and within one instruction
-//             the sm_100 shared-memory atomic unit returns the old values of
-//             lanes that hit the same address in ascending lane order).  RANK2 = 1
-//             (count-then-rank) only counts here, with non-returning REDs.  The
-//             lane order is a measured hardware property, not a PTX guarantee:
-//             the library checks it with a probe kernel of this kernel's shape
-//             before it selects this design (radix.cu) and otherwise runs design
-//             2 (ballot ranks, onesweep_ec.cuh).  The final counter values are the
-//             warp's digit histogram: the counting of PAPER.md:664-667.
+//             (the tile was prefetched into L2 by the TMA engine at [next]);
+//             keys-only large tiles keep them in registers until [scatter]
+//   [rank]    warp w, row j (32 consecutive keys, lane order = input order).
+//             Pairs (RANK2 = 0): one returning atomicAdd per key on the warp's
+//             16-bit counter of its digit d; the returned old values ARE the
+//             stable ranks of the keys among the warp's keys of digit d (earlier
+//             rows were counted by earlier instructions, and within one
+//             instruction the sm_100 shared-memory atomic unit returns the old
+//             values of lanes that hit the same address in ascending lane order).
+//             Keys only (RANK2 = 1, count-then-rank): this phase only counts —
+//             on the large tiles into LANE-PRIVATE byte counters laid over the
+//             (then unused) sorted-tile buffer, warp w / lane l / digit d at byte
+//             d % 4 of word w·2048 + (d / 4)·32 + l, so every lane's RED hits its
+//             own bank (one shared-memory wavefront per warp instruction instead
+//             of ~3.8 for 32 random digits), after which each warp sums its 32
+//             lanes' bytes into its 16-bit counters; on the small tiles by REDs on
+//             the warp's 16-bit counters.  The lane order of the returning atomics
+//             is a measured hardware property, not a PTX guarantee: the library
+//             checks it with a probe kernel of this kernel's shape before it
+//             selects this design (radix.cu) and otherwise runs design 2 (ballot
+//             ranks, onesweep_ec.cuh).  The counters end as the warp's digit
+//             histogram: the counting of PAPER.md:664-667.
 //   [offset]  thread d: tile count, in-tile offset of digit d, per-warp start
 //             offsets; publish the tile count to the look-back status (flag A,
 //             or P for tile 0) — the tiles x 256 counter matrix of PR4,
 //             PAPER.md:690-694
 //   [scatter] key -> s_out[start_w[d] + r]  (the tile sorted by digit, stably);
-//             RANK2 = 1 takes start + r from a second returning atomic on the
-//             counters [offset] turned into warp starts (no rank registers)
+//             RANK2 = 1 takes start + r from a returning atomic on the counters
+//             [offset] turned into warp starts (no rank registers)
 //   [lookback] thread d: windowed decoupled look-back over earlier tiles,
 //             publishes the inclusive prefix (flag P)
 //   [next]    thread 0 takes the next tile id and L2-prefetches it (TMA engine)
-//   [store]   consecutive threads store consecutive s_out slots: each bucket run
-//             is a coalesced burst at base[d] + prefix[d] + offset
+//   [store]   32 consecutive sorted slots per warp instruction: each bucket run
+//             leaves as coalesced bursts at base[d] + prefix[d] + offset.  Keys
+//             only: each warp walks a contiguous range of the tile and each lane
+//             caches the bucket offset of its previous key's digit, so the offset
+//             lookup is a rare predicated shared load (a lane's next key, 32
+//             slots on, is mostly in the same run)
+//
+// What bounds the pass: the SM's L1 / shared-memory data pipe (ncu, u32 at 2^27:
+// ~83 % of its wavefronts busy before the lane-private count, the register-
+// resident keys and the cached offsets, which together cut its wavefronts per key
+// by ~12 %).
 #pragma once
 
 #include "onesweep_ec.cuh"
-
-// LPC (count-then-rank passes): [rank] counts into LANE-PRIVATE byte counters laid
-// over the (then unused) sorted-tile buffer — warp w, lane l, digit d at byte d % 4
-// of word w·2048 + (d / 4)·32 + l, so every lane's RED hits its own bank (one
-// shared-memory wavefront per warp instruction instead of ~3.8 for 32 random
-// digits on shared counters); each warp then sums its 32 lanes' bytes into its
-// 16-bit digit counters (staggered 16-byte loads, two words added byte-wise
-// before the 16-bit split: a byte holds <= KPT <= 127 keys).
-#ifndef RS_AR_LPC
-#define RS_AR_LPC 0
-#endif
 
 namespace rs {
 
@@ -60,6 +66,9 @@ struct OnesweepArCfg {
     static constexpr size_t gofs_off = tcnt_off + R * 4;
     static constexpr size_t misc_off = gofs_off + R * 4;
     static constexpr size_t smem_bytes = misc_off + 64 * 4;
+    // keys-only large tiles: lane-private count + keys in registers + cached offsets
+    static constexpr bool kLpc =
+        !HAS_VAL && KPT % 8 == 0 && KPT <= 127 && (size_t)W * 2048 * 4 <= (size_t)TILE * sizeof(K);
 };
 
 template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, int RANK2, int LB>
@@ -70,6 +79,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
     static_assert(RT % R == 0, "threads 0..255: one per digit in the offset and look-back phases");
     static_assert(KPT % 2 == 0 && WK <= 65536, "16-bit counters; ranks are packed two per register");
     constexpr bool R2A = RANK2 == 1;
+    constexpr bool LPC = R2A && C::kLpc;  // lane-private count, keys in registers, cached offsets
     extern __shared__ __align__(128) unsigned char smem[];
     K* s_out = reinterpret_cast<K*>(smem + C::out_off);
     uint32_t* s_vout = reinterpret_cast<uint32_t*>(smem + C::vout_off);
@@ -101,7 +111,6 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         vdst = pick<uint32_t>(ds, const_cast<uint32_t*>(a.vals_in), a.vals_out, a.vals_alt);
     }
     const int shift = a.shift;
-    constexpr bool LPC = RS_AR_LPC && R2A && KPT <= 127 && (size_t)W * 2048 * 4 <= (size_t)TILE * sizeof(K);
 
     auto prefetch = [&](uint32_t t) {  // thread 0 only: the tile into L2 by the TMA engine
         const size_t base = (size_t)t * TILE;
@@ -121,8 +130,10 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
     for (int i = tid; i < WCW; i += THREADS) s_wc[i] = 0;
     __syncthreads();
     uint32_t tile = s_misc[0];
-    constexpr int G = KPT % 8 == 0 ? 8 : (KPT % 6 == 0 ? 6 : (KPT % 4 == 0 ? 4 : 2));  // batch of keys
-    uint32_t rr[R2A ? 1 : KPT / 2];  // stable ranks within the warp's keys of their digit, 16 bits each
+    // batches of G keys: G loads, then G atomics, so G shared-memory round trips overlap
+    constexpr int G = KPT % 8 == 0 ? 8 : (KPT % 6 == 0 ? 6 : (KPT % 4 == 0 ? 4 : 2));
+    uint32_t rr[R2A ? 1 : KPT / 2];  // pairs: stable ranks within the warp's keys of their digit, 16 bits each
+    K kr[LPC ? KPT : 1];             // keys-only large tiles: this thread's keys of the tile
 
     while (tile < a.num_tiles) {
         const size_t base = (size_t)tile * TILE;
@@ -132,7 +143,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         const K* gk = src + base + warp * WK + lane;
         const uint32_t lim = valid - min(valid, (uint32_t)(warp * WK + lane));
 
-        // ---- [rank] one shared atomic per key: per-warp histogram (+ ranks)
+        // ---- [rank]
         if (LPC) {
             uint32_t* lp = reinterpret_cast<uint32_t*>(smem + C::out_off) + warp * 2048;
 #pragma unroll
@@ -140,12 +151,12 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             __syncwarp();
 #pragma unroll
             for (int g = 0; g < KPT; g += G) {
-                K kk[G];
 #pragma unroll
-                for (int i = 0; i < G; ++i) kk[i] = (uint32_t)((g + i) * 32) < lim ? gk[(g + i) * 32] : ~K(0);
+                for (int i = 0; i < G; ++i)
+                    kr[LPC ? g + i : 0] = (uint32_t)((g + i) * 32) < lim ? gk[(g + i) * 32] : ~K(0);
 #pragma unroll
                 for (int i = 0; i < G; ++i) {
-                    const uint32_t d = digit8<K>(kk[i], shift);
+                    const uint32_t d = digit8<K>(kr[LPC ? g + i : 0], shift);
                     atomicAdd(&lp[(d >> 2) * 32 + lane], 1u << ((d & 3u) << 3));
                 }
             }
@@ -169,8 +180,6 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             }
         } else {
             uint32_t* wc = s_wc + warp * (WCW / W);
-            // groups of G keys: G loads, then G atomics, then the packing of their
-            // results, so G shared-memory round trips overlap
 #pragma unroll
             for (int g = 0; g < KPT; g += G) {
                 K kk[G];
@@ -239,7 +248,9 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                 K kk[G];
                 uint32_t pos[G], vv[HAS_VAL ? G : 1];
 #pragma unroll
-                for (int i = 0; i < G; ++i) kk[i] = (uint32_t)((g + i) * 32) < lim ? __ldcs(gk + (g + i) * 32) : ~K(0);
+                for (int i = 0; i < G; ++i)
+                    kk[i] = LPC ? kr[LPC ? g + i : 0]
+                                : ((uint32_t)((g + i) * 32) < lim ? __ldcs(gk + (g + i) * 32) : ~K(0));
 #pragma unroll
                 for (int i = 0; i < G; ++i) {
                     const int j = g + i;
@@ -296,14 +307,44 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             s_misc[0] = nt;
             if (nt < a.num_tiles) prefetch(nt);
         }
+        if (!LPC) {  // (the lane-private count rewrites every counter)
 #pragma unroll
-        for (int i = 0; i < (WCW + THREADS - 1) / THREADS; ++i)
-            if (WCW % THREADS == 0 || i * THREADS + tid < WCW) s_wc[i * THREADS + tid] = 0;
+            for (int i = 0; i < (WCW + THREADS - 1) / THREADS; ++i)
+                if (WCW % THREADS == 0 || i * THREADS + tid < WCW) s_wc[i * THREADS + tid] = 0;
+        }
 
-        // ---- [store] bucket runs leave as coalesced bursts (full tiles in batches of
-        // 4 loads, 4 offset lookups, 4 stores: u32 2^27 pass 0.336 -> 0.326 ms against 8)
-        if (valid == (uint32_t)TILE) {
-            constexpr int SG = KPT % 4 == 0 ? 4 : 2;
+        // ---- [store] bucket runs leave as coalesced bursts (batches of 4 loads, 4
+        // offset lookups, 4 stores: u32 2^27 pass 0.336 -> 0.326 ms against 8)
+        constexpr int SG = KPT % 4 == 0 ? 4 : 2;
+        if (LPC && valid == (uint32_t)TILE) {
+            const int sb = warp * WK + lane;     // warp w: slots [w·WK, (w+1)·WK)
+            uint32_t cd = 0xFFFFFFFFu, cg = 0;  // cached digit and its bucket offset
+#pragma unroll 1
+            for (int j = 0; j < KPT; j += SG) {
+                K k[SG];
+                uint32_t g[SG];
+#pragma unroll
+                for (int i = 0; i < SG; ++i) k[i] = s_out[sb + (j + i) * 32];
+#pragma unroll
+                for (int i = 0; i < SG; ++i) {
+                    const uint32_t d = digit8<K>(k[i], shift);
+                    g[i] = cg;  // predicated load: only lanes whose digit changed touch shared memory
+                    asm volatile("{\n.reg .pred p;\nsetp.ne.u32 p, %1, %2;\n@p ld.shared.u32 %0, [%3];\n}"
+                                 : "+r"(g[i])
+                                 : "r"(d), "r"(cd), "r"(smem_addr(s_gofs + d)));
+                    if (i == SG - 1) cd = d;
+                }
+                cg = g[SG - 1];
+#pragma unroll
+                for (int i = 0; i < SG; ++i) {
+                    const uint32_t gi = g[i] + (uint32_t)(sb + (j + i) * 32);
+                    RS_DCHECK(gi < a.n);
+                    // evict-first stores for u32 keys (2^27 pass 0.335 -> 0.328 ms, DRAM bytes unchanged)
+                    if (sizeof(K) == 4) __stcs(&dst[gi], k[i]);
+                    else dst[gi] = k[i];
+                }
+            }
+        } else if (valid == (uint32_t)TILE) {
 #pragma unroll 1
             for (int b = 0; b < KPT; b += SG) {
                 K k[SG];
@@ -318,7 +359,6 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
 #pragma unroll
                 for (int i = 0; i < SG; ++i) {
                     RS_DCHECK(g[i] < a.n);
-                    // evict-first stores for u32 keys (2^27 pass 0.335 -> 0.328 ms, DRAM bytes unchanged)
                     if (sizeof(K) == 4 && !HAS_VAL) __stcs(&dst[g[i]], k[i]);
                     else dst[g[i]] = k[i];
                     if (HAS_VAL) vdst[g[i]] = vv[HAS_VAL ? i : 0];

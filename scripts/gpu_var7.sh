@@ -1,0 +1,6 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+for v in krlpcsc abltma; do
+  L=paper_1808_10292_b200/librsort_$v.so
+  RS_ONE_PASS=1 RS_LIB_PATH=$L python scripts/quick_bench.py 27 31 > gpurun_out/qb7_$v.log 2>&1
+  echo "== $v"; grep -h "pass" gpurun_out/qb7_$v.log
+done

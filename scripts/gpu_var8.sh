@@ -1,0 +1,10 @@
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+for v in tb tb72; do
+  RS_LIB_PATH=paper_1808_10292_b200/librsort_$v.so timeout 900 python -m pytest tests/test_gpu_radix.py -m "gpu and not slow" -q -x -p no:cacheprovider > gpurun_out/t_$v.log 2>&1
+  echo "$v $(tail -1 gpurun_out/t_$v.log)"
+done
+for v in krlpcsc tb tb80 tb72; do
+  L=paper_1808_10292_b200/librsort_$v.so
+  RS_LIB_PATH=$L python scripts/quick_bench.py 27 31 28:u64 > gpurun_out/qb8_$v.log 2>&1
+  echo "== $v"; grep -h "pass" gpurun_out/qb8_$v.log
+done
