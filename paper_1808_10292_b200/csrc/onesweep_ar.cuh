@@ -149,13 +149,17 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
 #pragma unroll
             for (int q = 0; q < 16; ++q) reinterpret_cast<uint4*>(lp)[q * 32 + lane] = make_uint4(0u, 0u, 0u, 0u);
             __syncwarp();
+            // loads per batch (they all land in kr): half a row block in flight at once
+            // (u32 2^31 pass: batches of 8 4.42 ms, 22 4.43, 44 4.29, 88 4.35)
+            // (u64 keys: batches of 8, 0.936 ms per 2^28 pass against 0.952 with 20)
+            constexpr int GR = sizeof(K) == 4 && (KPT / 2) % 2 == 0 ? KPT / 2 : G;
 #pragma unroll
-            for (int g = 0; g < KPT; g += G) {
+            for (int g = 0; g < KPT; g += GR) {
 #pragma unroll
-                for (int i = 0; i < G; ++i)
+                for (int i = 0; i < GR; ++i)
                     kr[LPC ? g + i : 0] = (uint32_t)((g + i) * 32) < lim ? gk[(g + i) * 32] : ~K(0);
 #pragma unroll
-                for (int i = 0; i < G; ++i) {
+                for (int i = 0; i < GR; ++i) {
                     const uint32_t d = digit8<K>(kr[LPC ? g + i : 0], shift);
                     atomicAdd(&lp[(d >> 2) * 32 + lane], 1u << ((d & 3u) << 3));
                 }
@@ -243,16 +247,21 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             uint32_t* wcp = s_wc + warp * (WCW / W);
             const uint16_t* wc16 = s_wc16 + warp * R;
             const int ibase = warp * WK + lane;
+#ifdef RS_AR_GS
+            constexpr int GS = LPC && KPT % RS_AR_GS == 0 ? RS_AR_GS : G;
+#else
+            constexpr int GS = G;
+#endif
 #pragma unroll
-            for (int g = 0; g < KPT; g += G) {
-                K kk[G];
-                uint32_t pos[G], vv[HAS_VAL ? G : 1];
+            for (int g = 0; g < KPT; g += GS) {
+                K kk[GS];
+                uint32_t pos[GS], vv[HAS_VAL ? GS : 1];
 #pragma unroll
-                for (int i = 0; i < G; ++i)
+                for (int i = 0; i < GS; ++i)
                     kk[i] = LPC ? kr[LPC ? g + i : 0]
                                 : ((uint32_t)((g + i) * 32) < lim ? __ldcs(gk + (g + i) * 32) : ~K(0));
 #pragma unroll
-                for (int i = 0; i < G; ++i) {
+                for (int i = 0; i < GS; ++i) {
                     const int j = g + i;
                     const uint32_t d = digit8<K>(kk[i], shift);
                     if (R2A) {
@@ -266,7 +275,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                         vv[HAS_VAL ? i : 0] = (uint32_t)(j * 32) < lim ? __ldcs(vsrc + base + ibase + j * 32) : 0u;
                 }
 #pragma unroll
-                for (int i = 0; i < G; ++i) {
+                for (int i = 0; i < GS; ++i) {
                     RS_DCHECK(pos[i] < (uint32_t)TILE);
                     s_out[pos[i]] = kk[i];
                     if (HAS_VAL) s_vout[pos[i]] = vv[HAS_VAL ? i : 0];

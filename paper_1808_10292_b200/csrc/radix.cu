@@ -143,7 +143,10 @@ static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st) 
     using TN = typename std::conditional<SMALL, TuneArSmall<K, V>, TuneAr<K, V>>::type;
     using C = OnesweepArCfg<K, V, TN::THREADS, TN::KPT>;
     // look-back window 8 (measured 2..64 on the small tiles, 4 and 16 on the large)
-    auto kern = k_onesweep_ar<K, V, TN::THREADS, TN::KPT, TN::MINB, S, Rank2<V>::value, 8>;
+#ifndef RS_AR_LB
+#define RS_AR_LB 8
+#endif
+    auto kern = k_onesweep_ar<K, V, TN::THREADS, TN::KPT, TN::MINB, S, Rank2<V>::value, SMALL ? 8 : RS_AR_LB>;
     int grid_cap = 0;
     rs_status_t s = kernel_setup(reinterpret_cast<const void*>(kern), C::THREADS, C::smem_bytes, &grid_cap);
     if (s != RS_OK) return s;
