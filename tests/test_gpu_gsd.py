@@ -64,6 +64,20 @@ def test_gsd_hand_trace_p3_r2():
     assert [host(y, np.uint32).tolist() for y in got["Y"]] == g["Y"]
 
 
+def test_ger_gvr_hand_trace_p2_s2():
+    """The hand-derived GER / GVR traces (tests/golden/ger_gvr_hand_trace_p2_s2.json)
+    through rs_sort_u32 with a comm on two in-process ranks: literal splitters,
+    count matrix and Y_j."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "ger_gvr_hand_trace_p2_s2.json")))
+    for mode in ("ger", "gvr"):
+        got = rs.sort_ranks([dev(np.array(b, dtype=np.uint32)) for b in g["blocks"]], mode, s=g["s"], seed=g["seed"])
+        assert got["splitters"].tolist() == g[mode]["splitters"], mode
+        assert got["counts"].tolist() == g[mode]["counts"], mode
+        assert [host(y, np.uint32).tolist() for y in got["Y"]] == g[mode]["Y"], mode
+
+
 @pytest.mark.parametrize("b", [8, 16])
 def test_gsd_pairs_global_stability(b):
     p, N = 4, 30000

@@ -189,3 +189,24 @@ def test_gvr_sampling_lemma_bound_over_seeds():
     blocks = [a[k * n // p:(k + 1) * n // p] for k in range(p)]
     worst = max(int(oracle.gvr(blocks, s=s, seed=seed)["Ylen"].max()) - s for seed in range(40))
     assert worst <= bound, (worst, bound)
+
+
+def test_hand_trace_ger_gvr_p2_s2():
+    """GER and GVR traces derived by hand (tests/golden/ger_gvr_hand_trace_p2_s2.json)
+    from the PUBLISHED SplitMix64 outputs for seed 1234567: the draw positions, the
+    composite sample, the splitter with its rank and position, the cuts / destinations,
+    and Y_j — an outside pin of readings R28-R30 (a draw taken from the wrong block
+    order, position formula or composite tie rule changes the splitter or the counts)."""
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "ger_gvr_hand_trace_p2_s2.json")))
+    ref = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "splitmix64_seed1234567.json")))
+    for i, q in enumerate(g["draw_positions"]):  # floor(z_i * n / 2^64) of the published vector
+        assert int(ref["outputs"][i]) * g["n"] >> 64 == q
+        assert oracle.splitmix64_at(g["seed"], i) == int(ref["outputs"][i])
+    blocks = [np.array(b, dtype=np.uint32) for b in g["blocks"]]
+    for mode in ("ger", "gvr"):
+        res = getattr(oracle, mode)(blocks, s=g["s"], seed=g["seed"])
+        assert res["splitters"].tolist() == g[mode]["splitters"], mode
+        assert res["counts"].tolist() == g[mode]["counts"], mode
+        assert [y.tolist() for y in res["Y"]] == g[mode]["Y"], mode
