@@ -396,7 +396,11 @@ struct Layout16 {
 
 static Layout16 layout16(void* ws, int key_bytes, bool has_val, size_t n) {
     Layout16 L{};
+#ifdef RS_R16_G
+    L.G = std::min<size_t>((size_t)RS_R16_G, (size_t)sm_count());  // bounded-frontier experiment
+#else
     L.G = (size_t)sm_count();
+#endif
     L.part = (n + L.G - 1) / L.G;
     L.part = std::max<size_t>(1, (L.part + kS16Chunk - 1) / kS16Chunk * kS16Chunk);
     L.G = std::max<size_t>(1, (n + L.part - 1) / L.part);
