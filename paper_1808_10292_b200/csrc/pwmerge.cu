@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(kPwT) k_pw_merge(PwRuns R, const uint32_t* __r
     }
     __syncthreads();
     const int E = (int)s_seg[p];
-    RS_DCHECK(pw_pad(E) <= cap);
+    RS_DCHECK(pw_pad(E) < cap);  // (the merge reads one slot past the last element)
     // stage the pieces: warp w copies pieces w, w + 8, ...; each lane keeps SB
     // independent (remote) loads in flight before writing shared memory
     {
@@ -231,17 +231,18 @@ __global__ void __launch_bounds__(kPwT) k_pw_merge(PwRuns R, const uint32_t* __r
                     if (src[pw_pad(a0 + mid)] <= src[pw_pad(a1 + diag - 1 - mid)]) lo = mid + 1;
                     else hi = mid;
                 }
-                int ia = lo, ib = diag - lo;
-                K ha = ia < la ? src[pw_pad(a0 + ia)] : K(0), hb = ib < lb ? src[pw_pad(a1 + ib)] : K(0);
+                // absolute positions; a head past its run's end is read (the tile has one
+                // slot of slack past E) but never selected
+                int pa = a0 + lo, pb = a1 + diag - lo;
+                K ha = src[pw_pad(pa)], hb = src[pw_pad(pb)];
                 for (; o < stop; ++o) {  // branchless: select, advance, reload the consumed head
-                    const bool takeA = ib >= lb || (ia < la && ha <= hb);
-                    const int from = takeA ? a0 + ia : a1 + ib;
+                    const bool takeA = pb >= b1 || (pa < a1 && ha <= hb);
+                    const int from = takeA ? pa : pb;
                     dst[pw_pad(o)] = takeA ? ha : hb;
                     if (V) vdst[pw_pad(o)] = vsrc[pw_pad(from)];
-                    ia += takeA;
-                    ib += !takeA;
-                    const bool more = takeA ? ia < la : ib < lb;
-                    const K nv = more ? src[pw_pad(from + 1)] : K(0);
+                    const K nv = src[pw_pad(from + 1)];
+                    pa += takeA;
+                    pb += !takeA;
                     ha = takeA ? nv : ha;
                     hb = takeA ? hb : nv;
                 }
