@@ -27,7 +27,7 @@ def q(prefix):
 
 
 def run(log2n, kind="u32", b=8, dist="uniform", reps=5):
-    n = 1 << log2n
+    n = 1 << log2n if isinstance(log2n, int) else int(log2n[1:])  # "n133365760": an explicit size
     if kind == "u32":
         a = inputs.gen_u32(n, 4, dist)
         src = torch.from_numpy(a.view(np.int32)).cuda()
@@ -70,7 +70,7 @@ def run(log2n, kind="u32", b=8, dist="uniform", reps=5):
     per_key = {("u32", 8): 36, ("u32", 16): 20, ("u64", 8): 72, ("pairs", 8): 200, ("u64", 16): 40,
                ("pairs", 16): 104}[(kind, b)]
     gk = n / t / 1e6
-    print(f"{kind} b={b} {dist} n=2^{log2n}: {t:.3f} ms  {gk:.1f} Gkeys/s  "
+    print(f"{kind} b={b} {dist} n={n}: {t:.3f} ms  {gk:.1f} Gkeys/s  "
           f"{per_key * n / t / 1e6:.0f} GB/s ({per_key * n / t / 1e6 / PEAK * 100:.1f}% of {PEAK})")
     for name in ["hist", "plan", "onesweep", "final_copy", "r16_count", "r16_total", "r16_scan", "r16_offsets",
                  "r16_scatter"]:
@@ -91,7 +91,7 @@ if __name__ == "__main__":
     cfgs = sys.argv[1:] or ["20", "24", "27", "30"]
     for c in cfgs:
         parts = c.split(":")
-        log2n = int(parts[0])
+        log2n = int(parts[0]) if not parts[0].startswith("n") else parts[0]
         kind = parts[1] if len(parts) > 1 else "u32"
         b = int(parts[2]) if len(parts) > 2 else 8
         dist = parts[3] if len(parts) > 3 else "uniform"
