@@ -26,6 +26,7 @@ rs_status_t check_common(int key_bytes, const void* keys, const void* vals, bool
 rs_status_t sort_entry(int key_bytes, void* keys, uint32_t* vals, bool want_vals, size_t n, int b, void* comm,
                        void* out, uint32_t* vout, size_t out_cap, size_t* n_out, void* ws, size_t ws_bytes,
                        void* stream) {
+    NvtxRange nr(comm ? "rsort.sort.collective" : "rsort.sort");
     rs_status_t s = check_common(key_bytes, keys, vals, want_vals, n, b, out, vout);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     // collective: a rank whose arguments fail still takes part in the header

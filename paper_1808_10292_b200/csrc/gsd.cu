@@ -683,9 +683,13 @@ static rs_status_t gsd_regular(Comm* c, const CallArgs& a, const std::string& lo
     const size_t N = valid ? a.n : 0;  // an invalid rank takes part with an empty block
     rs_status_t sst = RS_OK;
     // step 1: local sort in place -> X_k
-    if (N && (sst = local_sort(kb, a.keys, a.vals, N, a.b, kb * 8, a.keys, a.vals, L.local_ws, L.local_ws_bytes,
-                               st)) != RS_OK)
-        return sst;
+    {
+        NvtxRange nr("rsort.gsd.local_sort");
+        if (N && (sst = local_sort(kb, a.keys, a.vals, N, a.b, kb * 8, a.keys, a.vals, L.local_ws, L.local_ws_bytes,
+                                   st)) != RS_OK)
+            return sst;
+    }
+    NvtxRange nr_split("rsort.gsd.sample_split_sync");
     // step 2: sample into this rank's record; C1 all-gather of the records
     if ((sst = launch_sample(kb, a.keys, N, rank, s, reinterpret_cast<Comp*>(samp_send + 128), st)) != RS_OK) return sst;
     if ((sst = c->tr->allgather(samp_send, samp_all, Bs, st)) != RS_OK) return sst;
@@ -724,6 +728,7 @@ static rs_status_t gsd_regular(Comm* c, const CallArgs& a, const std::string& lo
                                           " keys > out_cap " + std::to_string(caps[j]));
     }
     uint64_t total = 0;
+    NvtxRange nr_x("rsort.gsd.exchange_merge");
     sst = exchange_and_merge(c, a, L, a.keys, a.vals, in_cnt, R.wc, false, &total, st);
     if (sst != RS_OK) return sst;
     if (n_out) *n_out = total;

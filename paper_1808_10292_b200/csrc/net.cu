@@ -112,6 +112,7 @@ static rs_status_t merge_split_half(int key_bytes, size_t N, int self, int partn
 // out_cap >= n, workspaces sized, BTN p a power of 2)
 rs_status_t net_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, bool hv, size_t n, int b, void* out,
                      uint32_t* vout, size_t* n_out, void* ws, cudaStream_t st) {
+    NvtxRange nr(c->sampling == 4 ? "rsort.btn" : "rsort.oet");
     const int p = c->nranks, rank = c->rank;
     if (n_out) *n_out = n;
     if (p == 1 || n == 0) {

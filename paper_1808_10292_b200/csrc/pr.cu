@@ -138,6 +138,7 @@ size_t pr_ws_bytes(int key_bytes, bool hv, size_t n_local_max, int p) {
 // every peer's S block (agreed collectively, else RS_ECUDA on every rank)
 rs_status_t pr_sort(Comm* c, int key_bytes, void* keys, uint32_t* vals, bool hv, size_t n, void* out, uint32_t* vout,
                     size_t* n_out, void* ws, const std::vector<uint64_t>& n_all, cudaStream_t st) {
+    NvtxRange nr("rsort.pr4_across_gpus");
     const int p = c->nranks, rank = c->rank;
     const PrLayout L = pr_layout(ws, key_bytes, hv, n, p);
     const int P = key_bytes;  // radix-256 rounds

@@ -390,6 +390,7 @@ rs_status_t local_sort(int key_bytes, const void* keys_in, const uint32_t* vals_
                        int end_bit, void* out, uint32_t* vout, void* ws, size_t ws_bytes,
                        cudaStream_t st) {
     if (n == 0) return RS_OK;
+    NvtxRange nr(b == 8 ? "rsort.radix256" : "rsort.radix65536");
     rs_status_t s = local_sort_impl(key_bytes, keys_in, vals_in, n, b, end_bit, out, vout, ws, ws_bytes, st);
     if (s == RS_OK && options().self_check) s = self_check(key_bytes, out, n, end_bit, ws, st);
     return s;

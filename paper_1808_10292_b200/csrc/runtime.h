@@ -8,6 +8,8 @@
 #include <cstdint>
 #include <string>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/rsort.h"
 #include "../../include/rsort_dev.h"
 
@@ -36,6 +38,15 @@ struct LaunchScope {
 };
 
 int sm_count();
+
+// NVTX range over a host-side phase of a call (header-only NVTX 3: a no-op unless a
+// profiler injects itself), e.g. "rsort.gsd.exchange"
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // process-wide test / tuning knobs (include/rsort_dev.h rs_dev_set_option); read
 // once per call, written only between calls
