@@ -86,16 +86,20 @@ __global__ void k_pw_pos(PwRuns R, const uint32_t* __restrict__ smv, uint64_t M,
     }
 }
 
-// cnt[i * p + k] for boundaries i = 1 .. nch-1 (rows 0 and nch are set by the host)
+// cnt[i * p + k] for boundaries i = 0 .. nch (row 0: nothing, row nch: the whole run)
 template <typename K>
 __global__ void k_pw_bounds(PwRuns R, const K* __restrict__ smk, const uint32_t* __restrict__ smv,
                             const uint32_t* __restrict__ pos, uint64_t nch, uint32_t* __restrict__ cnt) {
     const int p = R.p;
-    const uint64_t total = (nch - 1) * (uint64_t)p;
+    const uint64_t total = (nch + 1) * (uint64_t)p;
     for (uint64_t x = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; x < total;
          x += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t i = x / p + 1;
+        const uint64_t i = x / p;
         const int k = (int)(x % p);
+        if (i == 0 || i == nch) {
+            cnt[x] = i == 0 ? 0u : (uint32_t)R.len[k];
+            continue;
+        }
         const uint64_t bj = i * R.c - 1;  // boundary b_i = Sm[bj]
         const K bv = smk[bj];
         const int bk = (int)(smv[bj] >> 24);
@@ -315,17 +319,9 @@ rs_status_t pway(const PwRuns& R, uint64_t M, void* scratch, K* out, uint32_t* v
         LaunchScope ls("pw_pos", st);
         k_pw_pos<<<g, 256, 0, st>>>(R, L.mv, M, L.pos);
     }
-    // rows 0 and nch of the count table
-    std::vector<uint32_t> edge(2 * (size_t)p);
-    for (int k = 0; k < p; ++k) {
-        edge[k] = 0;
-        edge[p + k] = (uint32_t)R.len[k];
-    }
-    RS_CUDA_TRY(cudaMemcpyAsync(L.cnt, edge.data(), p * 4, cudaMemcpyHostToDevice, st));
-    RS_CUDA_TRY(cudaMemcpyAsync(L.cnt + nch * p, edge.data() + p, p * 4, cudaMemcpyHostToDevice, st));
-    if (nch > 1) {
+    {
         LaunchScope ls("pw_bounds", st);
-        const unsigned gb = (unsigned)std::min<uint64_t>(((nch - 1) * p + 255) / 256, 65535);
+        const unsigned gb = (unsigned)std::min<uint64_t>(((nch + 1) * p + 255) / 256, 65535);
         k_pw_bounds<K><<<gb, 256, 0, st>>>(R, static_cast<const K*>(L.mk), L.mv, L.pos, nch, L.cnt);
     }
     const int cap = pw_cap_padded(p, R.c);
@@ -339,7 +335,7 @@ rs_status_t pway(const PwRuns& R, uint64_t M, void* scratch, K* out, uint32_t* v
         LaunchScope ls("pw_merge", st);
         k_pw_merge<K, V><<<(unsigned)nch, kPwT, smem, st>>>(R, L.cnt, cap, out, vout);
     }
-    RS_CUDA_TRY(cudaGetLastError());  // (pageable H2D copies are staged before they return)
+    RS_CUDA_TRY(cudaGetLastError());
     return RS_OK;
 }
 
