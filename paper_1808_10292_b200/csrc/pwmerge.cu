@@ -18,7 +18,11 @@
 //   4 k_pw_merge   one CTA per chunk: its p pieces [cnt[i−1][k], cnt[i][k]) are
 //                  staged in shared memory, merged there by a ⌈log2 p⌉-level tree
 //                  of merge-path merges (left = lower runs: ties stay stable), and
-//                  stored coalesced at Σ_k cnt[i−1][k].
+//                  stored coalesced at Σ_k cnt[i−1][k].  Per level every merged
+//                  pair gets its own IT-output thread slots: warps 0-6 merge the
+//                  regular slots forwards (one search, IT unrolled unchecked
+//                  steps), warp 7 the last kPwSpecial slots of every pair
+//                  backwards from their end co-rank (where a run runs out).
 // A chunk holds at most c·m + p·(m − 1) elements (each run contributes its
 // bracketed samples plus less than one block), so the shared-memory tile is fixed.
 #include <algorithm>
@@ -37,16 +41,22 @@ namespace {
 #define RS_PW_C 0  // 0: 32 samples per chunk for 4-byte keys without values, else 16
 #endif
 #ifndef RS_PW_IT
-// outputs per thread per merge round; odd, so neighbouring threads' merge-path
-// positions fall in different banks without padding (u32 at 2^31, p = 8,
-// k_pw_merge ms: padded 16 -> 1.68, unpadded 16 / 15 / 17 / 19 / 23 -> 2.41 /
-// 1.48 / 1.37 / 1.34 / 1.38)
-#define RS_PW_IT 19
+// outputs per thread slot; odd, so neighbouring threads' merge-path positions fall
+// in different banks.  k_pw_merge at 2^28 outputs, p = 8, ncu-serialised us
+// (scripts/gpu_pw_ab.sh): round-1 tree (IT 19, slots straddling pairs) 1169;
+// per-pair slots + unrolled unchecked steps + backwards special slots, IT/special
+// 19/2 1174, 19/3 1121, 21/3 1106, 23/3 1097, 23/4 1100, 25/3 1106, 27/2 1174
+#define RS_PW_IT 23
 #endif
 constexpr int kPwM = RS_PW_M;  // sample stride m
 constexpr int kPwCMax = 32;     // samples per chunk c (PwRuns::c) at most
 constexpr int kPwMaxP = 32;   // runs handled by the single-pass merge (shared-memory tile)
 constexpr int kPwT = 256;     // threads per merge CTA
+constexpr int kPwLevels = 5;  // ⌈log2 kPwMaxP⌉
+#ifndef RS_PW_SPECIAL
+#define RS_PW_SPECIAL 3
+#endif
+constexpr int kPwSpecial = RS_PW_SPECIAL;  // slots per merged pair merged backwards from its end
 
 struct PwRuns {
     const void* k[kPwMaxP];
@@ -126,10 +136,18 @@ __global__ void k_pw_bounds(PwRuns R, const K* __restrict__ smk, const uint32_t*
     }
 }
 
-#ifndef RS_PW_PAD
-#define RS_PW_PAD 0  // 1: one pad word per 32 in the shared tiles
-#endif
-__device__ __forceinline__ int pw_pad(int i) { return RS_PW_PAD ? i + (i >> 5) : i; }
+template <typename K>
+__device__ __forceinline__ K lds(uint32_t addr) {  // a shared-memory load from a shared address
+    if (sizeof(K) == 4) {
+        uint32_t x;
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(addr));
+        return (K)x;
+    } else {
+        unsigned long long x;
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(x) : "r"(addr));
+        return (K)x;
+    }
+}
 
 template <typename K, bool V>
 __global__ void __launch_bounds__(kPwT) k_pw_merge(PwRuns R, const uint32_t* __restrict__ cnt, int cap,
@@ -140,6 +158,8 @@ __global__ void __launch_bounds__(kPwT) k_pw_merge(PwRuns R, const uint32_t* __r
     uint32_t* XV = reinterpret_cast<uint32_t*>(Y + cap);
     uint32_t* YV = XV + (V ? cap : 0);
     __shared__ uint32_t s_seg[kPwMaxP + 1];  // piece offsets in the chunk
+    __shared__ uint32_t s_reg[kPwLevels][kPwMaxP / 2 + 1];  // prefix of regular slots per pair
+    __shared__ uint32_t s_spc[kPwLevels][kPwMaxP / 2 + 1];  // prefix of special slots per pair
     __shared__ uint32_t s_src[kPwMaxP];      // piece start in its run
     __shared__ uint64_t s_o;
     __shared__ const void* s_rk[kPwMaxP];
@@ -169,10 +189,36 @@ __global__ void __launch_bounds__(kPwT) k_pw_merge(PwRuns R, const uint32_t* __r
         }
         if (tid == p - 1) s_seg[p] = incl;
         if (tid == 0) s_o = o;
+        // thread-slot tables of every merge level: pair q of level L (stride 2^L)
+        // has ⌈len/IT⌉ slots; its last kPwSpecial are "special" (near the runs'
+        // ends, merged backwards) and numbered after all regular ones, so they
+        // share one or two warps and their code path diverges only there
+        const uint32_t excl = incl - len, total = __shfl_sync(0xffffffffu, incl, 31);
+        for (int L = 0, st = 1; st < p; ++L, st *= 2) {
+            const int npair = ((p + st - 1) / st + 1) / 2;
+            const int ia = min(2 * tid * st, p), ib = min((2 * tid + 2) * st, p);
+            const uint32_t qa = __shfl_sync(0xffffffffu, excl, ia & 31), qb = __shfl_sync(0xffffffffu, excl, ib & 31);
+            const uint32_t va = ia >= 32 ? total : qa, vb = ib >= 32 ? total : qb;
+            const uint32_t ns = tid < npair ? (vb - va + RS_PW_IT - 1) / RS_PW_IT : 0u;
+            uint32_t sp = min(ns, (uint32_t)kPwSpecial), rg = ns - sp;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, rg, d), z = __shfl_up_sync(0xffffffffu, sp, d);
+                if (tid >= d) {
+                    rg += y;
+                    sp += z;
+                }
+            }
+            if (tid < npair) {
+                s_reg[L][tid + 1] = rg;
+                s_spc[L][tid + 1] = sp;
+            }
+            if (tid == 0) s_reg[L][0] = s_spc[L][0] = 0;
+        }
     }
     __syncthreads();
     const int E = (int)s_seg[p];
-    RS_DCHECK(pw_pad(E) < cap);  // (the merge reads one slot past the last element)
+    RS_DCHECK(E < cap);  // (the merge reads one slot past the last element)
     // stage the pieces: warp w copies pieces w, w + 8, ...; each lane keeps SB
     // independent (remote) loads in flight before writing shared memory
     {
@@ -197,8 +243,8 @@ __global__ void __launch_bounds__(kPwT) k_pw_merge(PwRuns R, const uint32_t* __r
                 for (int j = 0; j < SB; ++j) {
                     const int e = b + j * 32 + lane;
                     if (e < len) {
-                        X[pw_pad(s0 + e)] = r[j];
-                        if (V) XV[pw_pad(s0 + e)] = rv[V ? j : 0];
+                        X[s0 + e] = r[j];
+                        if (V) XV[s0 + e] = rv[V ? j : 0];
                     }
                 }
             }
@@ -206,45 +252,112 @@ __global__ void __launch_bounds__(kPwT) k_pw_merge(PwRuns R, const uint32_t* __r
     }
     __syncthreads();
     // merge tree in shared memory: segments [seg[j], seg[j+1]) -> pairs -> ...
-    // (padded indices spread the merge-path reads over the banks; each thread
-    // merges IT consecutive outputs with both heads in registers)
+    // Each level gives every merged pair its own ⌈len/IT⌉ thread slots, so a
+    // thread's IT outputs never straddle two pairs: one merge-path search, then
+    // (unless a run ends inside the slot) IT unrolled steps without bound checks
+    // on shared addresses — compare, select, store, reload the consumed head.
     int nseg = p, stride = 1;  // current segment j covers pieces [j·stride, min((j+1)·stride, p))
     K* src = X;
     K* dst = Y;
     uint32_t* vsrc = XV;
     uint32_t* vdst = YV;
-    constexpr int IT = RS_PW_IT;  // outputs per thread per round
-    while (nseg > 1) {
-        for (int o0 = tid * IT; o0 < E; o0 += kPwT * IT) {
-            int o = o0;
-            const int oend = min(o0 + IT, E);
-            while (o < oend) {
-                // the merged pair holding output o: largest even segment index with start <= o
-                int pj = 0;
-                for (int j2 = 2; j2 < nseg; j2 += 2)
-                    if ((int)s_seg[j2 * stride] <= o) pj = j2;
-                const int a0 = (int)s_seg[pj * stride];
-                const int a1 = (int)s_seg[min((pj + 1) * stride, p)];
-                const int b1 = (int)s_seg[min((pj + 2) * stride, p)];
-                const int la = a1 - a0, lb = b1 - a1;
-                const int stop = min(oend, b1);
-                const int diag = o - a0;
-                int lo = diag > lb ? diag - lb : 0, hi = diag < la ? diag : la;
-                while (lo < hi) {
+    constexpr int IT = RS_PW_IT;  // outputs per thread slot
+    constexpr uint32_t KB = (uint32_t)sizeof(K);
+    for (int L = 0; nseg > 1; ++L) {
+        const int npair = (nseg + 1) >> 1;
+        const uint32_t sbase = smem_addr(src);
+        const int nreg = (int)s_reg[L][npair], nslot = nreg + (int)s_spc[L][npair];
+        // warps 0..6 take the regular slots, warp 7 the special ones
+        const bool special = tid >= kPwT - 32;
+        const int nmine = special ? nslot - nreg : nreg;
+        for (int u = special ? tid - (kPwT - 32) : tid; u < nmine; u += special ? 32 : kPwT - 32) {
+            const uint32_t* tab = special ? s_spc[L] : s_reg[L];
+            int q = 0;  // the pair owning slot u
+            while (q + 1 < npair && u >= (int)tab[q + 1]) ++q;
+            const int a0 = (int)s_seg[2 * q * stride];
+            const int a1 = (int)s_seg[min((2 * q + 1) * stride, p)];
+            const int b1 = (int)s_seg[min((2 * q + 2) * stride, p)];
+            const int slot = (u - (int)tab[q]) + (special ? (int)(s_reg[L][q + 1] - s_reg[L][q]) : 0);
+            const int o0 = a0 + slot * IT;
+            const int oend = min(o0 + IT, b1);
+            const int la = a1 - a0, lb = b1 - a1;
+            if (la == 0 || lb == 0) {  // an unpaired (or empty-sided) segment moves as it is
+                for (int o = o0; o < oend; ++o) {
+                    dst[o] = src[o];
+                    if (V) vdst[o] = vsrc[o];
+                }
+                continue;
+            }
+            // merge path: the co-rank (pa, pb) of output position d of the pair
+            auto corank = [&](int d, int& pa, int& pb) {
+                int lo = d > lb ? d - lb : 0, hi = d < la ? d : la;
+                const uint32_t sa = sbase + (uint32_t)a0 * KB, sb = sbase + (uint32_t)(a1 + d - 1) * KB;
+                while (lo < hi) {  // A[mid] at sa + mid·|K| against B[d − 1 − mid] at sb − mid·|K|
                     const int mid = (lo + hi) >> 1;
-                    if (src[pw_pad(a0 + mid)] <= src[pw_pad(a1 + diag - 1 - mid)]) lo = mid + 1;
+                    const uint32_t off = (uint32_t)mid * KB;
+                    if (lds<K>(sa + off) <= lds<K>(sb - off)) lo = mid + 1;
                     else hi = mid;
                 }
-                // absolute positions; a head past its run's end is read (the tile has one
-                // slot of slack past E) but never selected
-                int pa = a0 + lo, pb = a1 + diag - lo;
-                K ha = src[pw_pad(pa)], hb = src[pw_pad(pb)];
-                for (; o < stop; ++o) {  // branchless: select, advance, reload the consumed head
+                pa = a0 + lo;
+                pb = a1 + d - lo;
+            };
+            const int r = oend - o0;
+            int pa, pb;
+            if (special) {
+                // backwards from the slot's end co-rank (the pair's last slot: the runs'
+                // ends, an empty search): unchecked while r steps cannot pass either
+                // run's start; ties leave B first
+                corank(oend - a0, pa, pb);
+                if (pa - a0 > r && pb - a1 > r) {
+                    uint32_t sa = sbase + (uint32_t)(pa - 1) * KB, sb = sbase + (uint32_t)(pb - 1) * KB;
+                    K ha = lds<K>(sa), hb = lds<K>(sb);
+                    for (int o = oend - 1; o >= o0; --o) {
+                        const bool takeB = hb >= ha;
+                        const uint32_t from = takeB ? sb : sa;
+                        dst[o] = takeB ? hb : ha;
+                        if (V) vdst[o] = vsrc[(from - sbase) / KB];
+                        const uint32_t nxt = from - KB;
+                        const K nv = lds<K>(nxt);
+                        sb = takeB ? nxt : sb;
+                        sa = takeB ? sa : nxt;
+                        hb = takeB ? nv : hb;
+                        ha = takeB ? ha : nv;
+                    }
+                    continue;
+                }
+            }
+            corank(o0 - a0, pa, pb);
+            // absolute positions; a head past its run's end is read (the tile has one
+            // slot of slack past E) but never selected
+            K ha = src[pa], hb = src[pb];
+            if (r == IT && a1 - pa >= IT && b1 - pb >= IT) {  // no run ends inside the slot
+                uint32_t sa = sbase + (uint32_t)pa * KB, sb = sbase + (uint32_t)pb * KB;
+#pragma unroll
+                for (int k = 0; k < IT; ++k) {
+                    const bool takeA = ha <= hb;
+                    const uint32_t from = takeA ? sa : sb;
+                    dst[o0 + k] = takeA ? ha : hb;
+                    if (V) vdst[o0 + k] = vsrc[(from - sbase) / KB];
+                    const uint32_t nxt = from + KB;
+                    const K nv = lds<K>(nxt);
+                    sa = takeA ? nxt : sa;
+                    sb = takeA ? sb : nxt;
+                    ha = takeA ? nv : ha;
+                    hb = takeA ? hb : nv;
+                }
+            } else if (pa == a1 || pb == b1) {  // one run is spent: the other one's tail
+                const int sh = pa == a1 ? 0 : lb;  // B[o − a1 + a0 − la] = src[o]; A: src[o − lb]
+                for (int o = o0; o < oend; ++o) {
+                    dst[o] = src[o - sh];
+                    if (V) vdst[o] = vsrc[o - sh];
+                }
+            } else {
+                for (int o = o0; o < oend; ++o) {  // a run ends inside the slot: bound-checked
                     const bool takeA = pb >= b1 || (pa < a1 && ha <= hb);
                     const int from = takeA ? pa : pb;
-                    dst[pw_pad(o)] = takeA ? ha : hb;
-                    if (V) vdst[pw_pad(o)] = vsrc[pw_pad(from)];
-                    const K nv = src[pw_pad(from + 1)];
+                    dst[o] = takeA ? ha : hb;
+                    if (V) vdst[o] = vsrc[from];
+                    const K nv = src[from + 1];
                     pa += takeA;
                     pb += !takeA;
                     ha = takeA ? nv : ha;
@@ -265,13 +378,13 @@ __global__ void __launch_bounds__(kPwT) k_pw_merge(PwRuns R, const uint32_t* __r
     // coalesced store of the merged chunk
     const uint64_t o = s_o;
     for (int e = tid; e < E; e += kPwT) {
-        out[o + e] = src[pw_pad(e)];
-        if (V) vout[o + e] = vsrc[pw_pad(e)];
+        out[o + e] = src[e];
+        if (V) vout[o + e] = vsrc[e];
     }
 }
 
 constexpr int pw_cap(int p, int c) { return c * kPwM + p * kPwM; }
-constexpr int pw_cap_padded(int p, int c) { return pw_cap(p, c) + pw_cap(p, c) / 32 + 1; }
+constexpr int pw_cap_padded(int p, int c) { return pw_cap(p, c) + 1; }  // one slot of slack
 int pw_c(int key_bytes, bool hv) { return RS_PW_C ? RS_PW_C : (key_bytes == 4 && !hv ? 32 : 16); }
 
 struct PwLayout {
