@@ -317,6 +317,8 @@ def main():
                     help="single GPU e2e: device buffer sets pipelined on their own streams (H2D of later "
                          "steps overlaps the sort and D2H of earlier ones)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", action="store_true",
+                    help="single GPU: also time the sort replayed from a CUDA graph (rs.SortGraph)")
     ap.add_argument("--no-verify", action="store_true",
                     help="skip the device-side check of the output (profiling runs: keeps the launch list to the sort)")
     ap.add_argument("--sampling", default="gsd", choices=["gsd", "ger", "gvr", "pr4", "btn", "oet"],
@@ -416,14 +418,29 @@ def main():
         one_sort()
     barrier()
 
-    # ---- timed steps: inputs reset outside the timed region, each step bracketed
+    # ---- timed steps: inputs reset outside the timed region (between the step events).
+    # One GPU: the K steps issued back to back inside one barrier + synchronize bracket,
+    # each step's reset (input restore, L2 flush) before its start event, so the device
+    # does not idle on the host's per-call launch latency.  GSD (p > 1) synchronises
+    # the host once per call: each step bracketed on its own.  No per-kernel timing
+    # events here (they put a bubble at every kernel boundary); the kernel times for
+    # the roofline come from a second, separately timed set of K steps below.
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    step_ms = []
-    L.rs_timing_reset()
-    L.rs_timing_enable(1)
-    launches = 0
-    with ClockSampler(torch.cuda.current_device()) as clk:
-        for _ in range(args.steps):
+
+    def run_steps(k):
+        ms, nl = [], 0
+        if p == 1:
+            ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+            barrier()
+            c0 = L.rs_launch_count()
+            for a, z in ev:
+                reset()
+                a.record()
+                one_sort()
+                z.record()
+            barrier()
+            return [a.elapsed_time(z) for a, z in ev], L.rs_launch_count() - c0
+        for _ in range(k):
             reset()
             barrier()
             c0 = L.rs_launch_count()
@@ -431,9 +448,12 @@ def main():
             one_sort()
             e1.record()
             barrier()
-            launches += L.rs_launch_count() - c0
-            step_ms.append(e0.elapsed_time(e1))
-    L.rs_timing_enable(0)
+            nl += L.rs_launch_count() - c0
+            ms.append(e0.elapsed_time(e1))
+        return ms, nl
+
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        step_ms, launches = run_steps(args.steps)
     clocks = clk.summary()
 
     # ---- the last timed step's output, checked on the device against the pristine
@@ -443,6 +463,41 @@ def main():
     if not args.no_verify:
         verified, verify = verify_output(out, vout, comm, comm_n_out[0], pristine, vals_pristine, kind, p, n_total,
                                          dist, dev)
+    # ---- per-kernel device times (K3's average launch for the roofline, the exchange
+    # for nvlink_roofline): K more steps with an event pair around every launch
+    L.rs_timing_reset()
+    L.rs_timing_enable(1)
+    run_steps(args.steps)
+    L.rs_timing_enable(0)
+    # ---- optional (--graph, single GPU): the same sort captured once in a CUDA graph
+    # (rs.SortGraph) and replayed, same reset / flush / bracketing; its output is
+    # verified like the direct one's
+    graph = None
+    if args.graph and p == 1:
+        try:
+            reset()
+            sg = rs.SortGraph(work, vals_work, digit_bits=b)
+            g_ms = []
+            for _ in range(args.warmup):
+                reset()
+                sg.replay()
+            for _ in range(args.steps):
+                reset()
+                barrier()
+                e0.record()
+                sg.replay()
+                e1.record()
+                barrier()
+                g_ms.append(e0.elapsed_time(e1))
+            gms = sum(g_ms) / len(g_ms)
+            graph = {"value": round(n_total / (gms / 1e3) / 1e9, 4), "unit": "Gkeys/s", "ms_per_step": round(gms, 4),
+                     "kernels_per_replay": sg.launches,
+                     "note": "rs.SortGraph: the sort captured once in a CUDA graph, replayed per step"}
+            if not args.no_verify:
+                graph["verified"], graph["verify"] = verify_output(out, vout, comm, n, pristine, vals_pristine, kind,
+                                                                   p, n_total, dist, dev)
+        except Exception as e:  # reported, not fatal: the direct numbers stand
+            graph = {"error": f"{type(e).__name__}: {e}"}
     ms_q, cnt_q = ctypes.c_double(), ctypes.c_int()
     L.rs_timing_query(b"onesweep", ctypes.byref(ms_q), ctypes.byref(cnt_q))
     pass_ms = ms_q.value / max(cnt_q.value, 1)
@@ -590,8 +645,13 @@ def main():
                    if p > 1 else "single GPU",
                    "l2": ("L2 flushed before every step (2x L2 write)" if flush is not None
                           else "inputs larger than L2 (no flush)"), "l2_bytes": l2_bytes,
-                   "inputs": "resident in HBM, reset outside timed region"},
+                   "inputs": "resident in HBM, reset outside timed region",
+                   "timing": ("CUDA events around each sort; the K steps issued back to back inside one "
+                              "barrier + synchronize bracket, resets between the event pairs" if p == 1 else
+                              "CUDA events around each sort, each step bracketed by barrier + synchronize, "
+                              "max over ranks")},
         "verified": verified, "verify": verify,
+        **({"graph_replay": graph} if graph is not None else {}),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         **({"nvlink_roofline": xchg} if xchg else {}),
         "clocks": clocks, "kernel_ms_per_step": round(all_kernels_ms / args.steps, 4),

@@ -394,3 +394,32 @@ def test_cuda_graph_capture_and_replay():
         g.replay()
         torch.cuda.synchronize()
         assert (host(work, np.uint32) == want).all()
+
+
+def test_sort_graph_u32_and_pairs():
+    """rs.SortGraph: capture once, replay on new contents of the same buffers;
+    every replay matches the oracle (u32 at config 1's size, pairs ragged)."""
+    n = 1 << 20
+    g0 = None
+    for seed in (3, 4):
+        a = inputs.gen_u32(n, seed)
+        if g0 is None:
+            buf = dev(a)
+            g0 = rs.SortGraph(buf)
+            assert g0.launches >= 2
+        else:
+            buf.copy_(dev(a))
+            g0.replay()
+        torch.cuda.synchronize()
+        assert (host(buf, np.uint32) == oracle.sr(a, 8)).all(), seed
+    m = 3 * TILEP + 11
+    k1, k2 = inputs.gen_u64(m, 5), inputs.gen_u64(m, 6, "mod1024")
+    v = inputs.iota_u32(m)
+    tk, tv = dev(k1), dev(v)
+    gp = rs.SortGraph(tk, tv)
+    tk.copy_(dev(k2))
+    tv.copy_(dev(v))
+    gp.replay()
+    torch.cuda.synchronize()
+    wk, wv = oracle.sr(k2, 8, vals=v)
+    assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
