@@ -184,14 +184,19 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             }
         } else {
             uint32_t* wc = s_wc + warp * (WCW / W);
+#ifdef RS_AR_GP
+            constexpr int GK = HAS_VAL && KPT % RS_AR_GP == 0 ? RS_AR_GP : G;  // (tuning: pairs rank batch)
+#else
+            constexpr int GK = G;
+#endif
 #pragma unroll
-            for (int g = 0; g < KPT; g += G) {
-                K kk[G];
-                uint32_t rg[G];
+            for (int g = 0; g < KPT; g += GK) {
+                K kk[GK];
+                uint32_t rg[GK];
 #pragma unroll
-                for (int i = 0; i < G; ++i) kk[i] = (uint32_t)((g + i) * 32) < lim ? gk[(g + i) * 32] : ~K(0);
+                for (int i = 0; i < GK; ++i) kk[i] = (uint32_t)((g + i) * 32) < lim ? gk[(g + i) * 32] : ~K(0);
 #pragma unroll
-                for (int i = 0; i < G; ++i) {
+                for (int i = 0; i < GK; ++i) {
                     const uint32_t d = digit8<K>(kk[i], shift);
                     const uint32_t sh = (d & 1u) << 4;
                     if (R2A) {
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                 }
                 if (!R2A) {
 #pragma unroll
-                    for (int i = 0; i < G; i += 2) rr[R2A ? 0 : (g + i) / 2] = __byte_perm(rg[i], rg[i + 1], 0x5410);
+                    for (int i = 0; i < GK; i += 2) rr[R2A ? 0 : (g + i) / 2] = __byte_perm(rg[i], rg[i + 1], 0x5410);
                 }
             }
         }
@@ -247,8 +252,10 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             uint32_t* wcp = s_wc + warp * (WCW / W);
             const uint16_t* wc16 = s_wc16 + warp * R;
             const int ibase = warp * WK + lane;
-#ifdef RS_AR_GS
+#if defined(RS_AR_GS)
             constexpr int GS = LPC && KPT % RS_AR_GS == 0 ? RS_AR_GS : G;
+#elif defined(RS_AR_GSP)
+            constexpr int GS = HAS_VAL && KPT % RS_AR_GSP == 0 ? RS_AR_GSP : G;  // (tuning: pairs scatter batch)
 #else
             constexpr int GS = G;
 #endif

@@ -43,8 +43,17 @@ template <>
 struct TuneAr<uint32_t, false> : TuneT<RS_AR_U32_T, RS_AR_U32_KPT, RS_AR_U32_MINB> {};
 template <>
 struct TuneAr<uint64_t, false> : TuneT<256, 40, 2> {};
+#ifndef RS_AR_P_T
+#define RS_AR_P_T 256
+#endif
+#ifndef RS_AR_P_KPT
+#define RS_AR_P_KPT 24
+#endif
+#ifndef RS_AR_P_MINB
+#define RS_AR_P_MINB 2
+#endif
 template <>
-struct TuneAr<uint64_t, true> : TuneT<256, 24, 2> {};
+struct TuneAr<uint64_t, true> : TuneT<RS_AR_P_T, RS_AR_P_KPT, RS_AR_P_MINB> {};
 template <>
 struct TuneAr<uint32_t, true> : TuneT<256, 24, 2> {};
 // design 5 for small inputs (fewer than three large tiles per SM): smaller tiles
