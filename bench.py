@@ -196,6 +196,20 @@ def order_violations(keys, vals=None, chunk=1 << 26):
     return bad
 
 
+def rank_boundary_violations(edges):
+    """edges[j] = (first, last) key of Y_j as int64 bit patterns, or (None, None)
+    for an empty Y_j; counts ranks whose first key is below the last key of the
+    nearest nonempty rank before it, in unsigned order"""
+    bad, last = 0, None
+    for fe, le in edges:
+        if fe is None:
+            continue
+        if last is not None and (fe & ((1 << 64) - 1)) < last:
+            bad += 1
+        last = le & ((1 << 64) - 1)
+    return bad
+
+
 def verify_output(out, vout, comm, n_out, pristine, vals_pristine, kind, p, n_total, dist, dev):
     """the last timed step's output, checked on the device against the pristine
     input: nondecreasing (pairs: stable), same multiset (count + two SplitMix64
@@ -218,15 +232,7 @@ def verify_output(out, vout, comm, n_out, pristine, vals_pristine, kind, p, n_to
         viol = int(t[5])
         allg = [None] * p
         dist.all_gather_object(allg, edges)
-        last = None
-        for fe, le in allg:  # ranks in order; empty Y_j skipped
-            if fe is None:
-                continue
-            ufe = fe & ((1 << 64) - 1)
-            if last is not None and (ufe ^ (1 << 63) if kind == "pairs" else ufe) < last:
-                viol += 1
-            ule = le & ((1 << 64) - 1)
-            last = ule ^ (1 << 63) if kind == "pairs" else ule
+        viol += rank_boundary_violations(allg)
     verified = viol == 0 and h_in == h_out
     verify = {"method": "device: adjacent order" + (" + stability (value = global index)" if kind == "pairs" else "") +
                         (" + rank boundaries" if p > 1 else "") + "; multiset (count, two SplitMix64 sums) vs the "
