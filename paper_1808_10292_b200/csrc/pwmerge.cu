@@ -160,81 +160,80 @@ __global__ void __launch_bounds__(kPwT) k_pw_merge(PwRuns R, const uint32_t* __r
     __shared__ uint32_t s_seg[kPwMaxP + 1];  // piece offsets in the chunk
     __shared__ uint32_t s_reg[kPwLevels][kPwMaxP / 2 + 1];  // prefix of regular slots per pair
     __shared__ uint32_t s_spc[kPwLevels][kPwMaxP / 2 + 1];  // prefix of special slots per pair
-    __shared__ uint32_t s_src[kPwMaxP];      // piece start in its run
     __shared__ uint64_t s_o;
-    __shared__ const void* s_rk[kPwMaxP];
-    __shared__ const uint32_t* s_rv[kPwMaxP];
     const int p = R.p, tid = threadIdx.x;
     const uint64_t i = blockIdx.x;
-    // piece table: lanes k < p of warp 0 load their bounds in parallel, one warp scan
-    if (tid < 32) {
-        uint32_t c0 = 0, len = 0;
-        if (tid < p) {
-            c0 = cnt[i * p + tid];
-            len = cnt[(i + 1) * p + tid] - c0;
-        }
-        uint32_t incl = len;
+    // piece table: in EVERY warp, lanes k < p load their bounds (L2 hits) and one
+    // warp scan gives the pieces' offsets in the chunk, so each warp starts staging
+    // its pieces at once (no CTA barrier behind warp 0's global loads: that wait was
+    // 18 % of the kernel's stall samples); warp 0 also writes the tables the merge
+    // levels read after the staging barrier
+    const int warp = tid >> 5, lane = tid & 31;
+    uint32_t c0 = 0, len = 0;
+    if (lane < p) {
+        c0 = cnt[i * p + lane];
+        len = cnt[(i + 1) * p + lane] - c0;
+    }
+    uint32_t incl = len;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += y;
+    }
+    const uint32_t excl = incl - len, total = __shfl_sync(0xffffffffu, incl, 31);
+    const int E = (int)total;
+    RS_DCHECK(E < cap);  // (the merge reads one slot past the last element)
+    if (warp == 0) {
         uint64_t o = c0;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-            if (tid >= d) incl += y;
-            o += __shfl_xor_sync(0xffffffffu, o, d);
+        for (int d = 1; d < 32; d <<= 1) o += __shfl_xor_sync(0xffffffffu, o, d);
+        if (lane < p) s_seg[lane] = excl;
+        if (lane == 0) {
+            s_seg[p] = total;
+            s_o = o;
         }
-        if (tid < p) {
-            s_seg[tid] = incl - len;
-            s_src[tid] = c0;
-            s_rk[tid] = R.k[tid];
-            s_rv[tid] = R.v[tid];
-        }
-        if (tid == p - 1) s_seg[p] = incl;
-        if (tid == 0) s_o = o;
         // thread-slot tables of every merge level: pair q of level L (stride 2^L)
         // has ⌈len/IT⌉ slots; its last kPwSpecial are "special" (near the runs'
         // ends, merged backwards) and numbered after all regular ones, so they
         // share one or two warps and their code path diverges only there
-        const uint32_t excl = incl - len, total = __shfl_sync(0xffffffffu, incl, 31);
         for (int L = 0, st = 1; st < p; ++L, st *= 2) {
             const int npair = ((p + st - 1) / st + 1) / 2;
-            const int ia = min(2 * tid * st, p), ib = min((2 * tid + 2) * st, p);
+            const int ia = min(2 * lane * st, p), ib = min((2 * lane + 2) * st, p);
             const uint32_t qa = __shfl_sync(0xffffffffu, excl, ia & 31), qb = __shfl_sync(0xffffffffu, excl, ib & 31);
             const uint32_t va = ia >= 32 ? total : qa, vb = ib >= 32 ? total : qb;
-            const uint32_t ns = tid < npair ? (vb - va + RS_PW_IT - 1) / RS_PW_IT : 0u;
+            const uint32_t ns = lane < npair ? (vb - va + RS_PW_IT - 1) / RS_PW_IT : 0u;
             uint32_t sp = min(ns, (uint32_t)kPwSpecial), rg = ns - sp;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, rg, d), z = __shfl_up_sync(0xffffffffu, sp, d);
-                if (tid >= d) {
+                if (lane >= d) {
                     rg += y;
                     sp += z;
                 }
             }
-            if (tid < npair) {
-                s_reg[L][tid + 1] = rg;
-                s_spc[L][tid + 1] = sp;
+            if (lane < npair) {
+                s_reg[L][lane + 1] = rg;
+                s_spc[L][lane + 1] = sp;
             }
-            if (tid == 0) s_reg[L][0] = s_spc[L][0] = 0;
+            if (lane == 0) s_reg[L][0] = s_spc[L][0] = 0;
         }
     }
-    __syncthreads();
-    const int E = (int)s_seg[p];
-    RS_DCHECK(E < cap);  // (the merge reads one slot past the last element)
     // stage the pieces: warp w copies pieces w, w + 8, ...; each lane keeps SB
     // independent (remote) loads in flight before writing shared memory
     {
-        const int warp = tid >> 5, lane = tid & 31;
         constexpr int SB = 8;
         for (int k = warp; k < p; k += kPwT / 32) {
-            const int s0 = (int)s_seg[k], len = (int)s_seg[k + 1] - s0;
-            const K* src = static_cast<const K*>(s_rk[k]) + s_src[k];
-            const uint32_t* vs = V ? s_rv[k] + s_src[k] : nullptr;
-            for (int b = 0; b < len; b += 32 * SB) {
+            const int s0 = (int)__shfl_sync(0xffffffffu, excl, k), ln = (int)__shfl_sync(0xffffffffu, len, k);
+            const uint32_t off = __shfl_sync(0xffffffffu, c0, k);
+            const K* src = static_cast<const K*>(R.k[k]) + off;
+            const uint32_t* vs = V ? R.v[k] + off : nullptr;
+            for (int b = 0; b < ln; b += 32 * SB) {
                 K r[SB];
                 uint32_t rv[V ? SB : 1];
 #pragma unroll
                 for (int j = 0; j < SB; ++j) {
                     const int e = b + j * 32 + lane;
-                    if (e < len) {
+                    if (e < ln) {
                         r[j] = src[e];
                         if (V) rv[V ? j : 0] = vs[e];
                     }
@@ -242,7 +241,7 @@ __global__ void __launch_bounds__(kPwT) k_pw_merge(PwRuns R, const uint32_t* __r
 #pragma unroll
                 for (int j = 0; j < SB; ++j) {
                     const int e = b + j * 32 + lane;
-                    if (e < len) {
+                    if (e < ln) {
                         X[s0 + e] = r[j];
                         if (V) XV[s0 + e] = rv[V ? j : 0];
                     }
