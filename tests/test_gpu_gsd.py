@@ -293,6 +293,27 @@ def test_exchange_fallback_with_pull_merges(option, merge):
     _check([a[i * 40000:(i + 1) * 40000] for i in range(5)], r=8, b=8)
 
 
+@pytest.mark.parametrize("span", [1, 3, 6])
+def test_pway_merge_partially_overlapping_runs(option, span):
+    """p-way merge with runs that overlap only in part (block k holds keys in
+    [k·D, (k + span)·D)): inside a merged pair one run is spent long before the
+    pair ends, so the unchecked forward slots, the copy of the surviving run, the
+    bound-checked slots and the backwards pair-end slots all run; u32 keys against
+    the simulator, (u64, u32) pairs with many ties also stable."""
+    option("gsd_merge", 3)
+    p, N, D = 8, 50021, 1 << 26
+    base = inputs.gen_u32(p * N, 470 + span)
+    blocks = [(base[i * N:(i + 1) * N] % np.uint32(span * D)) + np.uint32(i * D) for i in range(p)]
+    _check(blocks, r=8, b=8)
+    k = inputs.gen_u64(p * N, 480 + span, "mod1024")
+    kb = [(k[i * N:(i + 1) * N] % np.uint64(64 * span)) + np.uint64(64 * i) for i in range(p)]
+    v = inputs.iota_u32(p * N)
+    got = _check(kb, r=8, b=8, vals_np=[v[i * N:(i + 1) * N] for i in range(p)])
+    K = np.concatenate([host(y, np.uint64) for y in got["Y"]])
+    V = np.concatenate([host(y, np.uint32) for y in got["Yv"]])
+    assert oracle.pairs_stable(K, V)
+
+
 def test_pway_merge_pairs_uneven_tiny_and_empty_blocks(option):
     """p-way merge: stable pairs over uneven blocks, including blocks shorter than
     one sample stride and empty ones (runs with no samples)."""
