@@ -210,23 +210,27 @@ static rs_status_t launch_probe(uint32_t seed, uint32_t* bad, cudaStream_t st) {
     return RS_OK;
 }
 
+static std::mutex g_probe_run_mu;  // one probe at a time: concurrent first callers wait for its verdict
+
 static rs_status_t rank_order_ok(Ctrl* ctrl, cudaStream_t st, bool* ok) {
     int dev = 0;
     RS_CUDA_TRY(cudaGetDevice(&dev));
-    {
+    auto cached = [&]() {
         std::lock_guard<std::mutex> lk(g_probe_mu);
         auto it = g_probe.find(dev);
-        if (it != g_probe.end()) {
-            *ok = it->second == 1;
-            return RS_OK;
-        }
-    }
+        if (it == g_probe.end()) return false;
+        *ok = it->second == 1;
+        return true;
+    };
+    if (cached()) return RS_OK;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     RS_CUDA_TRY(cudaStreamIsCapturing(st, &cs));
     if (cs != cudaStreamCaptureStatusNone) {
         *ok = false;
         return RS_OK;
     }
+    std::lock_guard<std::mutex> run(g_probe_run_mu);
+    if (cached()) return RS_OK;  // another thread probed this device meanwhile
     uint32_t* bad = reinterpret_cast<uint32_t*>(&ctrl->pad[0]);  // zeroed with the control block
     rs_status_t s = launch_probe<TuneAr<uint32_t, false>>(0x9E3779B9u, bad, st);
     if (s == RS_OK) s = launch_probe<TuneArSmall<uint32_t, false>>(0x7F4A7C15u, bad, st);
