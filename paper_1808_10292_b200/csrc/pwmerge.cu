@@ -140,11 +140,11 @@ template <typename K>
 __device__ __forceinline__ K lds(uint32_t addr) {  // a shared-memory load from a shared address
     if (sizeof(K) == 4) {
         uint32_t x;
-        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(addr));
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(x) : "r"(addr) : "memory");
         return (K)x;
     } else {
         unsigned long long x;
-        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(x) : "r"(addr));
+        asm volatile("ld.shared.u64 %0, [%1];" : "=l"(x) : "r"(addr) : "memory");
         return (K)x;
     }
 }
