@@ -71,6 +71,24 @@ struct OnesweepArCfg {
         !HAS_VAL && KPT % 8 == 0 && KPT <= 127 && (size_t)W * 2048 * 4 <= (size_t)TILE * sizeof(K);
 };
 
+#ifdef RS_AR_TRACE
+// (diagnostic build only) per tile: globaltimer at start, after [rank], after
+// [scatter], after [look-back], at the end of [store]; SM id
+__device__ unsigned long long g_rs_trace[1 << 17][6];
+__device__ __forceinline__ unsigned long long rs_gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define RS_TRACE(tile, k)                                                      \
+    do {                                                                        \
+        if (tid == 0 && (tile) < (1u << 17)) g_rs_trace[tile][k] = rs_gtime(); \
+    } while (0)
+#else
+#define RS_TRACE(tile, k) \
+    do {                  \
+    } while (0)
+#endif
 template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, int RANK2, int LB>
 __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
     using ST = Status<S>;
@@ -142,6 +160,14 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         // padding (digit 255, ranked after every real key)
         const K* gk = src + base + warp * WK + lane;
         const uint32_t lim = valid - min(valid, (uint32_t)(warp * WK + lane));
+        RS_TRACE(tile, 0);
+#ifdef RS_AR_TRACE
+        if (tid == 0 && tile < (1u << 17)) {
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            g_rs_trace[tile][5] = smid;
+        }
+#endif
 
         // ---- [rank]
         if (LPC) {
@@ -213,6 +239,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             }
         }
         __syncthreads();
+        RS_TRACE(tile, 1);
 
         // ---- [offset] thread d: tile count, in-tile offset, warp start offsets; publish
         if (tid < R) {
@@ -290,6 +317,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             }
         }
 
+        RS_TRACE(tile, 2);
         // ---- [look-back] one digit per thread, windowed walk over earlier tiles
         if (tid < R) {
             S excl = 0;
@@ -316,6 +344,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             s_gofs[tid] = a.bases[a.pass * R + tid] + (uint32_t)excl - s_texcl[tid];
         }
         __syncthreads();
+        RS_TRACE(tile, 3);
 
         // ---- [next] take the next tile and prefetch it; the counters are free
         if (tid == 0) {
@@ -391,6 +420,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             }
         }
         __syncthreads();
+        RS_TRACE(tile, 4);
         tile = s_misc[0];
     }
 }

@@ -441,3 +441,11 @@ rs_status_t digit_histogram(int key_bytes, const void* keys, size_t n, int b, ui
 }
 
 }  // namespace rs
+
+#ifdef RS_AR_TRACE
+// diagnostic builds only (RS_NVCC_DEFINES=-DRS_AR_TRACE): the per-tile phase
+// timestamps of the last radix-256 pass launches (scripts/trace_pass.py)
+extern "C" __attribute__((visibility("default"))) int rs_dev_trace_copy(void* host, size_t bytes) {
+    return cudaMemcpyFromSymbol(host, rs::g_rs_trace, bytes) == cudaSuccess ? 0 : 1;
+}
+#endif
