@@ -266,6 +266,26 @@ def test_config5_single_gpu_full_size():
     assert oracle.multiset_hash(gk, gv) == h_in
 
 
+@pytest.mark.slow
+def test_config5_single_gpu_full_memcmp():
+    """configs[4] at p = 1 compared element by element with the serial SR-8 oracle:
+    2^30 (u64 key, u32 index) pairs, all 8 passes, keys and payloads."""
+    n = 1 << 30
+    if free_host_gb() < 64 or free_dev_gb() < 30:
+        pytest.skip(f"needs ~64 GB host (have {free_host_gb():.0f})")
+    k = inputs.gen_u64(n, 5)
+    v = inputs.iota_u32(n)
+    tk, tv = dev(k), dev(v)
+    rs.sort_pairs(tk, tv, digit_bits=8)
+    gk, gv = host(tk, np.uint64), host(tv, np.uint32)
+    del tk, tv
+    torch.cuda.empty_cache()
+    wk, wv = oracle.sr(k, 8, vals=v)
+    del k, v
+    assert np.array_equal(gk, wk)
+    assert np.array_equal(gv, wv)
+
+
 def test_narrow_pairs_stability_at_scale():
     """configs[4] narrow-range variant: key = z mod 1024, many equal keys."""
     n = (1 << 22) + 5
