@@ -2,11 +2,12 @@
 ranks as threads on this GPU, each calling rs_sort_u32 / rs_sort_pairs_u64_u32
 with its comm (LocalGroup: the multi-GPU orchestration — local sort, sample,
 splitters, split, the one host sync, and the default one-pass p-way pull merge
-reading the peers' blocks in place — over the in-process transport).  Too large for the serial GSD simulator in a
-test: the concatenation Y_0‖…‖Y_7 is checked for order, for the input multiset
-(hash + count), for 64 sampled order statistics against the unsorted input, and
-every |Y_j| against the balance bound ⌊(1 + 1/r)·N⌋ + p (R18); pairs
-also for global stability (payload = global index)."""
+reading the peers' blocks in place — over the in-process transport).  Too large
+for the serial GSD simulator in a test: the concatenation Y_0‖…‖Y_7 is compared
+element by element with the serial SR-8 oracle's sort of the whole input (keys,
+and payloads for pairs), checked for order, multiset (hash + count) and 64 sampled
+order statistics, and every |Y_j| against the balance bound ⌊(1 + 1/r)·N⌋ + p
+(R18); pairs also for global stability (payload = global index)."""
 import numpy as np
 import pytest
 import torch
@@ -22,8 +23,8 @@ pytestmark = [pytest.mark.gpu, pytest.mark.slow]
 def test_config4_gsd_p8_full_size():
     n, p, r = 1 << 31, 8, 8
     N = n // p
-    if free_host_gb() < 40 or free_dev_gb() < 40:
-        pytest.skip("needs ~40 GB host/device")
+    if free_host_gb() < 48 or free_dev_gb() < 40:
+        pytest.skip("needs ~48 GB host, ~40 GB device")
     a = inputs.gen_u32(n, 4)
     h_in = oracle.multiset_hash(a)
     blocks = [torch.from_numpy(a[k * N:(k + 1) * N].view(np.int32)).cuda() for k in range(p)]
@@ -40,19 +41,19 @@ def test_config4_gsd_p8_full_size():
     assert oracle.multiset_hash(y) == h_in
     pos = np.unique(np.linspace(0, n - 1, 64).astype(np.uint64))
     assert oracle.check_order_stats_u32(a, pos, y[pos.astype(np.int64)]) == 0
+    assert np.array_equal(y, oracle.sr(a, 8))  # the serial oracle, element by element (~40 s)
 
 
 def test_config5_gsd_p8_full_size():
     n, p, r = 1 << 30, 8, 8
     N = n // p
-    if free_host_gb() < 60 or free_dev_gb() < 60:
-        pytest.skip("needs ~60 GB host/device")
+    if free_host_gb() < 80 or free_dev_gb() < 60:
+        pytest.skip("needs ~80 GB host, ~60 GB device")
     k = inputs.gen_u64(n, 5)
     v = inputs.iota_u32(n)
     h_in = oracle.multiset_hash(k, v)
     kb = [torch.from_numpy(k[i * N:(i + 1) * N].view(np.int64)).cuda() for i in range(p)]
     vb = [torch.from_numpy(v[i * N:(i + 1) * N].view(np.int32)).cuda() for i in range(p)]
-    del k, v
     got = rs.sort_ranks(kb, "gsd", r=r, digit_bits=8, vals=vb)
     del kb, vb
     yk = [host(t, np.uint64) for t in got["Y"]]
@@ -65,3 +66,6 @@ def test_config5_gsd_p8_full_size():
     assert gk.size == n
     assert oracle.pairs_stable(gk, gv)
     assert oracle.multiset_hash(gk, gv) == h_in
+    wk, wv = oracle.sr(k, 8, vals=v)  # the serial oracle, element by element
+    del k, v
+    assert np.array_equal(gk, wk) and np.array_equal(gv, wv)
