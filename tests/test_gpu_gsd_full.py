@@ -69,3 +69,27 @@ def test_config5_gsd_p8_full_size():
     wk, wv = oracle.sr(k, 8, vals=v)  # the serial oracle, element by element
     del k, v
     assert np.array_equal(gk, wk) and np.array_equal(gv, wv)
+
+
+def test_config4_every_collective_mode_p8_full_size():
+    """configs[3] at full size through every collective path at p = 8 — GER, GVR
+    (random oversampling), PR4 across ranks, BTN and OET — each concatenation
+    compared element by element with the serial oracle's sort (computed once)."""
+    n, p = 1 << 31, 8
+    N = n // p
+    if free_host_gb() < 48 or free_dev_gb() < 40:
+        pytest.skip("needs ~48 GB host, ~40 GB device")
+    a = inputs.gen_u32(n, 4)
+    want = oracle.sr(a, 8)
+    for mode in ("ger", "gvr", "pr4", "btn", "oet"):
+        blocks = [torch.from_numpy(a[k * N:(k + 1) * N].view(np.int32)).cuda() for k in range(p)]
+        got = rs.sort_ranks(blocks, mode, digit_bits=8, seed=11)
+        del blocks
+        ys = [host(y, np.uint32) for y in got["Y"]]
+        del got
+        torch.cuda.empty_cache()
+        y = np.concatenate(ys)
+        del ys
+        assert y.size == n, mode
+        assert np.array_equal(y, want), mode
+        del y
