@@ -94,10 +94,6 @@ rs_status_t rs_ipc_close_all(void);
  *                  and the call fails with RS_ECUDA on a violation (debug).
  *   "wide_status"  1 = 64-bit look-back status words at any n (tests that path).
  *   "small_tiles"  design-5 tiles: 0 auto, 1 always large, 2 always small.
- *   "chain"        design 5, every active pass in ONE launch whose tiles wait
- *                  on the previous pass's output regions instead of a kernel
- *                  boundary: 1 (default) on small inputs (the small-tile
- *                  regime), 0 never, 2 always.
  *   "gsd_merge"    GSD step 5 (all give the same Y_j): 3 = one p-way pass
  *                  (default), 2 = tree of 2-way merges, 1 = stable radix
  *                  re-sort (after an all-to-all), 0 = tree after an all-to-all.

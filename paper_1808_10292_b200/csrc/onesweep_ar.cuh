@@ -66,8 +66,6 @@ struct OnesweepArCfg {
     static constexpr size_t gofs_off = tcnt_off + R * 4;
     static constexpr size_t misc_off = gofs_off + R * 4;
     static constexpr size_t smem_bytes = misc_off + 64 * 4;
-    static constexpr size_t prun_off = smem_bytes;  // chained launch only: [2][2][256] runs of the last two tiles
-    static constexpr size_t smem_bytes_chain = prun_off + 4 * R * 4;
     // keys-only large tiles: lane-private count + keys in registers + cached offsets
     static constexpr bool kLpc =
         !HAS_VAL && KPT % 8 == 0 && KPT <= 127 && (size_t)W * 2048 * 4 <= (size_t)TILE * sizeof(K);
@@ -91,27 +89,7 @@ __device__ __forceinline__ unsigned long long rs_gtime() {
     do {                  \
     } while (0)
 #endif
-// CH (chained launch): every active pass of the sort in ONE launch.  Tile ids u
-// run over (active pass i, tile t) in pass order from one counter, so a CTA moves
-// on to the next pass's tiles while the last tiles of this pass are still in
-// flight, and the next pass starts on the regions of its input that are already
-// complete instead of after a kernel boundary.  Two device-side dependencies
-// replace the boundary:
-//   RAW  tile t of pass i reads region [t·TILE, (t+1)·TILE) of pass i-1's output:
-//        every tile of pass i-1 adds, per digit run it stored, the keys it wrote
-//        into each region it overlaps (region_done, after a fence); tile t waits
-//        until its region's count is its key count.  Most regions of a pass are
-//        complete long before the pass ends (only the ~256 regions holding a
-//        bucket's last keys need its last tiles).
-//   WAR  pass i writes the buffer pass i-1 reads: its stores wait until every tile
-//        of pass i-1 has read its keys (reads_done).
-// Every wait is on work of tiles with smaller u, all taken by running CTAs, so
-// the chain cannot deadlock.  The region counts of a tile are added by warp 0
-// during the next tile's [rank] (its stores are long acknowledged by then, the
-// fence is cheap), or at once when the CTA's next tile is in another pass.
-// Source loads bypass L1 (ld.global.cg): the SM's L1 may hold lines of an earlier
-// pass's read of the same buffer.
-template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, int RANK2, int LB, bool CH = false>
+template <typename K, bool HAS_VAL, int RT, int KPT, int MINB, typename S, int RANK2, int LB>
 __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
     using ST = Status<S>;
     using C = OnesweepArCfg<K, HAS_VAL, RT, KPT>;
@@ -129,169 +107,58 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
     uint32_t* s_tcnt = reinterpret_cast<uint32_t*>(smem + C::tcnt_off);
     uint32_t* s_gofs = reinterpret_cast<uint32_t*>(smem + C::gofs_off);
     uint32_t* s_misc = reinterpret_cast<uint32_t*>(smem + C::misc_off);
-    // chained: per digit, the global start and length of a tile's run, double-buffered
-    // by the CTA's tile count (s_misc[46]) so the last tile's runs survive this tile's
-    uint32_t* s_prun = reinterpret_cast<uint32_t*>(smem + C::prun_off);
-    // s_misc: [0] next tile id, [2] chained: the next tile must wait for its region,
-    // [8..15] warp sums of [offset], [31] number of active passes, [32..39] their
-    // indices; chained, the CTA's current pass: [40] active index i, [41] pass,
-    // [42] / [43] source / destination buffer selectors, [44] the last tile's region
-    // counts (its runs in s_prun) are still to be added,
-    // [45] (thread 0) pass i - 1 has read all its keys, [46] tiles this CTA finished.  Kept in shared memory and
-    // read where used, so none of it occupies registers next to the tile's keys.
-    volatile uint32_t* vs = s_misc;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     Ctrl* ctrl = a.ctrl;
-    const uint32_t Tn = a.num_tiles;
+    S* const status = static_cast<S*>(a.status_cur);
 
-    if (!CH) {
-        // clear the next pass's status rows (no reader in this launch)
-        for (size_t i = (size_t)blockIdx.x * THREADS + tid; i < (size_t)Tn * R; i += (size_t)gridDim.x * THREADS)
-            static_cast<S*>(a.status_next)[i] = 0;
-        if (!ctrl->active[a.pass]) return;
-    } else if (tid == 0) {
-        int k = 0;
-        for (int t = 0; t < a.P; ++t)
-            if (ctrl->active[t]) s_misc[32 + k++] = (uint32_t)t;
-        s_misc[31] = (uint32_t)k;
+    // clear the next pass's status rows (no reader in this launch)
+    for (size_t i = (size_t)blockIdx.x * THREADS + tid; i < (size_t)a.num_tiles * R; i += (size_t)gridDim.x * THREADS)
+        static_cast<S*>(a.status_next)[i] = 0;
+    if (!ctrl->active[a.pass]) return;
+
+    const int ss = ctrl->src_sel[a.pass], ds = ctrl->dst_sel[a.pass];
+    const K* src = pick<const K>(ss, static_cast<const K*>(a.keys_in), static_cast<const K*>(a.keys_out),
+                                 static_cast<const K*>(a.keys_alt));
+    K* dst = pick<K>(ds, const_cast<K*>(static_cast<const K*>(a.keys_in)), static_cast<K*>(a.keys_out),
+                     static_cast<K*>(a.keys_alt));
+    const uint32_t* vsrc = nullptr;
+    uint32_t* vdst = nullptr;
+    if (HAS_VAL) {
+        vsrc = pick<const uint32_t>(ss, a.vals_in, a.vals_out, a.vals_alt);
+        vdst = pick<uint32_t>(ds, const_cast<uint32_t*>(a.vals_in), a.vals_out, a.vals_alt);
     }
+    const int shift = a.shift;
 
-    // the pass being worked on: fixed by the arguments (one pass per launch), or
-    // chained, rebound (thread 0, then a CTA barrier) when the tile id enters another pass
-    const int ss0 = CH ? 0 : ctrl->src_sel[a.pass], ds0 = CH ? 0 : ctrl->dst_sel[a.pass];
-    auto sel_src = [&]() { return CH ? (int)vs[42] : ss0; };
-    auto sel_dst = [&]() { return CH ? (int)vs[43] : ds0; };
-    auto cur_ai = [&]() { return CH ? (int)vs[40] : 0; };
-    auto cur_pass = [&]() { return CH ? (int)vs[41] : a.pass; };
-    const K* const src0 = CH ? nullptr : pick<const K>(ss0, static_cast<const K*>(a.keys_in), static_cast<const K*>(a.keys_out),
-                                                       static_cast<const K*>(a.keys_alt));
-    K* const dst0 = CH ? nullptr : pick<K>(ds0, const_cast<K*>(static_cast<const K*>(a.keys_in)), static_cast<K*>(a.keys_out),
-                                           static_cast<K*>(a.keys_alt));
-    const uint32_t* const vsrc0 = CH || !HAS_VAL ? nullptr : pick<const uint32_t>(ss0, a.vals_in, a.vals_out, a.vals_alt);
-    uint32_t* const vdst0 = CH || !HAS_VAL ? nullptr : pick<uint32_t>(ds0, const_cast<uint32_t*>(a.vals_in), a.vals_out, a.vals_alt);
-    auto cur_src = [&]() {
-        return CH ? pick<const K>(sel_src(), static_cast<const K*>(a.keys_in), static_cast<const K*>(a.keys_out),
-                                  static_cast<const K*>(a.keys_alt))
-                  : src0;
-    };
-    auto cur_vsrc = [&]() { return CH ? pick<const uint32_t>(sel_src(), a.vals_in, a.vals_out, a.vals_alt) : vsrc0; };
-    auto cur_dst = [&]() {
-        return CH ? pick<K>(sel_dst(), const_cast<K*>(static_cast<const K*>(a.keys_in)), static_cast<K*>(a.keys_out),
-                            static_cast<K*>(a.keys_alt))
-                  : dst0;
-    };
-    auto cur_vdst = [&]() {
-        return CH ? pick<uint32_t>(sel_dst(), const_cast<uint32_t*>(a.vals_in), a.vals_out, a.vals_alt) : vdst0;
-    };
-    auto cur_status = [&]() {
-        return CH ? reinterpret_cast<S*>(static_cast<char*>(a.status_base) + (size_t)vs[40] * a.status_stride)
-                  : static_cast<S*>(a.status_cur);
-    };
-    auto bind = [&](uint32_t i) {  // chained, thread 0
-        const int p = (int)s_misc[32 + i];
-        vs[40] = i;
-        vs[41] = (uint32_t)p;
-        vs[42] = (uint32_t)ctrl->src_sel[p];
-        vs[43] = (uint32_t)ctrl->dst_sel[p];
-        vs[45] = 0;
-    };
-    auto ld_src = [&](const K* p) -> K { return CH ? __ldcg(p) : *p; };
-    auto valid_of = [&](uint32_t t) { return (uint32_t)min((size_t)TILE, (size_t)a.n - (size_t)t * TILE); };
-
-    auto prefetch = [&](uint32_t u) {  // thread 0 only: tile u into L2 by the TMA engine
-        uint32_t t = u;
-        const K* ps = cur_src();
-        const uint32_t* pv = HAS_VAL ? cur_vsrc() : nullptr;
-        if (CH) {
-            const uint32_t i = u / Tn;
-            t = u - i * Tn;
-            const int p = (int)s_misc[32 + i], ss = ctrl->src_sel[p];
-            ps = pick<const K>(ss, static_cast<const K*>(a.keys_in), static_cast<const K*>(a.keys_out),
-                               static_cast<const K*>(a.keys_alt));
-            if (HAS_VAL) pv = pick<const uint32_t>(ss, a.vals_in, a.vals_out, a.vals_alt);
-        }
+    auto prefetch = [&](uint32_t t) {  // thread 0 only: the tile into L2 by the TMA engine
         const size_t base = (size_t)t * TILE;
-        const uint32_t valid = valid_of(t);
+        const uint32_t valid = (uint32_t)min((size_t)TILE, (size_t)a.n - base);
         const uint32_t kbytes = (valid * (uint32_t)sizeof(K)) & ~15u;
-        if (kbytes) bulk_prefetch_l2(ps + base, kbytes);
+        if (kbytes) bulk_prefetch_l2(src + base, kbytes);
         const uint32_t vb = HAS_VAL ? ((valid * 4u) & ~15u) : 0u;
-        if (HAS_VAL && vb) bulk_prefetch_l2(pv + base, vb);
-    };
-    // chained, thread 0: the region count of tile u's input (u in pass i > 0), or
-    // "complete" for the first pass
-    auto region_count = [&](uint32_t u, bool acquire) -> uint32_t {
-        const uint32_t i = u / Tn;
-        if (i == 0) return 0xFFFFFFFFu;
-        const uint32_t* p = a.region_done + (size_t)(i - 1) * Tn + (u - i * Tn);
-        return acquire ? ld_acquire_gpu(p) : ld_relaxed_gpu(p);
-    };
-    // chained, warp 0: add the last tile's runs (s_prun) to the region counts
-    // of the current pass's output.  Runs after a CTA barrier that follows the tile's
-    // stores, at a point where warp 0 has no global access in flight (the fence is
-    // then cheap) and holds no keys: the end of the next tile's [scatter], or the
-    // pass change.
-    auto flush_runs = [&]() {
-        fence_acq_rel_gpu();  // the tile's stores, by every warp, before the counts
-        uint32_t* done = a.region_done + (size_t)cur_ai() * Tn;
-        const uint32_t* pr = s_prun + ((vs[46] & 1u) ^ 1u) * 2 * R;  // the last tile's buffer
-#pragma unroll 1
-        for (int d = lane; d < R; d += 32) {
-            const uint32_t len = pr[R + d];
-            if (!len) continue;
-            const uint32_t g0 = pr[d], g1 = g0 + len;
-            uint32_t r = g0 / (uint32_t)TILE;
-            uint64_t lo = (uint64_t)r * TILE;
-            while (true) {
-                const uint64_t hi = lo + TILE;
-                atomicAdd(done + r, (uint32_t)(min((uint64_t)g1, hi) - max((uint64_t)g0, lo)));
-                if ((uint64_t)g1 <= hi) break;
-                ++r;
-                lo = hi;
-            }
-        }
+        if (HAS_VAL && vb) bulk_prefetch_l2(vsrc + base, vb);
     };
 
-    uint32_t total = Tn;  // tile ids of this launch
     if (tid == 0) {
-        const uint32_t nu = atomicAdd(&ctrl->tile_ctr[CH ? 0 : a.pass], 1u);
-        s_misc[0] = nu;
-        s_misc[2] = 0;
-        if (CH) {
-            total = Tn * s_misc[31];
-            vs[44] = 0;
-            vs[46] = 0;
-            if (nu < total) bind(nu / Tn);
-        }
-        if (nu < total) {
-            prefetch(nu);
-            if (CH) s_misc[2] = region_count(nu, false) < valid_of(nu - (nu / Tn) * Tn) ? 1u : 0u;
-        }
+        const uint32_t t0 = atomicAdd(&ctrl->tile_ctr[a.pass], 1u);
+        s_misc[0] = t0;
+        if (t0 < a.num_tiles) prefetch(t0);
     }
     constexpr int WCW = W * R / 2;  // counter words
     for (int i = tid; i < WCW; i += THREADS) s_wc[i] = 0;
     __syncthreads();
-    total = CH ? Tn * s_misc[31] : Tn;  // tile ids over every pass of this launch
-    uint32_t u = s_misc[0];
-    if (CH && u < total && s_misc[2]) {
-        if (tid == 0)
-            while (region_count(u, true) < valid_of(u - (uint32_t)cur_ai() * Tn)) {
-            }
-        __syncthreads();
-    }
+    uint32_t tile = s_misc[0];
     // batches of G keys: G loads, then G atomics, so G shared-memory round trips overlap
     constexpr int G = KPT % 8 == 0 ? 8 : (KPT % 6 == 0 ? 6 : (KPT % 4 == 0 ? 4 : 2));
     uint32_t rr[R2A ? 1 : KPT / 2];  // pairs: stable ranks within the warp's keys of their digit, 16 bits each
     K kr[LPC ? KPT : 1];             // keys-only large tiles: this thread's keys of the tile
 
-    while (u < total) {
-        const uint32_t tile = CH ? u - (uint32_t)cur_ai() * Tn : u;  // tile index within the pass
-        const int shift = CH ? 8 * cur_pass() : a.shift;
+    while (tile < a.num_tiles) {
         const size_t base = (size_t)tile * TILE;
-        const uint32_t valid = valid_of(tile);
+        const uint32_t valid = (uint32_t)min((size_t)TILE, (size_t)a.n - base);
         // this thread's row-0 key; rows j*32 < lim are real, the rest are all-ones
         // padding (digit 255, ranked after every real key)
-        const K* gk = cur_src() + base + warp * WK + lane;
+        const K* gk = src + base + warp * WK + lane;
         const uint32_t lim = valid - min(valid, (uint32_t)(warp * WK + lane));
         RS_TRACE(tile, 0);
 #ifdef RS_AR_TRACE
@@ -316,7 +183,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             for (int g = 0; g < KPT; g += GR) {
 #pragma unroll
                 for (int i = 0; i < GR; ++i)
-                    kr[LPC ? g + i : 0] = (uint32_t)((g + i) * 32) < lim ? ld_src(gk + (g + i) * 32) : ~K(0);
+                    kr[LPC ? g + i : 0] = (uint32_t)((g + i) * 32) < lim ? gk[(g + i) * 32] : ~K(0);
 #pragma unroll
                 for (int i = 0; i < GR; ++i) {
                     const uint32_t d = digit8<K>(kr[LPC ? g + i : 0], shift);
@@ -353,7 +220,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                 K kk[GK];
                 uint32_t rg[GK];
 #pragma unroll
-                for (int i = 0; i < GK; ++i) kk[i] = (uint32_t)((g + i) * 32) < lim ? ld_src(gk + (g + i) * 32) : ~K(0);
+                for (int i = 0; i < GK; ++i) kk[i] = (uint32_t)((g + i) * 32) < lim ? gk[(g + i) * 32] : ~K(0);
 #pragma unroll
                 for (int i = 0; i < GK; ++i) {
                     const uint32_t d = digit8<K>(kk[i], shift);
@@ -371,7 +238,6 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                 }
             }
         }
-        // chained: the previous tile's region counts (warp 0; its stores are long done)
         __syncthreads();
         RS_TRACE(tile, 1);
 
@@ -393,7 +259,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
             if (lane == 31) s_misc[8 + warp] = incl;
             const uint32_t pub = tcnt - (tid == R - 1 ? (uint32_t)TILE - valid : 0u);  // drop padding
             s_tcnt[tid] = pub;
-            st_relaxed_gpu(cur_status() + (size_t)tile * R + tid, (tile == 0 ? ST::kFlagP : ST::kFlagA) | (S)pub);
+            st_relaxed_gpu(status + (size_t)tile * R + tid, (tile == 0 ? ST::kFlagP : ST::kFlagA) | (S)pub);
             named_barrier_sync(1, R);
             uint32_t pre = 0;
 #pragma unroll
@@ -427,7 +293,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
 #pragma unroll
                 for (int i = 0; i < GS; ++i)
                     kk[i] = LPC ? kr[LPC ? g + i : 0]
-                                : ((uint32_t)((g + i) * 32) < lim ? (CH ? __ldcg(gk + (g + i) * 32) : __ldcs(gk + (g + i) * 32)) : ~K(0));
+                                : ((uint32_t)((g + i) * 32) < lim ? __ldcs(gk + (g + i) * 32) : ~K(0));
 #pragma unroll
                 for (int i = 0; i < GS; ++i) {
                     const int j = g + i;
@@ -440,7 +306,7 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                         pos[i] = (uint32_t)wc16[d] + ((rw >> (16 * (j & 1))) & 0xFFFFu);
                     }
                     if (HAS_VAL)
-                        vv[HAS_VAL ? i : 0] = (uint32_t)(j * 32) < lim ? (CH ? __ldcg(cur_vsrc() + base + ibase + j * 32) : __ldcs(cur_vsrc() + base + ibase + j * 32)) : 0u;
+                        vv[HAS_VAL ? i : 0] = (uint32_t)(j * 32) < lim ? __ldcs(vsrc + base + ibase + j * 32) : 0u;
                 }
 #pragma unroll
                 for (int i = 0; i < GS; ++i) {
@@ -452,11 +318,9 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         }
 
         RS_TRACE(tile, 2);
-        if (CH && warp == 0 && vs[44]) flush_runs();  // the last tile's region counts
         // ---- [look-back] one digit per thread, windowed walk over earlier tiles
         if (tid < R) {
             S excl = 0;
-            S* const status = cur_status();
             if (tile != 0) {
                 const S* sp = status + (size_t)(tile - 1) * R + tid;
                 int64_t left = (int64_t)tile;
@@ -477,38 +341,16 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                 }
                 st_relaxed_gpu(status + (size_t)tile * R + tid, ST::kFlagP | (excl + (S)s_tcnt[tid]));
             }
-            const uint32_t g0 = a.bases[cur_pass() * R + tid] + (uint32_t)excl;  // the run's global start
-            s_gofs[tid] = g0 - s_texcl[tid];
-            if (CH) {  // this tile's run, for its region counts
-                uint32_t* pr = s_prun + (vs[46] & 1u) * 2 * R;
-                pr[tid] = g0;
-                pr[R + tid] = s_tcnt[tid];
-            }
-            // chained: this pass overwrites the previous pass's source only after all of it is read
-            if (CH && tid == 0 && cur_ai() > 0 && !vs[45]) {
-                while (ld_acquire_gpu(a.reads_done + cur_ai() - 1) < Tn) {
-                }
-                vs[45] = 1;
-            }
+            s_gofs[tid] = a.bases[a.pass * R + tid] + (uint32_t)excl - s_texcl[tid];
         }
         __syncthreads();
         RS_TRACE(tile, 3);
-        // chained: this tile has read its keys (the next pass may overwrite them), and its
-        // runs are in s_prun for region counts (added after its stores)
-        if (CH && tid == 0 && cur_ai() + 1 < (int)vs[31]) {
-            atomicAdd(a.reads_done + cur_ai(), 1u);
-            vs[44] = 1;
-        }
 
         // ---- [next] take the next tile and prefetch it; the counters are free
-        uint32_t nu = 0, rdv = 0;  // thread 0: the next tile id and (chained) its region count
         if (tid == 0) {
-            nu = atomicAdd(&ctrl->tile_ctr[CH ? 0 : a.pass], 1u);
-            s_misc[0] = nu;
-            if (nu < total) {
-                prefetch(nu);
-                if (CH) rdv = region_count(nu, false);  // consumed after [store]
-            }
+            const uint32_t nt = atomicAdd(&ctrl->tile_ctr[a.pass], 1u);
+            s_misc[0] = nt;
+            if (nt < a.num_tiles) prefetch(nt);
         }
         if (!LPC) {  // (the lane-private count rewrites every counter)
 #pragma unroll
@@ -519,8 +361,6 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
         // ---- [store] bucket runs leave as coalesced bursts (batches of 4 loads, 4
         // offset lookups, 4 stores: u32 2^27 pass 0.336 -> 0.326 ms against 8)
         constexpr int SG = KPT % 4 == 0 ? 4 : 2;
-        K* const dst = cur_dst();
-        uint32_t* const vdst = HAS_VAL ? cur_vdst() : nullptr;
         if (LPC && valid == (uint32_t)TILE) {
             const int sb = warp * WK + lane;     // warp w: slots [w·WK, (w+1)·WK)
             uint32_t cd = 0xFFFFFFFFu, cg = 0;  // cached digit and its bucket offset
@@ -579,33 +419,9 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
                 if (HAS_VAL) vdst[g] = s_vout[i];
             }
         }
-        if (CH && tid == 0) {
-            s_misc[2] = nu < total && rdv < valid_of(nu - (nu / Tn) * Tn) ? 1u : 0u;
-            vs[46] = vs[46] + 1u;
-        }
         __syncthreads();
         RS_TRACE(tile, 4);
-        u = s_misc[0];
-        if (CH) {
-            const bool change = u >= total || u / Tn != (uint32_t)cur_ai();
-            if (change) {
-                // the next tile may wait on this tile's counts: add them now
-                if (vs[44] && warp == 0) flush_runs();
-                __syncthreads();
-                if (u >= total) break;
-                if (tid == 0) {
-                    vs[44] = 0;
-                    bind(u / Tn);
-                }
-                __syncthreads();
-            }
-            if (s_misc[2]) {
-                if (tid == 0)
-                    while (region_count(u, true) < valid_of(u - (uint32_t)cur_ai() * Tn)) {
-                    }
-                __syncthreads();
-            }
-        }
+        tile = s_misc[0];
     }
 }
 

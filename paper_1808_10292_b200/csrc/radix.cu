@@ -117,10 +117,7 @@ struct Layout8 {
     Ctrl* ctrl;
     uint32_t* hist;
     uint32_t* bases;
-    void* status;  // [max(P, 2)][T][256] u32 or u64 words (one region per active pass when chained)
-    uint32_t* region_done;  // [P][T] chained: keys stored into each tile-sized region of a pass's output
-    uint32_t* reads_done;   // [kMaxPasses] chained: tiles of a pass that have read their keys
-    size_t zero_words;      // chained: status .. reads_done, zeroed by K1
+    void* status;  // [2][T][256] u32 or u64 words
     void* alt_keys;
     uint32_t* alt_vals;
     size_t T, status_bytes, bytes;
@@ -138,11 +135,7 @@ static Layout8 layout8(void* ws, int key_bytes, bool has_val, size_t n, size_t t
     L.ctrl = static_cast<Ctrl*>(c.take(sizeof(Ctrl)));
     L.hist = static_cast<uint32_t*>(c.take(P * 256 * 4));
     L.bases = static_cast<uint32_t*>(c.take(P * 256 * 4));
-    const int regions = std::max(P, 2);
-    L.status = c.take(regions * L.status_bytes);
-    L.region_done = static_cast<uint32_t*>(c.take(P * L.T * 4));
-    L.reads_done = static_cast<uint32_t*>(c.take(kMaxPasses * 4));
-    L.zero_words = (size_t)(reinterpret_cast<char*>(L.reads_done + kMaxPasses) - static_cast<char*>(L.status)) / 4;
+    L.status = c.take(2 * L.status_bytes);
     L.alt_keys = c.take(n * key_bytes);
     L.alt_vals = static_cast<uint32_t*>(has_val ? c.take(n * 4) : nullptr);
     L.bytes = c.used();
@@ -170,28 +163,6 @@ static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st) 
     LaunchScope ls("onesweep", st);
     kern<<<grid, C::THREADS, C::smem_bytes, st>>>(a);
     return RS_OK;
-}
-
-// every active pass in one launch (design 5, onesweep_ar.cuh CH)
-template <typename K, bool V, typename S, bool SMALL>
-static rs_status_t launch_chain_ar(const PassArgs& a, size_t T, cudaStream_t st) {
-    using TN = typename std::conditional<SMALL, TuneArSmall<K, V>, TuneAr<K, V>>::type;
-    using C = OnesweepArCfg<K, V, TN::THREADS, TN::KPT>;
-    auto kern = k_onesweep_ar<K, V, TN::THREADS, TN::KPT, TN::MINB, S, Rank2<V>::value, SMALL ? 8 : RS_AR_LB, true>;
-    int grid_cap = 0;
-    rs_status_t s = kernel_setup(reinterpret_cast<const void*>(kern), C::THREADS, C::smem_bytes_chain, &grid_cap);
-    if (s != RS_OK) return s;
-    const unsigned grid = (unsigned)std::min<size_t>(T * (size_t)a.P, (size_t)grid_cap);  // persistent CTAs
-    LaunchScope ls("onesweep_chain", st);
-    kern<<<grid, C::THREADS, C::smem_bytes_chain, st>>>(a);
-    return RS_OK;
-}
-
-template <typename K, bool V>
-static rs_status_t launch_chain(const PassArgs& a, size_t T, bool wide, cudaStream_t st) {
-    const bool small = small_input<K, V>(a.n);  // must match tile_keys()
-    if (wide) return small ? launch_chain_ar<K, V, uint64_t, true>(a, T, st) : launch_chain_ar<K, V, uint64_t, false>(a, T, st);
-    return small ? launch_chain_ar<K, V, uint32_t, true>(a, T, st) : launch_chain_ar<K, V, uint32_t, false>(a, T, st);
 }
 
 template <typename K, bool V, typename S>
@@ -331,17 +302,10 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
         if (!ar_ok) design = 2;
     }
     const Layout8 L = layout8(ws, sizeof(K), V, n, (size_t)tile_for(sizeof(K), V, design, n));
-    // every pass in one chained launch on small inputs, where a pass is a few tiles
-    // per CTA and the kernel boundaries dominate (2^20 u32: 0.119 -> 0.103 ms per
-    // sort); on large inputs the per-tile release fence of the region counts costs
-    // more than the boundaries it removes (2^31: 5.43 vs 4.50 ms per pass)
-    const int chain_opt = options().chain;
-    const bool chain = design == 5 && (chain_opt == 2 || (chain_opt == 1 && small_input<K, V>(n)));
     RS_CUDA_TRY(cudaMemsetAsync(L.hist, 0, (size_t)P * 256 * 4, st));
-    // K1 also zeroes the first pass's status region (as u32 words), or when chained
-    // every pass's status region and the region / reads-done counters
-    rs_status_t s = launch_hist<K>(keys_in, n, P, L.hist, static_cast<uint32_t*>(L.status),
-                                   chain ? L.zero_words : L.status_bytes / 4, st, first_pass);
+    // K1 also zeroes the first pass's status region (as u32 words)
+    rs_status_t s = launch_hist<K>(keys_in, n, P, L.hist, static_cast<uint32_t*>(L.status), L.status_bytes / 4, st,
+                                   first_pass);
     if (s != RS_OK) return s;
     if (hist_copy)
         RS_CUDA_TRY(cudaMemcpyAsync(hist_copy, L.hist + (size_t)first_pass * 256, 256 * 4, cudaMemcpyDeviceToDevice, st));
@@ -362,17 +326,7 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
     a.P = P;
     a.ctrl = L.ctrl;
     a.bases = L.bases;
-    a.status_base = L.status;
-    a.status_stride = L.status_bytes;
-    a.region_done = L.region_done;
-    a.reads_done = L.reads_done;
-    if (chain) {
-        a.pass = 0;
-        a.shift = 0;
-        s = launch_chain<K, V>(a, L.T, L.wide, st);
-        if (s != RS_OK) return s;
-    }
-    for (int t = 0; t < P && !chain; ++t) {
+    for (int t = 0; t < P; ++t) {
         a.pass = t;
         a.shift = 8 * t;
         a.status_cur = static_cast<char*>(L.status) + (size_t)(t & 1) * L.status_bytes;

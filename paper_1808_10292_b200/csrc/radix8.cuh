@@ -199,14 +199,6 @@ struct PassArgs {
     const uint32_t* bases;  // [P][256]
     void* status_cur;       // [T][256] status words, zero on entry
     void* status_next;      // [T][256], cleared here for the next pass
-    // chained launch (every active pass in one launch, onesweep_ar.cuh): the i-th
-    // active pass's status region at status_base + i * status_stride bytes, its
-    // output region counters at region_done + i * num_tiles, its reads-done
-    // counter at reads_done[i]; all zeroed by K1
-    void* status_base;
-    size_t status_stride;
-    uint32_t* region_done;
-    uint32_t* reads_done;
 };
 
 // ------------------------------------------------------------------ K4 ----

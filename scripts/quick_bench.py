@@ -15,7 +15,7 @@ import paper_1808_10292_b200 as rs  # noqa: E402
 L = rs.lib()
 PEAK = 6545.6
 ONE_PASS = os.environ.get("RS_ONE_PASS") == "1"
-for _opt in ("wide_status", "pass_design", "small_tiles", "chain"):
+for _opt in ("wide_status", "pass_design", "small_tiles"):
     if os.environ.get("RS_" + _opt.upper()):
         L.rs_dev_set_option(_opt.encode(), int(os.environ["RS_" + _opt.upper()]))
 
@@ -72,17 +72,13 @@ def run(log2n, kind="u32", b=8, dist="uniform", reps=5):
     gk = n / t / 1e6
     print(f"{kind} b={b} {dist} n={n}: {t:.3f} ms  {gk:.1f} Gkeys/s  "
           f"{per_key * n / t / 1e6:.0f} GB/s ({per_key * n / t / 1e6 / PEAK * 100:.1f}% of {PEAK})")
-    for name in ["hist", "plan", "onesweep_chain", "onesweep", "final_copy", "r16_count", "r16_total", "r16_scan", "r16_offsets",
+    for name in ["hist", "plan", "onesweep", "final_copy", "r16_count", "r16_total", "r16_scan", "r16_offsets",
                  "r16_scatter"]:
         ms, cnt = q(name)
         if cnt:
             avg = ms / cnt
             extra = ""
-            if name == "onesweep" and q("onesweep_chain")[1]:
-                continue  # (the prefix matches the chained launch too)
-            if name == "onesweep_chain":  # every pass in one launch: per pass = launch / passes
-                avg /= kb * 8 // b
-            if name.startswith("onesweep"):
+            if name == "onesweep":
                 bpk = {4: 8, 8: 16}[kb] + (8 if vb else 0)
                 extra = f"  pass {avg:.3f} ms -> {bpk * n / avg / 1e6:.0f} GB/s ({bpk * n / avg / 1e6 / PEAK * 100:.1f}%)"
             if name == "hist":

@@ -118,8 +118,6 @@ def test_dev_options_validation(L):
     assert L.rs_dev_set_option(b"gsd_merge", 4) == RS_EINVAL
     assert L.rs_dev_set_option(b"self_check", 1) == RS_OK
     assert L.rs_dev_set_option(b"self_check", 0) == RS_OK
-    assert L.rs_dev_get_option(b"chain", ctypes.byref(v)) == RS_OK and v.value == 1  # small inputs only
-    assert L.rs_dev_set_option(b"chain", 3) == RS_EINVAL
     assert L.rs_dev_get_option(b"nope", ctypes.byref(v)) == RS_EINVAL
 
 

@@ -443,55 +443,3 @@ def test_sort_graph_u32_and_pairs():
     torch.cuda.synchronize()
     wk, wv = oracle.sr(k2, 8, vals=v)
     assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
-
-
-@pytest.mark.parametrize("chain", [0, 2])
-@pytest.mark.parametrize("tiles", [1, 2])
-@pytest.mark.parametrize("dist", ["uniform", "mod16", "gauss", "sorted", "reversed", "equal", "half"])
-def test_chained_and_per_pass_launches(option, chain, tiles, dist):
-    """Design 5 with every active pass in ONE chained launch (tile t of pass i
-    waits for region t of pass i-1's output to be complete and for pass i-1 to
-    have read all its keys before overwriting them; onesweep_ar.cuh CH) and with
-    one launch per pass, large and small tiles, the c3 distributions (skipped
-    passes, few buckets, presorted runs): bit-exact against the oracle, u32 keys
-    in place and out of place, and stable pairs."""
-    option("chain", chain)
-    option("small_tiles", tiles)
-    n = 9 * TILE32 + 4097
-    a = inputs.gen_u32(n, 71, dist)
-    want = oracle.sr(a, 8)
-    assert (_sort_u32(a, 8) == want).all()
-    assert (_sort_u32(a, 8, inplace=False) == want).all()
-    k = inputs.gen_u64(3 * TILEP + 5, 72, "mod1024")
-    v = inputs.iota_u32(k.size)
-    tk, tv = dev(k), dev(v)
-    rs.sort_pairs(tk, tv)
-    wk, wv = oracle.sr(k, 8, vals=v)
-    assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
-
-
-@pytest.mark.parametrize("kind", ["u32", "pairs"])
-def test_chained_launch_wide_status_and_single_pass(option, kind):
-    """The chained launch with 64-bit look-back status words, and the one-digit
-    rounds PR4 runs (a single active pass: the launch's last pass needs no region
-    counts), every pass checked against the oracle's rounds."""
-    option("chain", 2)
-    option("wide_status", 1)
-    n = 4 * TILE32 + 333
-    if kind == "u32":
-        a = inputs.gen_u32(n, 73)
-        for t in range(1, 5):
-            got = host(rs.sort_bits(dev(a), end_bit=8 * t, digit_bits=8), np.uint32)
-            assert (got == oracle.sr(a, 8, rounds=t)).all(), t
-    else:
-        k = inputs.gen_u64(n, 74)
-        v = inputs.iota_u32(n)
-        for t in (1, 3, 8):
-            gk, gv = rs.sort_bits(dev(k), end_bit=8 * t, digit_bits=8, vals=dev(v))
-            wk, wv = oracle.sr(k, 8, rounds=t, vals=v)
-            assert (host(gk, np.uint64) == wk).all() and (host(gv, np.uint32) == wv).all(), t
-
-
-def test_chained_launch_default_is_small_inputs_only():
-    """The default (chain 1) chains the passes only in the small-tile regime."""
-    assert get_option("chain") == 1
