@@ -247,6 +247,31 @@ def test_31bit_lookback_prefixes():
 
 
 @pytest.mark.slow
+def test_maximum_n_wide_status():
+    """n = 2^32 - 1 u32 keys, the per-GPU maximum of the ABI (rsort.h: n < 2^32):
+    above 2^31 the look-back status words are u64 (radix8.cuh kNarrowStatusMaxN),
+    and the low byte of the first 5/8 of the keys is zeroed so pass 0's digit 0
+    holds > 2^31 keys — its inclusive prefixes need the 32nd bit, and every
+    32-bit position computation in the pass runs at its limit.  Checked by
+    sortedness, multiset hash and 64 sampled order statistics (full size)."""
+    n = (1 << 32) - 1
+    if free_host_gb() < 48 or free_dev_gb() < 40:
+        pytest.skip(f"needs ~48 GB host / 40 GB device (host {free_host_gb():.0f}, dev {free_dev_gb():.0f})")
+    a = inputs.gen_u32(n, 9)
+    a[: 5 * (n // 8)] &= np.uint32(0xFFFFFF00)
+    h_in = oracle.multiset_hash(a)
+    t = dev(a)
+    rs.sort(t, digit_bits=8)
+    got = host(t, np.uint32)
+    del t
+    torch.cuda.empty_cache()
+    assert oracle.is_nondecreasing(got)
+    assert oracle.multiset_hash(got) == h_in
+    pos = np.unique(np.linspace(0, n - 1, 64).astype(np.uint64))
+    assert oracle.check_order_stats_u32(a, pos, got[pos.astype(np.int64)]) == 0
+
+
+@pytest.mark.slow
 def test_config5_single_gpu_full_size():
     """BASELINE configs[4] at p=1: 2^30 (u64 key, u32 payload = index) pairs,
     seed 5, 8 radix-256 passes; stability via payload order."""
