@@ -9,9 +9,10 @@ reference leg may import this package.  The product path
 
 Parity status: SR-b, histograms and the GSD concatenated
 output are pinned (library sort, brute force, masked stable sort, bincount);
-GSD's per-rank partition is pinned only by the SPEC.md:290 hand trace and the
-balance bound — beyond those it is "parity unpinned" by the paper, which prints
-no partition.
+GSD's per-rank partition is pinned by two hand-derived traces (SPEC.md:290,
+p = 2; tests/golden/gsd_hand_trace_p3_r2.json, p = 3, r = 2 with duplicates
+within and across ranks) and the balance bound; the paper prints no partition,
+so beyond those traces it rests on DESIGN.md readings R10/R12/R14.
 """
 from __future__ import annotations
 

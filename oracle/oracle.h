@@ -20,9 +20,11 @@
  * Pins (tests/test_oracle.py, tests/test_oracle_gsd.py): library sort
  * (numpy/qsort), brute force over all short sequences on a 4-letter alphabet,
  * the stable-sort-by-masked-key identity for every intermediate round, bincount
- * for the histograms, the SPEC.md:290 GSD hand trace, and the balance bound
- * ⌊(1+1/r)·N_max⌋ (reading R18) by brute force.  Parity is unpinned
- * for GSD's per-rank partition beyond those.
+ * for the histograms, the SPEC.md:290 GSD hand trace, a hand-derived p = 3,
+ * r = 2 GSD trace with duplicates (tests/golden/gsd_hand_trace_p3_r2.json), and
+ * the balance bound ⌊(1+1/r)·N_max⌋ (reading R18) by brute force.
+ * The paper prints no partition: beyond those traces GSD's per-rank partition
+ * rests on DESIGN.md readings R10/R12/R14.
  */
 #ifndef RS_ORACLE_H
 #define RS_ORACLE_H
