@@ -1,5 +1,5 @@
-"""K1 (digit histogram) fixed cost: back-to-back launches timed with one event pair,
-per size (development aid).  python scripts/k1_probe.py"""
+"""K1 (digit histogram) timing: back-to-back calls timed with one event pair, per
+size (development aid).  python scripts/k1_probe.py 27 28:u64 ..."""
 import os
 import sys
 
@@ -8,9 +8,14 @@ import torch  # noqa: E402
 
 import paper_1808_10292_b200 as rs  # noqa: E402
 
-for lg in [int(x) for x in (sys.argv[1:] or [20, 22, 24, 26, 27, 28, 30])]:
+for arg in (sys.argv[1:] or ["20", "24", "26", "27", "28", "30"]):
+    lg, _, kind = arg.partition(":")
+    lg, kind = int(lg), kind or "u32"
     n = 1 << lg
-    keys = torch.randint(-2**31, 2**31 - 1, (n,), dtype=torch.int32, device="cuda")
+    dt, kb = (torch.int32, 4) if kind == "u32" else (torch.int64, 8)
+    keys = torch.randint(-2**31, 2**31 - 1, (n,), dtype=dt, device="cuda")
+    if kind == "u64":
+        keys = keys * 0x9E3779B97F4A7C15 + 12345
     for _ in range(3):
         rs.digit_histogram(keys)
     torch.cuda.synchronize()
@@ -22,5 +27,5 @@ for lg in [int(x) for x in (sys.argv[1:] or [20, 22, 24, 26, 27, 28, 30])]:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    print(f"n=2^{lg}: {ms * 1000:.1f} us per call  {4 * n / ms / 1e6:.0f} GB/s", flush=True)
+    print(f"{kind} n=2^{lg}: {ms * 1000:.1f} us per call  {kb * n / ms / 1e6:.0f} GB/s", flush=True)
     del keys

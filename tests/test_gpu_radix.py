@@ -16,7 +16,6 @@ from tests.gpu_util import dev, free_dev_gb, free_host_gb, host
 pytestmark = pytest.mark.gpu
 
 
-
 def _tile(kind):
     return rs.get_option(f"tile_{kind}")
 
@@ -55,6 +54,23 @@ def test_histogram_parity(b):
     k = inputs.gen_u64(2 * TILE64 + 77, 22)
     h = rs.digit_histogram(dev(k), b).cpu().numpy().view(np.uint32)
     assert (h.astype(np.uint64) == oracle.hist(k, b)).all()
+
+
+def test_histogram_u64_large_counts():
+    """K1 for u64 keys (8 passes, 16 lane-private 32-bit copies, radix8.cuh) at
+    2^29 + 3 keys: a constant top byte (pass 7: one bin holds every key, ~113 K
+    counts per copy per CTA), half the keys sharing byte 3, an odd tail; every
+    count against the oracle."""
+    n = (1 << 29) + 3
+    if free_host_gb() < 16 or free_dev_gb() < 16:
+        pytest.skip("needs ~16 GB host/device")
+    k = inputs.gen_u64(n, 25)
+    k &= np.uint64(0x00FFFFFFFFFFFFFF)
+    k[: n // 2] = (k[: n // 2] & np.uint64(0xFFFFFFFF00FFFFFF)) | np.uint64(0x5A000000)
+    h = rs.digit_histogram(dev(k), 8).cpu().numpy().view(np.uint32)
+    want = oracle.hist(k, 8)
+    assert want[7, 0] == n and want[3, 0x5A] > n // 2
+    assert (h.reshape(want.shape).astype(np.uint64) == want).all()
 
 
 @pytest.mark.parametrize("n", [3 * TILE32 + 1234, (1 << 20) + 7])
