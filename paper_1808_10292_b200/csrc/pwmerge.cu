@@ -51,7 +51,12 @@ namespace {
 constexpr int kPwM = RS_PW_M;  // sample stride m
 constexpr int kPwCMax = 32;     // samples per chunk c (PwRuns::c) at most
 constexpr int kPwMaxP = 32;   // runs handled by the single-pass merge (shared-memory tile)
-constexpr int kPwT = 256;     // threads per merge CTA
+// threads x samples per chunk, k_pw_merge at 2^28 outputs, p = 8 (scripts/gpu_pw_ab.sh, us):
+// 256 x 32 1101 (kept), 256 x 16 1375, 128 x 16 1206, 128 x 32 1400, 512 x 32 1500, 512 x 16 2343
+#ifndef RS_PW_T
+#define RS_PW_T 256
+#endif
+constexpr int kPwT = RS_PW_T;  // threads per merge CTA (warps 0..W-2 regular slots, the last warp the special ones)
 constexpr int kPwLevels = 5;  // ⌈log2 kPwMaxP⌉
 #ifndef RS_PW_SPECIAL
 #define RS_PW_SPECIAL 3
