@@ -308,6 +308,30 @@ def test_config5_single_gpu_full_size():
 
 
 @pytest.mark.slow
+def test_pairs_above_2p31_wide_status():
+    """(u64 key, u32 index) pairs with n = 2^31 + 7: the pairs pass with u64
+    look-back status words (n > 2^31), the top byte of 5/8 of the keys cleared so
+    pass 7's digit 0 holds > 2^31 pairs (inclusive prefixes past 31 bits).  The
+    payload is the input index, so nondecreasing keys + increasing payloads among
+    equal keys + the pair multiset hash pin the unique stable output."""
+    n = (1 << 31) + 7
+    if free_host_gb() < 64 or free_dev_gb() < 60:
+        pytest.skip(f"needs ~64 GB host / 60 GB device (host {free_host_gb():.0f}, dev {free_dev_gb():.0f})")
+    k = inputs.gen_u64(n, 27)
+    k[: 5 * (n // 8)] &= np.uint64(0x00FFFFFFFFFFFFFF)
+    v = inputs.iota_u32(n)
+    h_in = oracle.multiset_hash(k, v)
+    tk, tv = dev(k), dev(v)
+    del k, v
+    rs.sort_pairs(tk, tv, digit_bits=8)
+    gk, gv = host(tk, np.uint64), host(tv, np.uint32)
+    del tk, tv
+    torch.cuda.empty_cache()
+    assert oracle.pairs_stable(gk, gv)
+    assert oracle.multiset_hash(gk, gv) == h_in
+
+
+@pytest.mark.slow
 def test_config5_single_gpu_full_memcmp():
     """configs[4] at p = 1 compared element by element with the serial SR-8 oracle:
     2^30 (u64 key, u32 index) pairs, all 8 passes, keys and payloads."""
