@@ -151,11 +151,20 @@ template <typename K, bool V, typename S, bool SMALL>
 static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st) {
     using TN = typename std::conditional<SMALL, TuneArSmall<K, V>, TuneAr<K, V>>::type;
     using C = OnesweepArCfg<K, V, TN::THREADS, TN::KPT>;
-    // look-back window 8 (measured 2..64 on the small tiles, 4 and 16 on the large)
+    // look-back window: 8 for keys (measured 2..64 on the small tiles, 4 and 16 on the
+    // large), 4 for the pairs' large tiles (ms per pass at 2^26 / 2^28 / 2^30 pairs:
+    // window 1 0.416 / 1.635 / 6.49, 2 0.382 / 1.496 / 5.96, 3 0.375 / 1.461 / 5.85,
+    // 4 0.374 / 1.453 / 5.82, 6 0.378 / 1.472 / 5.84, 8 0.385 / 1.509 / 5.93,
+    // 16 - / 1.541 / -, 32 - / 1.594 / -): their 3.7x more tiles per key make every
+    // status row a window loads cost more than the deeper walk it saves
 #ifndef RS_AR_LB
 #define RS_AR_LB 8
 #endif
-    auto kern = k_onesweep_ar<K, V, TN::THREADS, TN::KPT, TN::MINB, S, Rank2<V>::value, SMALL ? 8 : RS_AR_LB>;
+#ifndef RS_AR_LB_P
+#define RS_AR_LB_P 4
+#endif
+    auto kern = k_onesweep_ar<K, V, TN::THREADS, TN::KPT, TN::MINB, S, Rank2<V>::value,
+                              SMALL ? 8 : (V ? RS_AR_LB_P : RS_AR_LB)>;
     int grid_cap = 0;
     rs_status_t s = kernel_setup(reinterpret_cast<const void*>(kern), C::THREADS, C::smem_bytes, &grid_cap);
     if (s != RS_OK) return s;
