@@ -151,8 +151,11 @@ template <typename K, bool V, typename S, bool SMALL>
 static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st) {
     using TN = typename std::conditional<SMALL, TuneArSmall<K, V>, TuneAr<K, V>>::type;
     using C = OnesweepArCfg<K, V, TN::THREADS, TN::KPT>;
-    // look-back window: 8 for keys (measured 2..64 on the small tiles, 4 and 16 on the
-    // large), 4 for the pairs' large tiles (ms per pass at 2^26 / 2^28 / 2^30 pairs:
+    // look-back window: 8 for keys (measured 2..64 on the small tiles; on the large, ms
+    // per pass at u32 2^26 / 2^27 / 2^31 and u64 2^28: window 2 0.157 / 0.293 / 4.404 /
+    // 0.966, 3 0.156 / 0.291 / 4.317 / 0.944, 4 0.156 / 0.290 / 4.292 / 0.937, 6 0.156 /
+    // 0.290 / 4.285-4.308 / 0.934, 8 0.156 / 0.290 / 4.291-4.298 / 0.935, 16 slower), 4
+    // for the pairs' large tiles (ms per pass at 2^26 / 2^28 / 2^30 pairs:
     // window 1 0.416 / 1.635 / 6.49, 2 0.382 / 1.496 / 5.96, 3 0.375 / 1.461 / 5.85,
     // 4 0.374 / 1.453 / 5.82, 6 0.378 / 1.472 / 5.84, 8 0.385 / 1.509 / 5.93,
     // 16 - / 1.541 / -, 32 - / 1.594 / -): their 3.7x more tiles per key make every
