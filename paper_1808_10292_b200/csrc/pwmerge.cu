@@ -223,16 +223,30 @@ __global__ void __launch_bounds__(kPwT) k_pw_merge(PwRuns R, const uint32_t* __r
             if (lane == 0) s_reg[L][0] = s_spc[L][0] = 0;
         }
     }
-    // stage the pieces: warp w copies pieces w, w + 8, ...; each lane keeps SB
-    // independent (remote) loads in flight before writing shared memory
+    // stage the pieces: with p >= 8 warps, warp w copies pieces w, w + 8, ...; with
+    // fewer pieces than warps, piece k is copied by warps k, k + p, ... together
+    // (p = 2: four warps per piece, not one warp walking 8 latency-bound batches);
+    // each lane keeps SB independent (remote) loads in flight before writing shared memory
     {
-        constexpr int SB = 8;
-        for (int k = warp; k < p; k += kPwT / 32) {
+// (k_pw_merge at c4 sizes, us: one warp per piece 3712 / 1744 / 1101 at p = 2 / 4 / 8;
+// grouped 2262 / 1552 / 1102; batches of SB = 12: 3025 / 1943 / 1215, SB = 16: 2351 / 1631 / 1087)
+#ifndef RS_PW_SB
+#define RS_PW_SB 8
+#endif
+        constexpr int SB = RS_PW_SB, NW = kPwT / 32;
+#ifdef RS_PW_STAGE_ONE_WARP
+        const bool grouped = false;  // (A/B: the round-2 one-warp-per-piece staging)
+#else
+        const bool grouped = p < NW;
+#endif
+        const int k0 = grouped ? warp % p : warp;
+        const int gi = grouped ? warp / p : 0, gn = grouped ? (NW - k0 + p - 1) / p : 1;
+        for (int k = k0; k < p; k += grouped ? p : NW) {
             const int s0 = (int)__shfl_sync(0xffffffffu, excl, k), ln = (int)__shfl_sync(0xffffffffu, len, k);
             const uint32_t off = __shfl_sync(0xffffffffu, c0, k);
             const K* src = static_cast<const K*>(R.k[k]) + off;
             const uint32_t* vs = V ? R.v[k] + off : nullptr;
-            for (int b = 0; b < ln; b += 32 * SB) {
+            for (int b = gi * 32 * SB; b < ln; b += gn * 32 * SB) {
                 K r[SB];
                 uint32_t rv[V ? SB : 1];
 #pragma unroll
