@@ -229,7 +229,9 @@ __global__ void __launch_bounds__(kPwT) k_pw_merge(PwRuns R, const uint32_t* __r
     // each lane keeps SB independent (remote) loads in flight before writing shared memory
     {
 // (k_pw_merge at c4 sizes, us: one warp per piece 3712 / 1744 / 1101 at p = 2 / 4 / 8;
-// grouped 2262 / 1552 / 1102; batches of SB = 12: 3025 / 1943 / 1215, SB = 16: 2351 / 1631 / 1087)
+// grouped 2262 / 1552 / 1102; batches of SB = 12: 3025 / 1943 / 1215, SB = 16: 2351 / 1631 / 1087;
+// 8 for grouped pieces and 16 for one warp per piece in one kernel: 2469 / 1655 / 1088, pairs
+// at 2^30: 3972 / 2782 / 1804 vs 3403 / 2767 / 1812 — the deeper path's registers cost every p)
 #ifndef RS_PW_SB
 #define RS_PW_SB 8
 #endif

@@ -2,7 +2,7 @@
 # usage: bash scripts/gpu_pw_ab.sh lib1.so lib2.so ...
 for so in "$@"; do
   RS_LIB_PATH=$PWD/$so timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_pw_merge -c 8 --csv \
-      python scripts/gsd_local_bench.py ${PW_LG:-31} ${PW_P:-8} gsd > gpurun_out/ab_$(basename $so).csv 2>&1
+      python scripts/gsd_local_bench.py ${PW_LG:-31} ${PW_P:-8} gsd ${PW_KIND:-u32} > gpurun_out/ab_$(basename $so).csv 2>&1
   python3 -c "
 import csv,sys
 rows=[r for r in csv.reader(open('gpurun_out/ab_$(basename $so).csv')) if len(r)>10]
