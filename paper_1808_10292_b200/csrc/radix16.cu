@@ -58,27 +58,37 @@ __global__ void __launch_bounds__(256) k16_total(const uint32_t* __restrict__ H,
 }
 
 // ------------------------------------------------------------------ C3 ----
+// One CTA: warp w owns digits [2048w, 2048w + 2048); pass 1 sums them with
+// coalesced loads (32 consecutive digits per instruction), the 32 warp totals are
+// scanned, pass 2 rescans the segment 32 digits at a time (warp inclusive scan +
+// running carry) and writes base coalesced.  (Was: thread t scanned digits
+// 64t..64t+63 serially, every load instruction touching 32 different lines: 77 us.)
 __global__ void __launch_bounds__(1024) k16_scan(const uint32_t* __restrict__ tot, uint32_t* __restrict__ base) {
     __shared__ uint32_t s_w[32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    constexpr int PER = kR16 / 1024;  // 64 consecutive digits per thread
-    uint32_t loc = 0;
-    for (int i = 0; i < PER; ++i) loc += tot[tid * PER + i];
-    uint32_t x = loc;
+    constexpr int SEG = kR16 / 32, ROUNDS = SEG / 32;
+    const uint32_t* t = tot + warp * SEG;
+    uint32_t sum = 0;
+#pragma unroll 16
+    for (int i = 0; i < ROUNDS; ++i) sum += t[32 * i + lane];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
-    }
-    if (lane == 31) s_w[warp] = x;
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) s_w[warp] = sum;
     __syncthreads();
-    uint32_t pre = 0;
-    for (int w = 0; w < warp; ++w) pre += s_w[w];
-    uint32_t run = pre + x - loc;
-    for (int i = 0; i < PER; ++i) {
-        const uint32_t t = tot[tid * PER + i];
-        base[tid * PER + i] = run;
-        run += t;
+    uint32_t carry = 0;
+    for (int w = 0; w < warp; ++w) carry += s_w[w];
+    uint32_t* bo = base + warp * SEG;
+#pragma unroll 8
+    for (int i = 0; i < ROUNDS; ++i) {
+        const uint32_t v = t[32 * i + lane];
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        bo[32 * i + lane] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
     }
 }
 
@@ -89,11 +99,18 @@ __global__ void __launch_bounds__(256) k16_offsets(uint32_t* __restrict__ H, int
                                                    uint32_t* __restrict__ big) {
     const int d = blockIdx.x * 256 + threadIdx.x;
     uint32_t run = base[d];
-    for (int g = 0; g < G; ++g) {
-        const uint32_t h = H[(size_t)g * kR16 + d];
-        H[(size_t)g * kR16 + d] = run;
-        run += h;
-        if (h >= 65536u) atomicOr(&big[g], 1u);
+    constexpr int B = 8;  // loads in flight per thread (the G-loop is latency-bound)
+    for (int g0 = 0; g0 < G; g0 += B) {
+        uint32_t h[B];
+#pragma unroll
+        for (int j = 0; j < B; ++j) h[j] = g0 + j < G ? H[(size_t)(g0 + j) * kR16 + d] : 0u;
+#pragma unroll
+        for (int j = 0; j < B; ++j) {
+            if (g0 + j >= G) break;
+            H[(size_t)(g0 + j) * kR16 + d] = run;
+            run += h[j];
+            if (h[j] >= 65536u) atomicOr(&big[g0 + j], 1u);
+        }
     }
 }
 
