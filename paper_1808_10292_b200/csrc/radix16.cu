@@ -193,8 +193,20 @@ struct Scatter16Smem {
     static constexpr size_t bytes = segs + 64 * 4;
 };
 
+// partitions per SM (> 1: the generic scatter, RS_R16_MINB CTAs per SM).  Measured (ms per
+// sort, u32 2^24 / u32 2^27 / pairs 2^24, b = 16): 1 partition per SM (fast path) 1.28 / 17.2
+// / 6.54; 2 per SM at 2 CTAs 1.95 / 18.5 / 6.01; 3 at 3 CTAs 2.69 / 20.7 / 6.41; 4 at 2 CTAs
+// 2.04 / 18.5 / 5.80 — the G x 65536 offset matrix grows with G (offsets kernel 17 -> 267 us
+// at G = 592) and the global running offsets cost more than the concurrency gains: the
+// paper's PR2 trade-off once more
+#ifndef RS_R16_GX
+#define RS_R16_GX 1
+#endif
+#ifndef RS_R16_MINB
+#define RS_R16_MINB 1
+#endif
 template <typename K, bool V>
-__global__ void __launch_bounds__(kS16Threads, 1)
+__global__ void __launch_bounds__(kS16Threads, RS_R16_MINB)
     k16_scatter(const K* __restrict__ src, K* __restrict__ dst, const uint32_t* __restrict__ vsrc,
                 uint32_t* __restrict__ vdst, size_t n, int shift, size_t part_keys, uint32_t* __restrict__ O) {
     using S = Scatter16Smem<K, V>;
@@ -416,7 +428,7 @@ static Layout16 layout16(void* ws, int key_bytes, bool has_val, size_t n) {
 #ifdef RS_R16_G
     L.G = std::min<size_t>((size_t)RS_R16_G, (size_t)sm_count());  // bounded-frontier experiment
 #else
-    L.G = (size_t)sm_count();
+    L.G = (size_t)sm_count() * RS_R16_GX;
 #endif
     L.part = (n + L.G - 1) / L.G;
     L.part = std::max<size_t>(1, (L.part + kS16Chunk - 1) / kS16Chunk * kS16Chunk);
@@ -477,7 +489,7 @@ static rs_status_t sort16(const K* in, const uint32_t* vin, size_t n, int end_bi
         }
         {
             LaunchScope ls("r16_scatter", st);
-            if (std::is_same<K, uint32_t>::value && !V)
+            if (std::is_same<K, uint32_t>::value && !V && RS_R16_GX == 1)
                 k16_scatter_fast<<<(unsigned)L.G, kS16Threads, Scatter16FastSmem::bytes, st>>>(
                     reinterpret_cast<const uint32_t*>(src), reinterpret_cast<uint32_t*>(dst), n, shift, L.part, L.H,
                     L.big);
