@@ -246,7 +246,8 @@ static rs_status_t rank_order_ok(Ctrl* ctrl, cudaStream_t st, bool* ok) {
     }
     std::lock_guard<std::mutex> run(g_probe_run_mu);
     if (cached()) return RS_OK;  // another thread probed this device meanwhile
-    uint32_t* bad = reinterpret_cast<uint32_t*>(&ctrl->pad[0]);  // zeroed with the control block
+    uint32_t* bad = reinterpret_cast<uint32_t*>(&ctrl->pad[0]);
+    RS_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(uint32_t), st));
     rs_status_t s = launch_probe<TuneAr<uint32_t, false>>(0x9E3779B9u, bad, st);
     if (s == RS_OK) s = launch_probe<TuneArSmall<uint32_t, false>>(0x7F4A7C15u, bad, st);
     if (s != RS_OK) return s;
@@ -308,7 +309,6 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
                          uint32_t* hist_copy = nullptr) {
     const int P = (end_bit + 7) / 8;
     Ctrl* ctrl = static_cast<Ctrl*>(ws);  // first carve of every layout
-    RS_CUDA_TRY(cudaMemsetAsync(ctrl, 0, sizeof(Ctrl), st));
     int design = options().pass_design;
     if (design == 5 && P > 0) {
         bool ar_ok = false;
@@ -317,7 +317,10 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
         if (!ar_ok) design = 2;
     }
     const Layout8 L = layout8(ws, sizeof(K), V, n, (size_t)tile_for(sizeof(K), V, design, n));
-    RS_CUDA_TRY(cudaMemsetAsync(L.hist, 0, (size_t)P * 256 * 4, st));
+    // the control block and the histograms are adjacent carves: one memset for both
+    // (one launch fewer per sort; 2^20 keys: see DESIGN.md §7)
+    RS_CUDA_TRY(cudaMemsetAsync(ctrl, 0, (size_t)(reinterpret_cast<char*>(L.hist + (size_t)P * 256) -
+                                                   reinterpret_cast<char*>(ctrl)), st));
     // K1 also zeroes the first pass's status region (as u32 words)
     rs_status_t s = launch_hist<K>(keys_in, n, P, L.hist, static_cast<uint32_t*>(L.status), L.status_bytes / 4, st,
                                    first_pass);
