@@ -380,7 +380,12 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
 
         // ---- [store] bucket runs leave as coalesced bursts (batches of 4 loads, 4
         // offset lookups, 4 stores: u32 2^27 pass 0.336 -> 0.326 ms against 8)
-        constexpr int SG = KPT % 4 == 0 ? 4 : 2;
+// pairs: 2 per batch (ms per pass at 2^26 / 2^28 / 2^30 pairs: 1 0.372 / 1.468 / 5.85, 2 0.371 /
+// 1.446 / 5.84, 4 0.374 / 1.454 / 5.88, 6 0.377 / 1.472 / 5.92, 8 0.382 / 1.493 / 6.01)
+#ifndef RS_AR_SGP
+#define RS_AR_SGP 2
+#endif
+        constexpr int SG = HAS_VAL ? (KPT % RS_AR_SGP == 0 ? RS_AR_SGP : 2) : (KPT % 4 == 0 ? 4 : 2);
         if (LPC && valid == (uint32_t)TILE) {
             const int sb = warp * WK + lane;     // warp w: slots [w·WK, (w+1)·WK)
             uint32_t cd = 0xFFFFFFFFu, cg = 0;  // cached digit and its bucket offset
