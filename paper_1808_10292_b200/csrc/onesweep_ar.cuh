@@ -385,7 +385,12 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
 #ifndef RS_AR_SGP
 #define RS_AR_SGP 2
 #endif
-        constexpr int SG = HAS_VAL ? (KPT % RS_AR_SGP == 0 ? RS_AR_SGP : 2) : (KPT % 4 == 0 ? 4 : 2);
+// keys: 4 (ms per pass at u32 2^26 / 2^27 / 2^31 and u64 2^28: 2 0.165 / 0.307 / 4.53 / 0.939,
+// 4 0.156 / 0.290 / 4.29 / 0.935, 8 0.159 / 0.294 / 4.38 / 0.945)
+#ifndef RS_AR_SGK
+#define RS_AR_SGK 4
+#endif
+        constexpr int SG = HAS_VAL ? (KPT % RS_AR_SGP == 0 ? RS_AR_SGP : 2) : (KPT % RS_AR_SGK == 0 ? RS_AR_SGK : 2);
         if (LPC && valid == (uint32_t)TILE) {
             const int sb = warp * WK + lane;     // warp w: slots [w·WK, (w+1)·WK)
             uint32_t cd = 0xFFFFFFFFu, cg = 0;  // cached digit and its bucket offset
