@@ -45,7 +45,8 @@ template <>
 struct TuneAr<uint64_t, false> : TuneT<256, 40, 2> {};
 // pairs re-swept at look-back window 4 (ms per pass at 2^26 / 2^28 / 2^30 pairs): 256x24
 // 0.374 / 1.453 / 5.82 (kept); 256x32 0.426 / 1.682 / 6.58 (window 3: 0.420 / 1.640 / 6.40);
-// 256x16 0.430 / 1.718 / 6.83; rank batches of 12 flat; scatter batches of 12 0.376 / 1.461 / 5.84
+// 256x16 0.430 / 1.718 / 6.83; rank batches of 12 flat; scatter batches of 12 0.376 / 1.461 / 5.84;
+// rank batches of 4 / 6 and scatter batches of 4 / 6 within +-0.6 % (mixed across sizes): 8 stays
 #ifndef RS_AR_P_T
 #define RS_AR_P_T 256
 #endif
