@@ -50,9 +50,27 @@ __global__ void __launch_bounds__(256) k_pull_pieces(const Piece* __restrict__ p
         if (pc.dst >= b1) break;
         const uint64_t s0 = max(pc.dst, b0), s1 = min(pc.dst + pc.len, b1);
         const K* sk = static_cast<const K*>(pc.src_k);
-        for (uint64_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
-            dk[i] = sk[i - pc.dst];
-            if (dv) dv[i] = pc.src_v[i - pc.dst];
+        // 4 independent loads in flight per thread (one per iteration was latency-bound)
+        constexpr int U = 4;
+        for (uint64_t i = s0 + threadIdx.x; i < s1; i += (uint64_t)U * blockDim.x) {
+            K r[U];
+            uint32_t rv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t j = i + (uint64_t)u * blockDim.x;
+                if (j < s1) {
+                    r[u] = sk[j - pc.dst];
+                    if (dv) rv[u] = pc.src_v[j - pc.dst];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint64_t j = i + (uint64_t)u * blockDim.x;
+                if (j < s1) {
+                    dk[j] = r[u];
+                    if (dv) dv[j] = rv[u];
+                }
+            }
         }
     }
 }
