@@ -1,8 +1,49 @@
 // Device helpers shared by the rsort kernels (sm_100a): PTX wrappers for
 // relaxed GPU-scope status words, mbarrier + 1-D bulk (TMA engine) copies, lane masks.
 #pragma once
+
+// programmatic dependent launch along the radix-256 sort's kernel chain K1 -> K2 ->
+// K3 x P -> K4 (0 = plain launches).  Each kernel of the chain waits (pdl_wait) before
+// its first global access, so a launch may be scheduled while its predecessor drains;
+// the wait returns once the predecessor grid has completed and its writes are visible.
+#ifndef RS_PDL
+#define RS_PDL 1
+#endif
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <utility>
+
+namespace rs {
+__device__ __forceinline__ void pdl_wait() {
+#if RS_PDL
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+// lets the next kernel of the chain launch; issued only by grids whose CTAs are all
+// resident at once (persistent or one wave), so a waiting dependent never holds a
+// slot one of this grid's CTAs still needs
+__device__ __forceinline__ void pdl_trigger() {
+#if RS_PDL
+    asm volatile("griddepcontrol.launch_dependents;" :::);
+#endif
+}
+// launch with the programmatic-serialisation attribute when pdl (and RS_PDL) is set
+template <typename... KP, typename... A>
+inline cudaError_t launch_chain(bool pdl, void (*kern)(KP...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                A&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = (RS_PDL && pdl) ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+}
+}  // namespace rs
 
 // Checked builds (-DRS_CHECKED, tests only): bounds asserts on computed store
 // indices (compute-sanitizer is not available on the GPU pool).

@@ -111,6 +111,11 @@ __global__ void __launch_bounds__(RT, MINB) k_onesweep_ar(PassArgs a) {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     Ctrl* ctrl = a.ctrl;
     S* const status = static_cast<S*>(a.status_cur);
+    // PDL (common.cuh): every global access below (the tile counter, the plan, the
+    // status rows the previous pass used, its output) comes after the wait; the
+    // persistent grid is resident before any CTA triggers the next kernel
+    pdl_wait();
+    pdl_trigger();
 
     // small tiles (about one tile per CTA): the first tile id and the pass plan are
     // fetched together, two global round trips in flight at once (2^20 keys: 14.5 ->

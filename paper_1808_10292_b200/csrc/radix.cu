@@ -152,7 +152,7 @@ size_t local_ws_bytes(int key_bytes, bool has_val, size_t n, int b) {
 }
 
 template <typename K, bool V, typename S, bool SMALL>
-static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st) {
+static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st, bool pdl) {
     using TN = typename std::conditional<SMALL, TuneArSmall<K, V>, TuneAr<K, V>>::type;
     using C = OnesweepArCfg<K, V, TN::THREADS, TN::KPT>;
     // look-back window: 8 for keys (measured 2..64 on the small tiles; on the large, ms
@@ -177,7 +177,8 @@ static rs_status_t launch_pass_ar(const PassArgs& a, size_t T, cudaStream_t st) 
     if (s != RS_OK) return s;
     const unsigned grid = (unsigned)std::min<size_t>(T, (size_t)grid_cap);  // persistent CTAs
     LaunchScope ls("onesweep", st);
-    kern<<<grid, C::THREADS, C::smem_bytes, st>>>(a);
+    // the previous kernel in the stream is K2 or the previous pass (sort8)
+    RS_CUDA_TRY(launch_chain(pdl, kern, dim3(grid), dim3(C::THREADS), C::smem_bytes, st, a));
     return RS_OK;
 }
 
@@ -263,14 +264,14 @@ static rs_status_t rank_order_ok(Ctrl* ctrl, cudaStream_t st, bool* ok) {
 }
 
 template <typename K, bool V>
-static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStream_t st, int design) {
+static rs_status_t launch_pass(const PassArgs& a, size_t T, bool wide, cudaStream_t st, int design, bool pdl) {
     if (design == 2) {
         if (wide) return launch_pass_ec<K, V, uint64_t>(a, T, st);
         return launch_pass_ec<K, V, uint32_t>(a, T, st);
     }
     const bool small = small_input<K, V>(a.n);  // must match tile_keys()
-    if (wide) return small ? launch_pass_ar<K, V, uint64_t, true>(a, T, st) : launch_pass_ar<K, V, uint64_t, false>(a, T, st);
-    return small ? launch_pass_ar<K, V, uint32_t, true>(a, T, st) : launch_pass_ar<K, V, uint32_t, false>(a, T, st);
+    if (wide) return small ? launch_pass_ar<K, V, uint64_t, true>(a, T, st, pdl) : launch_pass_ar<K, V, uint64_t, false>(a, T, st, pdl);
+    return small ? launch_pass_ar<K, V, uint32_t, true>(a, T, st, pdl) : launch_pass_ar<K, V, uint32_t, false>(a, T, st, pdl);
 }
 
 template <typename K, int C, int P>
@@ -304,6 +305,8 @@ static rs_status_t launch_hist(const K* keys, size_t n, int P, uint32_t* hist, u
     }
 }
 
+constexpr size_t kPdlMaxKeys = (size_t)1 << 24;
+
 template <typename K, bool V>
 static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, int end_bit, K* out,
                          uint32_t* vout, void* ws, cudaStream_t st, int first_pass = 0,
@@ -318,6 +321,11 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
         if (!ar_ok) design = 2;
     }
     const Layout8 L = layout8(ws, sizeof(K), V, n, (size_t)tile_for(sizeof(K), V, design, n));
+    // programmatic dependent launches along K2 -> K3 x P -> K4 (common.cuh) where they
+    // were measured to pay: u32 keys up to 2^24 (ms per sort without / with, one B200:
+    // 2^20 0.074-0.080 / 0.064-0.066, 2^22 0.121-0.126 / 0.112-0.113, 2^24 0.248 /
+    // 0.235; 2^26 to 2^31 equal within noise; u64 keys at 2^24 0.635-0.640 / 0.658-0.660)
+    const bool pdl = sizeof(K) == 4 && !V && design == 5 && n <= kPdlMaxKeys;
     // the control block and the histograms are adjacent carves: one memset for both
     // (one launch fewer per sort; 2^20 keys: see DESIGN.md §7)
     RS_CUDA_TRY(cudaMemsetAsync(ctrl, 0, (size_t)(reinterpret_cast<char*>(L.hist + (size_t)P * 256) -
@@ -330,8 +338,9 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
         RS_CUDA_TRY(cudaMemcpyAsync(hist_copy, L.hist + (size_t)first_pass * 256, 256 * 4, cudaMemcpyDeviceToDevice, st));
     {
         LaunchScope ls("plan", st);
-        k_plan<<<1, 256, 0, st>>>(L.hist, (uint32_t)n, P, L.bases, L.ctrl,
-                                  (const void*)keys_in == (const void*)out ? 1 : 0, first_pass);
+        RS_CUDA_TRY(launch_chain(pdl && hist_copy == nullptr, k_plan, dim3(1), dim3(256), 0, st, (const uint32_t*)L.hist,
+                                 (uint32_t)n, P, L.bases, L.ctrl,
+                                 (const void*)keys_in == (const void*)out ? 1 : 0, first_pass));
     }
     PassArgs a{};
     a.keys_in = keys_in;
@@ -350,14 +359,15 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
         a.shift = 8 * t;
         a.status_cur = static_cast<char*>(L.status) + (size_t)(t & 1) * L.status_bytes;
         a.status_next = static_cast<char*>(L.status) + (size_t)((t + 1) & 1) * L.status_bytes;
-        s = launch_pass<K, V>(a, L.T, L.wide, st, design);
+        s = launch_pass<K, V>(a, L.T, L.wide, st, design, pdl);
         if (s != RS_OK) return s;
     }
     {
         LaunchScope ls("final_copy", st);
         const unsigned grid = (unsigned)std::min<size_t>((n + 4095) / 4096 + 1, (size_t)sm_count() * 8);
-        k_final_copy<K><<<grid, 256, 0, st>>>(L.ctrl, keys_in, static_cast<const K*>(L.alt_keys), out, vals_in,
-                                              L.alt_vals, V ? vout : nullptr, n);
+        RS_CUDA_TRY(launch_chain(pdl, k_final_copy<K>, dim3(grid), dim3(256), 0, st, (const Ctrl*)L.ctrl,
+                                 keys_in, static_cast<const K*>(L.alt_keys), out, vals_in,
+                                 (const uint32_t*)L.alt_vals, V ? vout : (uint32_t*)nullptr, n));
     }
     RS_CUDA_TRY(cudaGetLastError());
     return RS_OK;

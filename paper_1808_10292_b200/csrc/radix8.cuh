@@ -111,6 +111,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_digit_hist_lp(const K* __restric
                                                              uint32_t* __restrict__ zero_ptr, size_t zero_words,
                                                              int shift0 = 0) {
     extern __shared__ __align__(16) uint32_t s_hist_lp[];
+    pdl_trigger();  // one CTA per SM: K2's single CTA may wait beside it
     digit_hist_lp_body<K, THREADS, C, P>(keys, n, hist, zero_ptr, zero_words, shift0, s_hist_lp);
 }
 
@@ -174,6 +175,8 @@ __device__ __forceinline__ void plan_body(const uint32_t* __restrict__ hist, uin
 __global__ void __launch_bounds__(256) k_plan(const uint32_t* __restrict__ hist, uint32_t n, int P,
                                               uint32_t* __restrict__ bases, Ctrl* __restrict__ ctrl,
                                               int inplace, int first = 0) {
+    pdl_wait();
+    pdl_trigger();
     plan_body(hist, n, P, bases, ctrl, inplace, first);
 }
 
@@ -228,6 +231,7 @@ __device__ __forceinline__ void final_copy_body(const Ctrl* __restrict__ ctrl, c
 template <typename K>
 __global__ void k_final_copy(const Ctrl* __restrict__ ctrl, const K* in, const K* alt, K* out,
                              const uint32_t* vin, const uint32_t* valt, uint32_t* vout, size_t n) {
+    pdl_wait();
     final_copy_body<K>(ctrl, in, alt, out, vin, valt, vout, n);
 }
 
