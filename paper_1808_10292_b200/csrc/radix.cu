@@ -325,7 +325,8 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
     // were measured to pay: u32 keys up to 2^24 (ms per sort without / with, one B200:
     // 2^20 0.074-0.080 / 0.064-0.066, 2^22 0.121-0.126 / 0.112-0.113, 2^24 0.248 /
     // 0.235; 2^26 to 2^31 equal within noise; u64 keys at 2^24 0.635-0.640 / 0.658-0.660)
-    const bool pdl = sizeof(K) == 4 && !V && design == 5 && n <= kPdlMaxKeys;
+    const int pdl_opt = options().pdl;
+    const bool pdl = design == 5 && pdl_opt != 1 && (pdl_opt == 2 || (sizeof(K) == 4 && !V && n <= kPdlMaxKeys));
     // the control block and the histograms are adjacent carves: one memset for both
     // (one launch fewer per sort; 2^20 keys: see DESIGN.md §7)
     RS_CUDA_TRY(cudaMemsetAsync(ctrl, 0, (size_t)(reinterpret_cast<char*>(L.hist + (size_t)P * 256) -

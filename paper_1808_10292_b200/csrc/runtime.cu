@@ -160,6 +160,7 @@ rs_status_t rs_dev_set_option(const char* name, long long value) {
     else if (n == "small_tiles" && value <= 2) o.small_tiles = (int)value;
     else if (n == "pass_design" && (value == 2 || value == 5)) o.pass_design = (int)value;
     else if (n == "self_check" && value <= 1) o.self_check = (int)value;
+    else if (n == "pdl" && value <= 2) o.pdl = (int)value;
     else return fail(RS_EINVAL, "rs_dev_set_option: unknown option or value: " + n);
     return RS_OK;
 }
@@ -174,6 +175,7 @@ rs_status_t rs_dev_get_option(const char* name, long long* value) {
     else if (n == "small_tiles") *value = o.small_tiles;
     else if (n == "pass_design") *value = o.pass_design;
     else if (n == "self_check") *value = o.self_check;
+    else if (n == "pdl") *value = o.pdl;
     else if (n == "rank_probe") *value = rank_probe_state();
     else if (n == "tile_u32") *value = tile_keys_for(4, false);
     else if (n == "tile_u64") *value = tile_keys_for(8, false);

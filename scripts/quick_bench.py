@@ -15,7 +15,7 @@ import paper_1808_10292_b200 as rs  # noqa: E402
 L = rs.lib()
 PEAK = 6545.6
 ONE_PASS = os.environ.get("RS_ONE_PASS") == "1"
-for _opt in ("wide_status", "pass_design", "small_tiles"):
+for _opt in ("wide_status", "pass_design", "small_tiles", "pdl"):
     if os.environ.get("RS_" + _opt.upper()):
         L.rs_dev_set_option(_opt.encode(), int(os.environ["RS_" + _opt.upper()]))
 

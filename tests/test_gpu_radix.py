@@ -508,3 +508,31 @@ def test_sort_graph_u32_and_pairs():
     torch.cuda.synchronize()
     wk, wv = oracle.sr(k2, 8, vals=v)
     assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all()
+
+
+@pytest.mark.parametrize("pdl", [1, 2])
+@pytest.mark.parametrize("tiles", [1, 2])
+def test_programmatic_dependent_launch_on_and_off(option, pdl, tiles):
+    """The radix-256 kernel chain K2 -> K3 x P -> K4 with programmatic dependent
+    launches forced on for every key type (pdl 2; by default only u32 keys up to
+    2^24) and forced off (pdl 1): bit-exact against the oracle at ragged
+    multi-tile sizes, with skipped passes (mod16, equal keys: the active-pass
+    parity decides whether K4 copies) and in place / out of place."""
+    option("pdl", pdl)
+    option("small_tiles", tiles)
+    for n in (1, TILE32 - 1, 3 * TILE32 + 5, (1 << 20) + 3, (1 << 22) + 7):
+        for dist in ("uniform", "mod16", "equal"):
+            a = inputs.gen_u32(n, 211 + n, dist)
+            want = oracle.sr(a, 8)
+            assert (_sort_u32(a, 8) == want).all(), (n, dist)
+            assert (_sort_u32(a, 8, inplace=False) == want).all(), (n, dist)
+    for n in (TILEP + 1, (1 << 20) + 5):
+        k = inputs.gen_u64(n, 212 + n, "mod1024")
+        v = inputs.iota_u32(n)
+        tk, tv = dev(k), dev(v)
+        rs.sort_pairs(tk, tv)
+        wk, wv = oracle.sr(k, 8, vals=v)
+        assert (host(tk, np.uint64) == wk).all() and (host(tv, np.uint32) == wv).all(), n
+        t = dev(k)
+        rs.sort(t)
+        assert (host(t, np.uint64) == wk).all(), n
