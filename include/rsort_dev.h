@@ -95,7 +95,7 @@ rs_status_t rs_ipc_close_all(void);
  *   "wide_status"  1 = 64-bit look-back status words at any n (tests that path).
  *   "small_tiles"  design-5 tiles: 0 auto, 1 always large, 2 always small.
  *   "pdl"          programmatic dependent launches along the radix-256 kernel chain:
- *                  0 auto (u32 keys without values, n <= 2^24), 1 never, 2 always.
+ *                  0 auto (n <= 2^25 u32 keys, 2^24 pairs, 2^22 u64 keys), 1 never, 2 always.
  *   "gsd_merge"    GSD step 5 (all give the same Y_j): 3 = one p-way pass
  *                  (default), 2 = tree of 2-way merges, 1 = stable radix
  *                  re-sort (after an all-to-all), 0 = tree after an all-to-all.

@@ -305,7 +305,7 @@ static rs_status_t launch_hist(const K* keys, size_t n, int P, uint32_t* hist, u
     }
 }
 
-constexpr size_t kPdlMaxKeys = (size_t)1 << 24;
+constexpr size_t kPdlMaxKeys32 = (size_t)1 << 25, kPdlMaxPairs = (size_t)1 << 24, kPdlMaxKeys64 = (size_t)1 << 22;
 
 template <typename K, bool V>
 static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, int end_bit, K* out,
@@ -322,11 +322,15 @@ static rs_status_t sort8(const K* keys_in, const uint32_t* vals_in, size_t n, in
     }
     const Layout8 L = layout8(ws, sizeof(K), V, n, (size_t)tile_for(sizeof(K), V, design, n));
     // programmatic dependent launches along K2 -> K3 x P -> K4 (common.cuh) where they
-    // were measured to pay: u32 keys up to 2^24 (ms per sort without / with, one B200:
-    // 2^20 0.074-0.080 / 0.064-0.066, 2^22 0.121-0.126 / 0.112-0.113, 2^24 0.248 /
-    // 0.235; 2^26 to 2^31 equal within noise; u64 keys at 2^24 0.635-0.640 / 0.658-0.660)
+    // were measured to pay (ms per sort never / always, rs_dev_set_option("pdl"), two
+    // interleaved reps on one B200, scripts/gpu_pdl_types.sh): u32 keys 2^20 0.073-0.075
+    // / 0.063-0.064, 2^22 0.126 / 0.113, 2^24 0.248-0.250 / 0.236-0.239, 2^25 0.403-0.404
+    // / 0.396-0.397, 2^26..2^31 equal within noise; pairs 2^20 0.154 / 0.145-0.146, 2^22
+    // 0.301 / 0.288-0.289, 2^24 0.908-0.909 / 0.888-0.892, 2^28 equal; u64 keys 2^20 0.150
+    // / 0.127-0.128, 2^22 0.305-0.306 / 0.285, but 2^24 0.632 / 0.659-0.660 (slower)
+    const size_t pdl_max = sizeof(K) == 4 ? kPdlMaxKeys32 : (V ? kPdlMaxPairs : kPdlMaxKeys64);
     const int pdl_opt = options().pdl;
-    const bool pdl = design == 5 && pdl_opt != 1 && (pdl_opt == 2 || (sizeof(K) == 4 && !V && n <= kPdlMaxKeys));
+    const bool pdl = design == 5 && pdl_opt != 1 && (pdl_opt == 2 || n <= pdl_max);
     // the control block and the histograms are adjacent carves: one memset for both
     // (one launch fewer per sort; 2^20 keys: see DESIGN.md §7)
     RS_CUDA_TRY(cudaMemsetAsync(ctrl, 0, (size_t)(reinterpret_cast<char*>(L.hist + (size_t)P * 256) -

@@ -58,7 +58,7 @@ struct Options {
     std::atomic<int> small_tiles{0};   // design 5 small-input tiles: 0 auto, 1 never, 2 always
     std::atomic<int> pass_design{5};   // 5 atomic ranks (if the lane-order probe passes, else 2); 2 ballots
     std::atomic<int> self_check{0};    // 1: verify every local sort's output on the device (debug)
-    std::atomic<int> pdl{0};           // programmatic dependent launches: 0 auto (radix.cu kPdlMaxKeys), 1 never, 2 always
+    std::atomic<int> pdl{0};           // programmatic dependent launches: 0 auto (radix.cu kPdlMax*), 1 never, 2 always
 };
 // per (kernel, device): set the kernel's dynamic shared-memory limit to `smem` once
 // and return its persistent grid (resident CTAs per SM at `threads` x SMs)
